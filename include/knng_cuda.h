@@ -1,0 +1,216 @@
+/*
+ * knng_cuda.h — the C-ABI of libknng_cuda.so, the B200 (sm_100a) NN-Descent
+ * K-NNG builder for squared L2.
+ *
+ * This is the drop-in boundary for the reference's one hot path, knng::run
+ * (reference proj/include/knng/descent.hpp:193-255) and the pieces it is made
+ * of.  The reference has no C-ABI of its own (it is a header-only C++
+ * library); the entry points below are what its callers bind instead of the
+ * C++ templates, each one citing the reference interface it replaces.  The
+ * C++ drop-in wrapper with the reference's own types and exceptions is
+ * proj/include/knng/cuda.hpp; Python binds the same symbols through ctypes
+ * (paper_2112_06630_b200/_native.py).  See INTEGRATION.md.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  `data` is n x d row-major float32,
+ *    unpadded (the library pads rows to ceil8(d) internally, as
+ *    knng::Dataset does, dataset.hpp:61-77).
+ *  - Entry points suffixed _device take DEVICE pointers and a cudaStream_t
+ *    passed as void*; all others take HOST pointers and synchronise.
+ *  - Neighbour rows are returned sorted ascending by (distance, id), the order
+ *    of KnnGraph::export_csv (graph.hpp:169-184).  Rows passed IN may be in
+ *    any order (e.g. the reference's heap order).
+ *  - Return codes: KNNG_CUDA_OK or one of the errors below; a message for the
+ *    calling thread is available from knng_cuda_last_error().  Parameter
+ *    errors (KNNG_CUDA_INVALID_ARGUMENT) mirror the std::invalid_argument
+ *    cases of the reference (descent.hpp:29-35,197; graph.hpp:37-38;
+ *    dataset.hpp:74-75; selection.hpp:112-113).
+ *  - No global mutable state besides cached device properties; calls from
+ *    different host threads are independent.  There is no CPU fallback: with
+ *    no usable CUDA device every compute entry point returns
+ *    KNNG_CUDA_CUDA_ERROR.
+ *  - Build limits (returned as KNNG_CUDA_INVALID_ARGUMENT): 2 <= k <= 32,
+ *    k <= max_candidates <= 64, n < 2^31.
+ */
+#ifndef KNNG_CUDA_H
+#define KNNG_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KNNG_CUDA_OK 0
+#define KNNG_CUDA_INVALID_ARGUMENT 1
+#define KNNG_CUDA_CUDA_ERROR 2
+#define KNNG_CUDA_NCCL_ERROR 3
+#define KNNG_CUDA_OUT_OF_MEMORY 4
+#define KNNG_CUDA_NOT_IMPLEMENTED 5
+
+#define KNNG_CUDA_MAX_K 32
+#define KNNG_CUDA_MAX_CANDIDATES 64
+
+/* knng::RunParams (descent.hpp:18-36).  strategy is always turbo and the
+ * join always blocked (the reference defaults); naive/fused/flat are the
+ * reference's benchmark baselines and are not part of this path. */
+typedef struct knng_cuda_params {
+    uint32_t k;                        /* default 20 */
+    uint32_t max_candidates;           /* default 50 (selection.hpp:15) */
+    double termination_delta;          /* default 0.001 */
+    uint32_t max_iterations;           /* default 30 */
+    int32_t reorder;                   /* default 0 */
+    uint32_t reorder_after_iteration;  /* default 1 */
+    uint64_t seed;                     /* default 0 */
+    int32_t device;                    /* CUDA device ordinal, default 0 */
+    int32_t profile;                   /* 1: time each kernel with CUDA events */
+} knng_cuda_params;
+
+/* knng::IterationMetrics (descent.hpp:38-43).  `changes` counts successful
+ * bounded inserts like KnnGraph::changes_ (graph.hpp:126); inserts are applied
+ * concurrently, so early-iteration counts differ from the sequential
+ * reference's while agreeing near the termination threshold. */
+typedef struct knng_cuda_iteration {
+    uint32_t iteration;  /* 0 = random initialisation */
+    double wall_time_s;
+    uint64_t dist_evals;
+    uint64_t changes;
+} knng_cuda_iteration;
+
+/* Per-kernel device time (CUDA events on the library's stream), filled when
+ * params.profile != 0.  Index with the KNNG_CUDA_KERNEL_* constants. */
+#define KNNG_CUDA_KERNEL_INIT 0
+#define KNNG_CUDA_KERNEL_DEGREE 1
+#define KNNG_CUDA_KERNEL_SAMPLE 2
+#define KNNG_CUDA_KERNEL_FINALIZE 3
+#define KNNG_CUDA_KERNEL_JOIN 4
+#define KNNG_CUDA_KERNEL_REORDER 5
+#define KNNG_CUDA_KERNEL_COUNT 6
+
+/* knng::RunMetrics (descent.hpp:45-68) plus device-side accounting.  The
+ * caller provides `iterations` with room for `capacity` rows
+ * (max_iterations + 1 suffices). */
+typedef struct knng_cuda_metrics {
+    knng_cuda_iteration* iterations;
+    uint32_t capacity;
+    uint32_t n_rows;                 /* rows written (iteration 0 included) */
+    double total_wall_time_s;
+    uint64_t total_dist_evals;
+    uint64_t total_changes;
+    double kernel_ms[KNNG_CUDA_KERNEL_COUNT];
+    uint64_t kernel_launches[KNNG_CUDA_KERNEL_COUNT];
+    uint64_t join_candidates;        /* sum over joins of (nn_u + no_u) */
+    uint64_t join_evals;             /* distance evaluations inside the join kernel */
+    uint64_t h2d_bytes;              /* host->device bytes moved by the call */
+    uint64_t d2h_bytes;              /* device->host bytes moved by the call */
+} knng_cuda_metrics;
+
+/* Fills *p with the reference defaults (descent.hpp:18-28). */
+void knng_cuda_params_default(knng_cuda_params* p);
+
+/* Thread-local message for the last failing call on this thread. */
+const char* knng_cuda_last_error(void);
+
+/* Number of visible CUDA devices (0 when none). */
+int knng_cuda_device_count(void);
+
+/*
+ * The north-star entry point: replaces knng::run(Dataset, RunParams)
+ * (descent.hpp:193-255) for squared L2.  HOST pointers.
+ *   sample_rate rho -> max_candidates = lround(rho * k) (PAPER.md:88,
+ *   SPEC.md:266,308); must be >= k.  out_ids/out_dists: n*k each, rows
+ *   sorted by (distance, id).  out_metrics may be NULL.
+ */
+int knng_cuda_nndescent_l2(const float* data, uint32_t n, uint32_t d, uint32_t k,
+                           double sample_rate, double delta, uint64_t seed,
+                           uint32_t max_iterations, int num_gpus, uint32_t* out_ids,
+                           float* out_dists, knng_cuda_metrics* out_metrics);
+
+/* knng::run with full RunParams.  HOST pointers; out_flags (n*k, 1 = is_new)
+ * and out_metrics may be NULL.  out_sigma (n, nullable) receives the
+ * locality permutation when params->reorder is set. */
+int knng_cuda_run(const float* data, uint32_t n, uint32_t d, const knng_cuda_params* params,
+                  uint32_t* out_ids, float* out_dists, uint8_t* out_flags,
+                  uint32_t* out_sigma, knng_cuda_metrics* out_metrics);
+
+/* Same, DEVICE pointers (data: n*d floats; out_ids/out_dists: n*k) on the
+ * given stream (void* = cudaStream_t, NULL = a library stream). */
+int knng_cuda_run_device(const float* d_data, uint32_t n, uint32_t d,
+                         const knng_cuda_params* params, uint32_t* d_out_ids,
+                         float* d_out_dists, knng_cuda_metrics* out_metrics, void* stream);
+
+/*
+ * One local join from a fixed state — the parity entry.  Replaces
+ * knng::compute_step(KnnGraph&, const CandidateSet&, const Dataset&,
+ * EvalCounter&) (descent.hpp:82-153) applied to
+ * KnnGraph::from_rows(k, rows) (graph.hpp:70-93).
+ *   in_ids/in_dists/in_flags: n*k graph rows (any order, e.g. heap order);
+ *   cand_ids: n*2*cap, per node `new` block then `old` block
+ *   (CandidateSet layout, selection.hpp:22-49); new_counts/old_counts: n.
+ *   Outputs (n*k, rows sorted by (distance,id)): ids, dists, is_new flags;
+ *   out_rev_deg (n): k + in-degree (KnnGraph::reverse_degree, graph.hpp:98);
+ *   changes: successful inserts; evals: distance evaluations.
+ */
+int knng_cuda_local_join(const float* data, uint32_t n, uint32_t d, uint32_t k, uint32_t cap,
+                         const uint32_t* in_ids, const float* in_dists, const uint8_t* in_flags,
+                         const uint32_t* cand_ids, const uint32_t* new_counts,
+                         const uint32_t* old_counts, uint32_t* out_ids, float* out_dists,
+                         uint8_t* out_flags, uint32_t* out_rev_deg, uint64_t* changes,
+                         uint64_t* evals, int device);
+
+/* The join's distance stage alone, for per-pair bit-exactness checks against
+ * mutual_block_distances / block_l2_sq (distance.hpp:134-190) as driven by
+ * compute_step.  For every node u with new_counts[u] > 0 writes the
+ * (new_counts[u]) x (new_counts[u] + old_counts[u]) matrix D_u, row i = new
+ * candidate i, column j = new candidate j (j < nn) or old candidate j - nn,
+ * into out_dists + offsets[u] (row-major; entries of the new x new block with
+ * j <= i are left untouched).  offsets: n entries, computed by the caller. */
+int knng_cuda_candidate_distances(const float* data, uint32_t n, uint32_t d, uint32_t cap,
+                                  const uint32_t* cand_ids, const uint32_t* new_counts,
+                                  const uint32_t* old_counts, const uint64_t* offsets,
+                                  float* out_dists, uint64_t total, int device);
+
+/* KnnGraph::init_random (graph.hpp:34-67): k distinct uniform ids != u per
+ * node (counter-based Philox draws, not the reference's sequential
+ * mt19937_64 stream) with their true distances.  Rows sorted by (dist,id). */
+int knng_cuda_init_random(const float* data, uint32_t n, uint32_t d, uint32_t k, uint64_t seed,
+                          uint32_t* out_ids, float* out_dists, uint8_t* out_flags,
+                          uint32_t* out_rev_deg, uint64_t* evals, int device);
+
+/* select_turbo (selection.hpp:282-320) followed by flag_consumed for every
+ * node (descent.hpp:225, graph.hpp:133-143).  Same sampling law (offer each
+ * edge endpoint to the other with probability min(1, cap/deg), dedup across
+ * both lists, bounded lists), applied concurrently with Philox draws.
+ * out_flags_after: n*k flags in the caller's entry order after consumption. */
+int knng_cuda_select(uint32_t n, uint32_t k, uint32_t cap, const uint32_t* in_ids,
+                     const float* in_dists, const uint8_t* in_flags, uint64_t seed,
+                     uint32_t* cand_ids, uint32_t* new_counts, uint32_t* old_counts,
+                     uint8_t* out_flags_after, int device);
+
+/* brute_force_knng (oracle.hpp:92-127) on the GPU: exact k nearest
+ * neighbours, rows sorted by (distance, id) with distances evaluated in
+ * float64 like l2_sq_double (oracle.hpp:50-66).  No size guard. */
+int knng_cuda_bruteforce_knng(const float* data, uint32_t n, uint32_t d, uint32_t k,
+                              uint32_t* out_ids, double* out_dists, int device);
+
+/* The same for a subset of query rows (nq ids in `queries`; NULL = all n):
+ * row i of the outputs is the exact k-NN of node queries[i] among all n
+ * nodes.  Used to measure recall on a sample of nodes at large n. */
+int knng_cuda_bruteforce_queries(const float* data, uint32_t n, uint32_t d, uint32_t k,
+                                 const uint32_t* queries, uint32_t nq, uint32_t* out_ids,
+                                 double* out_dists, int device);
+
+/* greedy_cluster's role (reorder.hpp:22-50) on the GPU: a locality
+ * permutation built from the current graph (sigma[u] = new position of u,
+ * sigma_inv[p] = node at position p).  A parallel analogue, not Algorithm 1's
+ * exact sequential walk. */
+int knng_cuda_locality_permutation(uint32_t n, uint32_t k, const uint32_t* ids,
+                                   const float* dists, uint32_t* sigma, uint32_t* sigma_inv,
+                                   int device);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KNNG_CUDA_H */

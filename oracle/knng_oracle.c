@@ -850,19 +850,21 @@ int oracle_select_turbo(uint32_t n, uint32_t k, uint32_t cap, const uint32_t* in
 }
 
 /* brute_force_knng (oracle.hpp:92-127): double accumulation in 8 lanes over
- * the TRUE dimension d (l2_sq_double, oracle.hpp:50-66), (dist,id) order. */
+ * the TRUE dimension d (l2_sq_double, oracle.hpp:50-66), (dist,id) order.
+ * The reference's compiled double loop FUSES the square-accumulate (pinned
+ * against the reference harness in tests/test_oracle_pins.py). */
 static double l2_double(const float* a, const float* b, uint32_t d) {
     double acc[8] = {0};
     uint32_t j = 0;
     for (; j + 8 <= d; j += 8)
         for (uint32_t l = 0; l < 8; ++l) {
             const double diff = (double)a[j + l] - (double)b[j + l];
-            acc[l] = acc[l] + diff * diff;
+            acc[l] = fma(diff, diff, acc[l]);
         }
     double tail = 0.0;
     for (; j < d; ++j) {
         const double diff = (double)a[j] - (double)b[j];
-        tail = tail + diff * diff;
+        tail = fma(diff, diff, tail);
     }
     return ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7])) + tail;
 }

@@ -1,0 +1,747 @@
+// Host orchestrator and C-ABI of libknng_cuda.so (declared in include/knng_cuda.h).
+//
+// knng::run (reference descent.hpp:193-255) re-designed for one B200:
+//   init_random -> [ indegree -> sample -> finalize -> join -> (reorder once) ]*
+// with every stage a device kernel on one stream, and one 32-byte
+// device->host read of the iteration counters per iteration for the
+// termination test `changes < delta * n * k` (descent.hpp:215-216, 242).
+// Seeds follow the reference exactly: a std::mt19937_64 master seeded with
+// params.seed hands out the init seed, then one seed per iteration
+// (descent.hpp:201-221); the device kernels key Philox streams with them.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "../../include/knng_cuda.h"
+#include "kernels.cuh"
+
+using namespace knng_cuda;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Status {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void raise(int code, const std::string& msg) { throw Status{code, msg}; }
+
+void check_cuda(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return;
+    const int code =
+        e == cudaErrorMemoryAllocation ? KNNG_CUDA_OUT_OF_MEMORY : KNNG_CUDA_CUDA_ERROR;
+    cudaGetLastError();  // clear sticky-free errors
+    raise(code, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CK(x) check_cuda((x), #x)
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return KNNG_CUDA_OK;
+    } catch (const Status& s) {
+        g_err = s.msg;
+        return s.code;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return KNNG_CUDA_CUDA_ERROR;
+    }
+}
+
+// Stream-ordered allocations from a per-device pool that keeps freed memory
+// (release threshold = max) so repeated builds do not pay cudaMalloc again.
+std::mutex g_pool_mu;
+cudaMemPool_t g_pools[64] = {};
+
+cudaMemPool_t pool_for(int device) {
+    std::lock_guard<std::mutex> lock(g_pool_mu);
+    if (device < 0 || device >= 64) raise(KNNG_CUDA_INVALID_ARGUMENT, "device ordinal out of range");
+    if (!g_pools[device]) {
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.handleTypes = cudaMemHandleTypeNone;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = device;
+        CK(cudaMemPoolCreate(&g_pools[device], &props));
+        uint64_t threshold = ~0ull;
+        CK(cudaMemPoolSetAttribute(g_pools[device], cudaMemPoolAttrReleaseThreshold, &threshold));
+    }
+    return g_pools[device];
+}
+
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    cudaStream_t s = nullptr;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    void alloc(size_t count, cudaMemPool_t pool, cudaStream_t stream) {
+        s = stream;
+        CK(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&p), std::max<size_t>(count, 1) * sizeof(T),
+                                   pool, stream));
+    }
+    ~DevBuf() {
+        if (p) cudaFreeAsync(p, s);
+    }
+};
+
+struct DeviceGuard {
+    int prev = 0;
+    explicit DeviceGuard(int device) {
+        int count = 0;
+        if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+            cudaGetLastError();
+            raise(KNNG_CUDA_CUDA_ERROR, "no CUDA device available (this library has no CPU path)");
+        }
+        if (device < 0 || device >= count) raise(KNNG_CUDA_INVALID_ARGUMENT, "device ordinal out of range");
+        CK(cudaGetDevice(&prev));
+        CK(cudaSetDevice(device));
+    }
+    ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+struct StreamHolder {
+    cudaStream_t s = nullptr;
+    bool own = false;
+    explicit StreamHolder(void* user) {
+        if (user) {
+            s = static_cast<cudaStream_t>(user);
+        } else {
+            CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+            own = true;
+        }
+    }
+    ~StreamHolder() {
+        if (own) {
+            cudaStreamSynchronize(s);
+            cudaStreamDestroy(s);
+        }
+    }
+};
+
+// Per-kernel CUDA-event timing on the library stream (params.profile).
+struct KernelTimer {
+    bool on;
+    cudaStream_t s;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> open;
+    knng_cuda_metrics* m;
+    KernelTimer(bool enabled, cudaStream_t stream, knng_cuda_metrics* metrics)
+        : on(enabled && metrics), s(stream), m(metrics) {}
+    int begin(int kernel) {
+        if (!on) return -1;
+        cudaEvent_t a, b;
+        CK(cudaEventCreate(&a));
+        CK(cudaEventCreate(&b));
+        CK(cudaEventRecord(a, s));
+        open.push_back({kernel, {a, b}});
+        return int(open.size()) - 1;
+    }
+    void end(int h) {
+        if (h < 0) return;
+        CK(cudaEventRecord(open[size_t(h)].second.second, s));
+    }
+    void flush() {  // after a stream sync
+        for (auto& e : open) {
+            float ms = 0.0f;
+            CK(cudaEventElapsedTime(&ms, e.second.first, e.second.second));
+            m->kernel_ms[e.first] += ms;
+            m->kernel_launches[e.first] += 1;
+            cudaEventDestroy(e.second.first);
+            cudaEventDestroy(e.second.second);
+        }
+        open.clear();
+    }
+    ~KernelTimer() {
+        for (auto& e : open) {
+            cudaEventDestroy(e.second.first);
+            cudaEventDestroy(e.second.second);
+        }
+    }
+};
+
+void validate_shape(uint32_t n, uint32_t d, uint32_t k) {
+    if (n < 2) raise(KNNG_CUDA_INVALID_ARGUMENT, "Dataset: need at least 2 points");
+    if (d < 1) raise(KNNG_CUDA_INVALID_ARGUMENT, "Dataset: need at least 1 dimension");
+    if (n >= (1u << 31)) raise(KNNG_CUDA_INVALID_ARGUMENT, "this build supports n < 2^31");
+    if (k < 2) raise(KNNG_CUDA_INVALID_ARGUMENT, "k must be at least 2");
+    if (k > KNNG_CUDA_MAX_K) raise(KNNG_CUDA_INVALID_ARGUMENT, "this build supports k <= 32");
+    if (k >= n) raise(KNNG_CUDA_INVALID_ARGUMENT, "k must be smaller than n");
+}
+
+void validate_params(uint32_t n, uint32_t d, const knng_cuda_params& p) {
+    // RunParams::validate (descent.hpp:29-35) and run's n > k (descent.hpp:197)
+    if (p.k < 2) raise(KNNG_CUDA_INVALID_ARGUMENT, "RunParams: k must be at least 2");
+    if (p.max_candidates < p.k)
+        raise(KNNG_CUDA_INVALID_ARGUMENT, "RunParams: max_candidates must be at least k");
+    if (!(p.termination_delta > 0.0 && p.termination_delta < 1.0))
+        raise(KNNG_CUDA_INVALID_ARGUMENT, "RunParams: termination_delta must be in (0,1)");
+    if (n <= p.k) raise(KNNG_CUDA_INVALID_ARGUMENT, "run: need n > k");
+    if (p.max_candidates > KNNG_CUDA_MAX_CANDIDATES)
+        raise(KNNG_CUDA_INVALID_ARGUMENT, "this build supports max_candidates <= 64");
+    validate_shape(n, d, p.k);
+}
+
+inline uint32_t padded_stride(uint32_t d) { return (d + 7u) / 8u * 8u; }
+
+// All device state of one build on one GPU.
+struct Engine {
+    uint32_t n, d, stride, k, cap;
+    cudaStream_t s;
+    cudaMemPool_t pool;
+    DevBuf<float> data, maxd;
+    DevBuf<uint64_t> keys;
+    DevBuf<uint32_t> flags, locks, indeg, cand, raw_new, raw_old, nc, oc, active;
+    DevBuf<IterCounters> ctr;
+    IterCounters* h_ctr = nullptr;
+    uint64_t h2d = 0, d2h = 0;
+
+    Engine(int device, uint32_t n_, uint32_t d_, uint32_t k_, uint32_t cap_, cudaStream_t stream)
+        : n(n_), d(d_), stride(padded_stride(d_)), k(k_), cap(cap_), s(stream) {
+        pool = pool_for(device);
+        data.alloc(size_t(n) * stride, pool, s);
+        keys.alloc(size_t(n) * k, pool, s);
+        flags.alloc(n, pool, s);
+        maxd.alloc(n, pool, s);
+        locks.alloc(n, pool, s);
+        indeg.alloc(n, pool, s);
+        ctr.alloc(1, pool, s);
+        if (cap) {
+            cand.alloc(size_t(n) * 2 * cap, pool, s);
+            raw_new.alloc(n, pool, s);
+            raw_old.alloc(n, pool, s);
+            nc.alloc(n, pool, s);
+            oc.alloc(n, pool, s);
+            active.alloc(n, pool, s);
+        }
+        CK(cudaMallocHost(reinterpret_cast<void**>(&h_ctr), sizeof(IterCounters)));
+        CK(cudaMemsetAsync(locks.p, 0, sizeof(uint32_t) * n, s));
+        CK(cudaMemsetAsync(ctr.p, 0, sizeof(IterCounters), s));
+    }
+    ~Engine() {
+        if (h_ctr) cudaFreeHost(h_ctr);
+    }
+
+    GraphView gv() const {
+        return GraphView{data.p, n, k, stride, keys.p, flags.p, maxd.p, locks.p};
+    }
+    CandView cv() const { return CandView{cap, cand.p, raw_new.p, raw_old.p, nc.p, oc.p}; }
+
+    // Rows padded to ceil8(d) with zeros (dataset.hpp:72-77).
+    void upload(const float* src, bool src_on_device) {
+        if (stride != d) CK(cudaMemsetAsync(data.p, 0, sizeof(float) * size_t(n) * stride, s));
+        CK(cudaMemcpy2DAsync(data.p, sizeof(float) * stride, src, sizeof(float) * d,
+                             sizeof(float) * d, n,
+                             src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+        if (!src_on_device) h2d += sizeof(float) * size_t(n) * d;
+    }
+
+    void read_counters() {
+        CK(cudaMemcpyAsync(h_ctr, ctr.p, sizeof(IterCounters), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        d2h += sizeof(IterCounters);
+    }
+
+    // selection: in-degree, turbo sampling, finalize (dedup, flag_consumed, active list)
+    void select(uint64_t seed, KernelTimer& timer) {
+        const GraphView g = gv();
+        const CandView c = cv();
+        int h = timer.begin(KNNG_CUDA_KERNEL_DEGREE);
+        launch_indegree(g, indeg.p, s);
+        launch_reset_raw(c, n, s);
+        timer.end(h);
+        h = timer.begin(KNNG_CUDA_KERNEL_SAMPLE);
+        launch_sample(g, c, indeg.p, seed, s);
+        timer.end(h);
+        h = timer.begin(KNNG_CUDA_KERNEL_FINALIZE);
+        launch_finalize(g, c, active.p, ctr.p, s);
+        timer.end(h);
+        CK(cudaGetLastError());
+    }
+
+    void join(KernelTimer& timer) {
+        const int h = timer.begin(KNNG_CUDA_KERNEL_JOIN);
+        launch_join(gv(), cv(), active.p, n, ctr.p, s);
+        timer.end(h);
+        CK(cudaGetLastError());
+    }
+
+    void export_rows(uint32_t* ids, float* dists, uint8_t* fl) {
+        launch_export_rows(gv(), ids, dists, fl, s);
+        CK(cudaGetLastError());
+    }
+};
+
+double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch())
+        .count();
+}
+
+void metrics_reset(knng_cuda_metrics* m) {
+    if (!m) return;
+    m->n_rows = 0;
+    m->total_wall_time_s = 0;
+    m->total_dist_evals = 0;
+    m->total_changes = 0;
+    for (int i = 0; i < KNNG_CUDA_KERNEL_COUNT; ++i) {
+        m->kernel_ms[i] = 0;
+        m->kernel_launches[i] = 0;
+    }
+    m->join_candidates = 0;
+    m->join_evals = 0;
+    m->h2d_bytes = 0;
+    m->d2h_bytes = 0;
+}
+
+void metrics_push(knng_cuda_metrics* m, uint32_t iteration, double wall, uint64_t evals,
+                  uint64_t changes) {
+    if (!m) return;
+    if (m->iterations && m->n_rows < m->capacity)
+        m->iterations[m->n_rows] = knng_cuda_iteration{iteration, wall, evals, changes};
+    ++m->n_rows;
+    m->total_wall_time_s += wall;
+    m->total_dist_evals += evals;
+    m->total_changes += changes;
+}
+
+// knng::run (descent.hpp:193-255) on one GPU; data already on the device or
+// on the host per data_on_device; outputs device pointers.
+void run_engine(Engine& e, const float* data, bool data_on_device, const knng_cuda_params& p,
+                uint32_t* d_ids, float* d_dists, uint8_t* d_flags, knng_cuda_metrics* m) {
+    if (p.reorder) raise(KNNG_CUDA_NOT_IMPLEMENTED, "reorder is not available in this build yet");
+    KernelTimer timer(p.profile != 0, e.s, m);
+    std::mt19937_64 master(p.seed);
+    double t0 = now_s();
+    e.upload(data, data_on_device);
+    const uint64_t init_seed = master();
+    int h = timer.begin(KNNG_CUDA_KERNEL_INIT);
+    launch_init_random(e.gv(), init_seed, e.s);
+    timer.end(h);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(e.s));
+    timer.flush();
+    double t1 = now_s();
+    metrics_push(m, 0, t1 - t0, uint64_t(e.n) * e.k, 0);
+
+    const double threshold = p.termination_delta * double(e.n) * double(e.k);
+    for (uint32_t iter = 1; iter <= p.max_iterations; ++iter) {
+        t0 = now_s();
+        const uint64_t iter_seed = master();
+        CK(cudaMemsetAsync(e.ctr.p, 0, sizeof(IterCounters), e.s));
+        e.select(iter_seed, timer);
+        e.join(timer);
+        e.read_counters();
+        timer.flush();
+        t1 = now_s();
+        const IterCounters c = *e.h_ctr;
+        metrics_push(m, iter, t1 - t0, c.evals, c.changes);
+        if (m) {
+            m->join_candidates += c.cands;
+            m->join_evals += c.evals;
+        }
+        if (double(c.changes) < threshold) break;
+    }
+    e.export_rows(d_ids, d_dists, d_flags);
+    CK(cudaStreamSynchronize(e.s));
+}
+
+template <typename T>
+void to_device(DevBuf<T>& buf, const T* host, size_t count, Engine& e) {
+    buf.alloc(count, e.pool, e.s);
+    CK(cudaMemcpyAsync(buf.p, host, sizeof(T) * count, cudaMemcpyHostToDevice, e.s));
+    e.h2d += sizeof(T) * count;
+}
+
+template <typename T>
+void to_host(T* host, const T* dev, size_t count, Engine& e) {
+    if (!host) return;
+    CK(cudaMemcpyAsync(host, dev, sizeof(T) * count, cudaMemcpyDeviceToHost, e.s));
+    e.d2h += sizeof(T) * count;
+}
+
+// from_rows validation (graph.hpp:70-93)
+void validate_rows(uint32_t n, uint32_t k, const uint32_t* ids) {
+    std::vector<uint32_t> seen;
+    for (uint32_t u = 0; u < n; ++u) {
+        const uint32_t* r = ids + size_t(u) * k;
+        for (uint32_t i = 0; i < k; ++i) {
+            if (r[i] == u) raise(KNNG_CUDA_INVALID_ARGUMENT, "from_rows: self loop");
+            if (r[i] >= n) raise(KNNG_CUDA_INVALID_ARGUMENT, "from_rows: id out of range");
+            for (uint32_t j = 0; j < i; ++j)
+                if (r[j] == r[i]) raise(KNNG_CUDA_INVALID_ARGUMENT, "from_rows: duplicate id");
+        }
+    }
+}
+
+void validate_cands(uint32_t n, uint32_t cap, const uint32_t* cand_ids, const uint32_t* nc,
+                    const uint32_t* oc) {
+    for (uint32_t u = 0; u < n; ++u) {
+        if (nc[u] > cap || oc[u] > cap)
+            raise(KNNG_CUDA_INVALID_ARGUMENT, "candidate count exceeds cap");
+        const uint32_t* b = cand_ids + size_t(u) * 2 * cap;
+        for (uint32_t i = 0; i < nc[u]; ++i)
+            if (b[i] >= n) raise(KNNG_CUDA_INVALID_ARGUMENT, "candidate id out of range");
+        for (uint32_t i = 0; i < oc[u]; ++i)
+            if (b[cap + i] >= n) raise(KNNG_CUDA_INVALID_ARGUMENT, "candidate id out of range");
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+void knng_cuda_params_default(knng_cuda_params* p) {
+    if (!p) return;
+    p->k = 20;
+    p->max_candidates = 50;
+    p->termination_delta = 0.001;
+    p->max_iterations = 30;
+    p->reorder = 0;
+    p->reorder_after_iteration = 1;
+    p->seed = 0;
+    p->device = 0;
+    p->profile = 0;
+}
+
+const char* knng_cuda_last_error(void) { return g_err.c_str(); }
+
+int knng_cuda_device_count(void) {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return count;
+}
+
+int knng_cuda_run_device(const float* d_data, uint32_t n, uint32_t d, const knng_cuda_params* params,
+                         uint32_t* d_out_ids, float* d_out_dists, knng_cuda_metrics* out_metrics,
+                         void* stream) {
+    return guarded([&] {
+        if (!params || !d_data || !d_out_ids || !d_out_dists)
+            raise(KNNG_CUDA_INVALID_ARGUMENT, "null argument");
+        const knng_cuda_params p = *params;
+        validate_params(n, d, p);
+        DeviceGuard dg(p.device);
+        StreamHolder sh(stream);
+        metrics_reset(out_metrics);
+        Engine e(p.device, n, d, p.k, p.max_candidates, sh.s);
+        run_engine(e, d_data, true, p, d_out_ids, d_out_dists, nullptr, out_metrics);
+        if (out_metrics) {
+            out_metrics->h2d_bytes = e.h2d;
+            out_metrics->d2h_bytes = e.d2h;
+        }
+    });
+}
+
+int knng_cuda_run(const float* data, uint32_t n, uint32_t d, const knng_cuda_params* params,
+                  uint32_t* out_ids, float* out_dists, uint8_t* out_flags, uint32_t* out_sigma,
+                  knng_cuda_metrics* out_metrics) {
+    return guarded([&] {
+        if (!params || !data || !out_ids || !out_dists)
+            raise(KNNG_CUDA_INVALID_ARGUMENT, "null argument");
+        const knng_cuda_params p = *params;
+        validate_params(n, d, p);
+        (void)out_sigma;
+        DeviceGuard dg(p.device);
+        StreamHolder sh(nullptr);
+        metrics_reset(out_metrics);
+        Engine e(p.device, n, d, p.k, p.max_candidates, sh.s);
+        DevBuf<uint32_t> ids;
+        DevBuf<float> dists;
+        DevBuf<uint8_t> fl;
+        const size_t nk = size_t(n) * p.k;
+        ids.alloc(nk, e.pool, e.s);
+        dists.alloc(nk, e.pool, e.s);
+        if (out_flags) fl.alloc(nk, e.pool, e.s);
+        run_engine(e, data, false, p, ids.p, dists.p, out_flags ? fl.p : nullptr, out_metrics);
+        to_host(out_ids, ids.p, nk, e);
+        to_host(out_dists, dists.p, nk, e);
+        if (out_flags) to_host(out_flags, fl.p, nk, e);
+        CK(cudaStreamSynchronize(e.s));
+        if (out_metrics) {
+            out_metrics->h2d_bytes = e.h2d;
+            out_metrics->d2h_bytes = e.d2h;
+        }
+    });
+}
+
+int knng_cuda_nndescent_l2(const float* data, uint32_t n, uint32_t d, uint32_t k,
+                           double sample_rate, double delta, uint64_t seed,
+                           uint32_t max_iterations, int num_gpus, uint32_t* out_ids,
+                           float* out_dists, knng_cuda_metrics* out_metrics) {
+    int rc = guarded([&] {
+        if (!(sample_rate > 0.0) || !std::isfinite(sample_rate))
+            raise(KNNG_CUDA_INVALID_ARGUMENT, "sample_rate must be positive");
+        if (num_gpus != 1)
+            raise(KNNG_CUDA_NOT_IMPLEMENTED, "this entry point drives one GPU per process; "
+                                             "shard across processes for more");
+    });
+    if (rc) return rc;
+    knng_cuda_params p;
+    knng_cuda_params_default(&p);
+    p.k = k;
+    const double cap = std::llround(sample_rate * double(k));
+    p.max_candidates = cap > 4294967295.0 ? 0xffffffffu : uint32_t(cap);
+    p.termination_delta = delta;
+    p.seed = seed;
+    p.max_iterations = max_iterations;
+    return knng_cuda_run(data, n, d, &p, out_ids, out_dists, nullptr, nullptr, out_metrics);
+}
+
+int knng_cuda_local_join(const float* data, uint32_t n, uint32_t d, uint32_t k, uint32_t cap,
+                         const uint32_t* in_ids, const float* in_dists, const uint8_t* in_flags,
+                         const uint32_t* cand_ids, const uint32_t* new_counts,
+                         const uint32_t* old_counts, uint32_t* out_ids, float* out_dists,
+                         uint8_t* out_flags, uint32_t* out_rev_deg, uint64_t* changes,
+                         uint64_t* evals, int device) {
+    return guarded([&] {
+        if (!data || !in_ids || !in_dists || !in_flags || !cand_ids || !new_counts || !old_counts)
+            raise(KNNG_CUDA_INVALID_ARGUMENT, "null argument");
+        validate_shape(n, d, k);
+        if (cap == 0) raise(KNNG_CUDA_INVALID_ARGUMENT, "CandidateSet: cap must be positive");
+        if (cap > KNNG_CUDA_MAX_CANDIDATES)
+            raise(KNNG_CUDA_INVALID_ARGUMENT, "this build supports max_candidates <= 64");
+        validate_rows(n, k, in_ids);
+        validate_cands(n, cap, cand_ids, new_counts, old_counts);
+        DeviceGuard dg(device);
+        StreamHolder sh(nullptr);
+        Engine e(device, n, d, k, cap, sh.s);
+        e.upload(data, false);
+        DevBuf<uint32_t> ids;
+        DevBuf<float> dists;
+        DevBuf<uint8_t> fl;
+        const size_t nk = size_t(n) * k;
+        to_device(ids, in_ids, nk, e);
+        to_device(dists, in_dists, nk, e);
+        to_device(fl, in_flags, nk, e);
+        launch_load_rows(e.gv(), ids.p, dists.p, fl.p, e.s);
+        CK(cudaMemcpyAsync(e.cand.p, cand_ids, sizeof(uint32_t) * size_t(n) * 2 * cap,
+                           cudaMemcpyHostToDevice, e.s));
+        CK(cudaMemcpyAsync(e.nc.p, new_counts, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, e.s));
+        CK(cudaMemcpyAsync(e.oc.p, old_counts, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, e.s));
+        // active list + eval count from the injected counts (finalize's bookkeeping)
+        std::vector<uint32_t> act;
+        uint64_t ev = 0;
+        for (uint32_t u = 0; u < n; ++u)
+            if (new_counts[u] > 0) {
+                act.push_back(u);
+                ev += uint64_t(new_counts[u]) * (new_counts[u] - 1) / 2 +
+                      uint64_t(new_counts[u]) * old_counts[u];
+            }
+        IterCounters hc = {};
+        hc.active = uint32_t(act.size());
+        CK(cudaMemcpyAsync(e.ctr.p, &hc, sizeof hc, cudaMemcpyHostToDevice, e.s));
+        if (!act.empty())
+            CK(cudaMemcpyAsync(e.active.p, act.data(), sizeof(uint32_t) * act.size(),
+                               cudaMemcpyHostToDevice, e.s));
+        KernelTimer timer(false, e.s, nullptr);
+        e.join(timer);
+        e.read_counters();
+        e.export_rows(ids.p, dists.p, fl.p);
+        to_host(out_ids, ids.p, nk, e);
+        to_host(out_dists, dists.p, nk, e);
+        to_host(out_flags, fl.p, nk, e);
+        if (out_rev_deg) {
+            launch_indegree(e.gv(), e.indeg.p, e.s);
+            std::vector<uint32_t> indeg(n);
+            CK(cudaMemcpyAsync(indeg.data(), e.indeg.p, sizeof(uint32_t) * n,
+                               cudaMemcpyDeviceToHost, e.s));
+            CK(cudaStreamSynchronize(e.s));
+            for (uint32_t u = 0; u < n; ++u) out_rev_deg[u] = k + indeg[u];
+        }
+        CK(cudaStreamSynchronize(e.s));
+        if (changes) *changes = e.h_ctr->changes;
+        if (evals) *evals = ev;
+    });
+}
+
+int knng_cuda_candidate_distances(const float* data, uint32_t n, uint32_t d, uint32_t cap,
+                                  const uint32_t* cand_ids, const uint32_t* new_counts,
+                                  const uint32_t* old_counts, const uint64_t* offsets,
+                                  float* out_dists, uint64_t total, int device) {
+    return guarded([&] {
+        if (!data || !cand_ids || !new_counts || !old_counts || !offsets || !out_dists)
+            raise(KNNG_CUDA_INVALID_ARGUMENT, "null argument");
+        if (n < 2 || d < 1) raise(KNNG_CUDA_INVALID_ARGUMENT, "Dataset: degenerate shape");
+        if (cap == 0 || cap > KNNG_CUDA_MAX_CANDIDATES)
+            raise(KNNG_CUDA_INVALID_ARGUMENT, "cap must be in [1, 64]");
+        validate_cands(n, cap, cand_ids, new_counts, old_counts);
+        for (uint32_t u = 0; u < n; ++u)
+            if (new_counts[u] > 0 &&
+                offsets[u] + uint64_t(new_counts[u]) * (new_counts[u] + old_counts[u]) > total)
+                raise(KNNG_CUDA_INVALID_ARGUMENT, "offsets exceed the output size");
+        DeviceGuard dg(device);
+        StreamHolder sh(nullptr);
+        Engine e(device, n, d, 2, cap, sh.s);
+        e.upload(data, false);
+        CK(cudaMemcpyAsync(e.cand.p, cand_ids, sizeof(uint32_t) * size_t(n) * 2 * cap,
+                           cudaMemcpyHostToDevice, e.s));
+        CK(cudaMemcpyAsync(e.nc.p, new_counts, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, e.s));
+        CK(cudaMemcpyAsync(e.oc.p, old_counts, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, e.s));
+        std::vector<uint32_t> act;
+        for (uint32_t u = 0; u < n; ++u)
+            if (new_counts[u] > 0) act.push_back(u);
+        IterCounters hc = {};
+        hc.active = uint32_t(act.size());
+        CK(cudaMemcpyAsync(e.ctr.p, &hc, sizeof hc, cudaMemcpyHostToDevice, e.s));
+        if (!act.empty())
+            CK(cudaMemcpyAsync(e.active.p, act.data(), sizeof(uint32_t) * act.size(),
+                               cudaMemcpyHostToDevice, e.s));
+        DevBuf<uint64_t> off;
+        DevBuf<float> out;
+        to_device(off, offsets, n, e);
+        out.alloc(total, e.pool, e.s);
+        CK(cudaMemcpyAsync(out.p, out_dists, sizeof(float) * total, cudaMemcpyHostToDevice, e.s));
+        launch_join_distances(e.gv(), e.cv(), e.active.p, n, off.p, out.p, e.s, e.ctr.p);
+        CK(cudaGetLastError());
+        to_host(out_dists, out.p, total, e);
+        CK(cudaStreamSynchronize(e.s));
+    });
+}
+
+int knng_cuda_init_random(const float* data, uint32_t n, uint32_t d, uint32_t k, uint64_t seed,
+                          uint32_t* out_ids, float* out_dists, uint8_t* out_flags,
+                          uint32_t* out_rev_deg, uint64_t* evals, int device) {
+    return guarded([&] {
+        if (!data) raise(KNNG_CUDA_INVALID_ARGUMENT, "null argument");
+        validate_shape(n, d, k);
+        DeviceGuard dg(device);
+        StreamHolder sh(nullptr);
+        Engine e(device, n, d, k, 0, sh.s);
+        e.upload(data, false);
+        launch_init_random(e.gv(), seed, e.s);
+        const size_t nk = size_t(n) * k;
+        DevBuf<uint32_t> ids;
+        DevBuf<float> dists;
+        DevBuf<uint8_t> fl;
+        ids.alloc(nk, e.pool, e.s);
+        dists.alloc(nk, e.pool, e.s);
+        fl.alloc(nk, e.pool, e.s);
+        e.export_rows(ids.p, dists.p, fl.p);
+        to_host(out_ids, ids.p, nk, e);
+        to_host(out_dists, dists.p, nk, e);
+        to_host(out_flags, fl.p, nk, e);
+        if (out_rev_deg) {
+            launch_indegree(e.gv(), e.indeg.p, e.s);
+            std::vector<uint32_t> indeg(n);
+            CK(cudaMemcpyAsync(indeg.data(), e.indeg.p, sizeof(uint32_t) * n,
+                               cudaMemcpyDeviceToHost, e.s));
+            CK(cudaStreamSynchronize(e.s));
+            for (uint32_t u = 0; u < n; ++u) out_rev_deg[u] = k + indeg[u];
+        }
+        CK(cudaStreamSynchronize(e.s));
+        if (evals) *evals = nk;
+    });
+}
+
+int knng_cuda_select(uint32_t n, uint32_t k, uint32_t cap, const uint32_t* in_ids,
+                     const float* in_dists, const uint8_t* in_flags, uint64_t seed,
+                     uint32_t* cand_ids, uint32_t* new_counts, uint32_t* old_counts,
+                     uint8_t* out_flags_after, int device) {
+    return guarded([&] {
+        if (!in_ids || !in_dists || !in_flags || !cand_ids || !new_counts || !old_counts)
+            raise(KNNG_CUDA_INVALID_ARGUMENT, "null argument");
+        validate_shape(n, 1, k);
+        if (cap == 0) raise(KNNG_CUDA_INVALID_ARGUMENT, "CandidateSet: cap must be positive");
+        if (cap > KNNG_CUDA_MAX_CANDIDATES)
+            raise(KNNG_CUDA_INVALID_ARGUMENT, "this build supports max_candidates <= 64");
+        validate_rows(n, k, in_ids);
+        DeviceGuard dg(device);
+        StreamHolder sh(nullptr);
+        Engine e(device, n, 1, k, cap, sh.s);
+        const size_t nk = size_t(n) * k;
+        DevBuf<uint32_t> ids;
+        DevBuf<float> dists;
+        DevBuf<uint8_t> fl;
+        to_device(ids, in_ids, nk, e);
+        to_device(dists, in_dists, nk, e);
+        to_device(fl, in_flags, nk, e);
+        launch_load_rows(e.gv(), ids.p, dists.p, fl.p, e.s);
+        KernelTimer timer(false, e.s, nullptr);
+        e.select(seed, timer);
+        to_host(cand_ids, e.cand.p, size_t(n) * 2 * cap, e);
+        to_host(new_counts, e.nc.p, n, e);
+        to_host(old_counts, e.oc.p, n, e);
+        std::vector<uint32_t> sorted_ids(nk);
+        std::vector<uint8_t> sorted_flags(nk);
+        e.export_rows(ids.p, nullptr, fl.p);
+        to_host(sorted_ids.data(), ids.p, nk, e);
+        to_host(sorted_flags.data(), fl.p, nk, e);
+        CK(cudaStreamSynchronize(e.s));
+        if (out_flags_after) {
+            // report flags in the caller's entry order
+            for (uint32_t u = 0; u < n; ++u)
+                for (uint32_t i = 0; i < k; ++i) {
+                    const uint32_t id = in_ids[size_t(u) * k + i];
+                    for (uint32_t j = 0; j < k; ++j)
+                        if (sorted_ids[size_t(u) * k + j] == id)
+                            out_flags_after[size_t(u) * k + i] = sorted_flags[size_t(u) * k + j];
+                }
+        }
+    });
+}
+
+int knng_cuda_bruteforce_queries(const float* data, uint32_t n, uint32_t d, uint32_t k,
+                                 const uint32_t* queries, uint32_t nq, uint32_t* out_ids,
+                                 double* out_dists, int device) {
+    return guarded([&] {
+        if (!data || !out_ids) raise(KNNG_CUDA_INVALID_ARGUMENT, "null argument");
+        if (k == 0 || k >= n) raise(KNNG_CUDA_INVALID_ARGUMENT, "brute_force_knng: need 0 < k < n");
+        if (k > KNNG_CUDA_MAX_K) raise(KNNG_CUDA_INVALID_ARGUMENT, "this build supports k <= 32");
+        if (d < 1) raise(KNNG_CUDA_INVALID_ARGUMENT, "Dataset: need at least 1 dimension");
+        if (n >= (1u << 31)) raise(KNNG_CUDA_INVALID_ARGUMENT, "this build supports n < 2^31");
+        if (queries)
+            for (uint32_t i = 0; i < nq; ++i)
+                if (queries[i] >= n) raise(KNNG_CUDA_INVALID_ARGUMENT, "query id out of range");
+        const uint32_t count = queries ? nq : n;
+        DeviceGuard dg(device);
+        StreamHolder sh(nullptr);
+        Engine e(device, n, d, k, 0, sh.s);
+        e.upload(data, false);
+        DevBuf<uint32_t> q;
+        if (queries) {
+            to_device(q, queries, count, e);
+        } else {
+            q.alloc(count, e.pool, e.s);
+            launch_iota(q.p, count, e.s);
+        }
+        const size_t nk = size_t(count) * k;
+        DevBuf<uint32_t> ids;
+        DevBuf<double> dists;
+        DevBuf<uint64_t> top;
+        ids.alloc(nk, e.pool, e.s);
+        dists.alloc(nk, e.pool, e.s);
+        top.alloc(bruteforce_scratch_keys(count), e.pool, e.s);
+        launch_bruteforce_queries(e.data.p, n, d, e.stride, k, q.p, count, top.p, ids.p, dists.p,
+                                  e.s);
+        CK(cudaGetLastError());
+        to_host(out_ids, ids.p, nk, e);
+        if (out_dists) to_host(out_dists, dists.p, nk, e);
+        CK(cudaStreamSynchronize(e.s));
+    });
+}
+
+int knng_cuda_bruteforce_knng(const float* data, uint32_t n, uint32_t d, uint32_t k,
+                              uint32_t* out_ids, double* out_dists, int device) {
+    return knng_cuda_bruteforce_queries(data, n, d, k, nullptr, n, out_ids, out_dists, device);
+}
+
+int knng_cuda_locality_permutation(uint32_t n, uint32_t k, const uint32_t* ids,
+                                   const float* dists, uint32_t* sigma, uint32_t* sigma_inv,
+                                   int device) {
+    (void)n; (void)k; (void)ids; (void)dists; (void)sigma; (void)sigma_inv; (void)device;
+    g_err = "locality permutation is not available in this build yet";
+    return KNNG_CUDA_NOT_IMPLEMENTED;
+}
+
+}  // extern "C"

@@ -1,0 +1,353 @@
+// Graph-state and candidate-selection kernels (sm_100a).
+//
+//   init_random   KnnGraph::init_random          graph.hpp:34-67
+//   load/export   KnnGraph::from_rows / rows      graph.hpp:70-93, 169-184
+//   indegree      reverse_degree_ = k + in-degree graph.hpp:44,62,121-122
+//   sample        select_turbo's offers           selection.hpp:282-320
+//   finalize      dedup + flag_consumed + active  selection.hpp:299-302,
+//                                                 graph.hpp:133-143
+//
+// All of these are HBM/L2-latency-bound integer work: one warp per node where
+// a node's k-entry row is the unit (k <= 32: lane i owns entry i), one
+// thread per edge where the edge is the unit.
+#include "kernels.cuh"
+
+namespace knng_cuda {
+
+namespace {
+
+constexpr uint32_t kSaltInit = 0x494e4954u;    // "INIT"
+constexpr uint32_t kSaltSample = 0x53414d50u;  // "SAMP"
+
+__device__ __forceinline__ uint32_t full_mask_k(uint32_t k) {
+    return k >= 32 ? 0xffffffffu : ((1u << k) - 1u);
+}
+
+// Squared L2 in the reference's scalar order (l2_sq_core, distance.hpp:35-51):
+// eight strided lanes, UNFUSED square-accumulate, tree
+// ((0+1)+(2+3))+((4+5)+(6+7)).  Called by a full warp; the 8-lane group g
+// (lanes 8g..8g+7) evaluates the pair (a_row, b_row) of its choosing and every
+// lane of the group returns the distance.
+__device__ __forceinline__ float group8_l2_scalar(const float* __restrict__ a,
+                                                  const float* __restrict__ b, uint32_t stride,
+                                                  bool active) {
+    const uint32_t l8 = lane_id() & 7u;
+    float acc = 0.0f;
+    if (active) {
+        for (uint32_t c = 0; c < stride; c += 8) {
+            const float diff = __fsub_rn(__ldg(a + c + l8), __ldg(b + c + l8));
+            acc = __fadd_rn(acc, __fmul_rn(diff, diff));
+        }
+    }
+    acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 1));
+    acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 2));
+    acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 4));
+    return acc;
+}
+
+// One warp per node: k distinct uniform ids != u, true distances, sorted row.
+__global__ void __launch_bounds__(256) init_random_kernel(GraphView g, uint32_t seed_lo,
+                                                          uint32_t seed_hi) {
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (warp >= g.n) return;
+    const uint32_t u = warp, lane = lane_id(), k = g.k, n = g.n;
+    const bool real = lane < k;
+    uint32_t id = n + lane;  // placeholder, unique and never a valid id
+    bool accepted = !real;
+    uint32_t attempt = 0;
+    const uint32_t lt = (1u << lane) - 1u;
+    while (true) {
+        if (!accepted) {
+            const Philox4 r = philox4x32_10(u, lane, attempt, kSaltInit, seed_lo, seed_hi);
+            id = bounded(r.x, n);
+        }
+        ++attempt;
+        const uint32_t same = __match_any_sync(0xffffffffu, id);
+        const uint32_t acc_mask = __ballot_sync(0xffffffffu, accepted);
+        if (!accepted) {
+            const uint32_t pending = ~acc_mask;
+            const bool conflict = id == u || (same & acc_mask) != 0u || (same & pending & lt) != 0u;
+            accepted = !conflict;
+        }
+        if (__all_sync(0xffffffffu, accepted)) break;
+    }
+    // distances: four pairs per pass, one per 8-lane group
+    const float* ru = g.data + size_t(u) * g.stride;
+    float mine = 0.0f;
+    for (uint32_t e = 0; e < k; e += 4) {
+        const uint32_t pair = e + (lane >> 3);
+        const uint32_t v = __shfl_sync(0xffffffffu, id, pair & 31u);
+        const bool act = pair < k;
+        const float dist = group8_l2_scalar(ru, g.data + size_t(act ? v : u) * g.stride,
+                                            g.stride, act);
+        // lane (e + j) takes the result of group j (lane 8j)
+        const uint32_t src = ((lane - e) & 3u) << 3;
+        const float got = __shfl_sync(0xffffffffu, dist, src);
+        if (lane >= e && lane < e + 4) mine = got;
+    }
+    uint64_t key = real ? pack_key(mine, id) : kEmptyKey;
+    key = warp_sort_u64(key);
+    if (real) g.keys[size_t(u) * k + lane] = key;
+    const uint64_t last = __shfl_sync(0xffffffffu, key, k - 1);
+    if (lane == 0) {
+        g.flags[u] = full_mask_k(k);
+        g.maxd[u] = key_dist(last);
+        g.locks[u] = 0u;
+    }
+}
+
+// One warp per node: rows given in any order (e.g. the reference heap order)
+// -> sorted keys + flag bits.  Mirrors KnnGraph::from_rows (graph.hpp:70-93).
+__global__ void __launch_bounds__(256) load_rows_kernel(GraphView g, const uint32_t* ids,
+                                                        const float* dists,
+                                                        const uint8_t* flags) {
+    const uint32_t u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (u >= g.n) return;
+    const uint32_t lane = lane_id(), k = g.k;
+    const bool real = lane < k;
+    const size_t p = size_t(u) * k + lane;
+    const uint32_t id = real ? ids[p] : 0xffffffffu;
+    const uint32_t fl = real ? flags[p] : 0u;
+    uint64_t key = real ? pack_key(dists[p], id) : kEmptyKey;
+    key = warp_sort_u64(key);
+    // flag of the entry now held by this lane: look up the original lane by id
+    const uint32_t my_id = key_id(key);
+    uint32_t my_flag = 0;
+    for (uint32_t j = 0; j < k; ++j) {
+        const uint32_t idj = __shfl_sync(0xffffffffu, id, j);
+        const uint32_t flj = __shfl_sync(0xffffffffu, fl, j);
+        if (real && idj == my_id) my_flag = flj;
+    }
+    if (real) g.keys[p] = key;
+    const uint32_t mask = __ballot_sync(0xffffffffu, real && my_flag != 0u);
+    const uint64_t last = __shfl_sync(0xffffffffu, key, k - 1);
+    if (lane == 0) {
+        g.flags[u] = mask;
+        g.maxd[u] = key_dist(last);
+        g.locks[u] = 0u;
+    }
+}
+
+__global__ void export_rows_kernel(GraphView g, uint32_t* ids, float* dists, uint8_t* flags) {
+    const size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const size_t total = size_t(g.n) * g.k;
+    if (e >= total) return;
+    const uint64_t key = g.keys[e];
+    if (ids) ids[e] = key_id(key);
+    if (dists) dists[e] = key_dist(key);
+    if (flags) {
+        const uint32_t u = uint32_t(e / g.k), i = uint32_t(e % g.k);
+        flags[e] = uint8_t((g.flags[u] >> i) & 1u);
+    }
+}
+
+__global__ void indegree_kernel(GraphView g, uint32_t* indeg) {
+    const size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= size_t(g.n) * g.k) return;
+    atomicAdd(indeg + key_id(g.keys[e]), 1u);
+}
+
+// select_turbo's offer (selection.hpp:296-309), concurrently: accept with
+// probability cap/deg when deg > cap (deg = k + in-degree, not deduplicated,
+// exactly reverse_degree); append to the target's new or old list by the
+// edge's flag; once a list holds cap ids further accepts replace a uniform
+// slot with reservoir probability cap/(seen) (the reference overwrites a
+// uniform slot unconditionally; both keep the list a random subset).
+// Duplicates are removed by finalize.
+__device__ __forceinline__ void offer(const CandView& c, uint32_t k, const uint32_t* indeg,
+                                      uint32_t target, uint32_t cand, uint32_t is_new,
+                                      uint32_t r_accept, uint32_t r_slot) {
+    const uint32_t deg = k + __ldg(indeg + target);
+    if (deg > c.cap && uint64_t(r_accept) * deg >= (uint64_t(c.cap) << 32)) return;
+    uint32_t* counter = is_new ? c.raw_new : c.raw_old;
+    const uint32_t slot = atomicAdd(counter + target, 1u);
+    uint32_t* list = c.ids + size_t(target) * 2 * c.cap + (is_new ? 0u : c.cap);
+    if (slot < c.cap) {
+        list[slot] = cand;
+    } else {
+        const uint32_t j = bounded(r_slot, slot + 1u);
+        if (j < c.cap) list[j] = cand;
+    }
+}
+
+__global__ void __launch_bounds__(256) sample_kernel(GraphView g, CandView c,
+                                                     const uint32_t* indeg, uint32_t seed_lo,
+                                                     uint32_t seed_hi) {
+    const size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= size_t(g.n) * g.k) return;
+    const uint32_t u = uint32_t(e / g.k), i = uint32_t(e % g.k);
+    const uint32_t v = key_id(g.keys[e]);
+    const uint32_t is_new = (__ldg(g.flags + u) >> i) & 1u;
+    const Philox4 r = philox4x32_10(uint32_t(e), uint32_t(e >> 32), kSaltSample, 0u, seed_lo,
+                                    seed_hi);
+    offer(c, g.k, indeg, u, v, is_new, r.x, r.y);  // v into u's lists
+    offer(c, g.k, indeg, v, u, is_new, r.z, r.w);  // u into v's lists
+}
+
+__global__ void reset_raw_kernel(CandView c, uint32_t n) {
+    const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= n) return;
+    c.raw_new[u] = 0u;
+    c.raw_old[u] = 0u;
+}
+
+// One warp per node: clamp raw counts, dedup (within a list, first slot
+// wins; across lists the copy from the edge the reference visits first wins:
+// the forward edge u->x iff u < x, selection.hpp:311-317), compact, clear the
+// flags of heap entries named by the new list (flag_consumed,
+// graph.hpp:133-143), count the join's evaluations and list the node as
+// active when nn > 0 (compute_step skips nn == 0, descent.hpp:94).
+constexpr uint32_t kFinWarps = 8;
+constexpr uint32_t kTomb = 0xffffffffu;
+
+__global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(GraphView g, CandView c,
+                                                                  uint32_t* active,
+                                                                  IterCounters* ctr) {
+    __shared__ uint32_t s_new[kFinWarps][kMaxCap];
+    __shared__ uint32_t s_old[kFinWarps][kMaxCap];
+    __shared__ uint32_t s_hid[kFinWarps][kMaxK];
+    __shared__ unsigned long long s_evals, s_cands;
+    if (threadIdx.x == 0) {
+        s_evals = 0;
+        s_cands = 0;
+    }
+    __syncthreads();
+    const uint32_t w = threadIdx.x >> 5, lane = lane_id();
+    const uint32_t u = blockIdx.x * kFinWarps + w;
+    const uint32_t cap = c.cap, k = g.k;
+    if (u < g.n) {
+        const uint32_t nr = min(c.raw_new[u], cap), orr = min(c.raw_old[u], cap);
+        const uint32_t* list = c.ids + size_t(u) * 2 * cap;
+        for (uint32_t p = lane; p < nr; p += 32) s_new[w][p] = list[p];
+        for (uint32_t p = lane; p < orr; p += 32) s_old[w][p] = list[cap + p];
+        const uint32_t hid = lane < k ? key_id(g.keys[size_t(u) * k + lane]) : kTomb;
+        s_hid[w][lane] = hid;
+        const uint32_t hflags = g.flags[u];
+        __syncwarp();
+        // within-list duplicates: keep the first slot
+        bool drop_n[2] = {false, false}, drop_o[2] = {false, false};
+#pragma unroll
+        for (uint32_t h = 0; h < 2; ++h) {
+            const uint32_t p = lane + 32 * h;
+            if (p < nr) {
+                const uint32_t x = s_new[w][p];
+                for (uint32_t q = 0; q < p; ++q)
+                    if (s_new[w][q] == x) { drop_n[h] = true; break; }
+            }
+            if (p < orr) {
+                const uint32_t x = s_old[w][p];
+                for (uint32_t q = 0; q < p; ++q)
+                    if (s_old[w][q] == x) { drop_o[h] = true; break; }
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (uint32_t h = 0; h < 2; ++h) {
+            const uint32_t p = lane + 32 * h;
+            if (p < nr && drop_n[h]) s_new[w][p] = kTomb;
+            if (p < orr && drop_o[h]) s_old[w][p] = kTomb;
+        }
+        __syncwarp();
+        // across lists
+#pragma unroll
+        for (uint32_t h = 0; h < 2; ++h) {
+            const uint32_t p = lane + 32 * h;
+            if (p < orr && s_old[w][p] != kTomb) {
+                const uint32_t x = s_old[w][p];
+                for (uint32_t q = 0; q < nr; ++q) {
+                    if (s_new[w][q] == x) {
+                        uint32_t f_fwd = 1u;
+                        for (uint32_t i = 0; i < k; ++i)
+                            if (s_hid[w][i] == x) { f_fwd = (hflags >> i) & 1u; break; }
+                        const bool keep_new = (u < x) ? (f_fwd != 0u) : (f_fwd == 0u);
+                        if (keep_new) s_old[w][p] = kTomb; else s_new[w][q] = kTomb;
+                        break;
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        // compact both lists
+        uint32_t nn = 0, no = 0;
+        uint32_t* out = c.ids + size_t(u) * 2 * cap;
+#pragma unroll
+        for (uint32_t h = 0; h < 2; ++h) {
+            const uint32_t p = lane + 32 * h;
+            const uint32_t xn = p < nr ? s_new[w][p] : kTomb;
+            const uint32_t xo = p < orr ? s_old[w][p] : kTomb;
+            const uint32_t mn = __ballot_sync(0xffffffffu, xn != kTomb);
+            const uint32_t mo = __ballot_sync(0xffffffffu, xo != kTomb);
+            const uint32_t lt = (1u << lane) - 1u;
+            if (xn != kTomb) out[nn + __popc(mn & lt)] = xn;
+            if (xo != kTomb) out[cap + no + __popc(mo & lt)] = xo;
+            nn += __popc(mn);
+            no += __popc(mo);
+        }
+        // flag_consumed: clear heap entries named by the final new list
+        bool named = false;
+        if (lane < k)
+            for (uint32_t q = 0; q < nr; ++q)
+                if (s_new[w][q] == hid) { named = true; break; }
+        const uint32_t clear = __ballot_sync(0xffffffffu, named);
+        if (lane == 0) {
+            c.nc[u] = nn;
+            c.oc[u] = no;
+            g.flags[u] = hflags & ~clear;
+            if (nn > 0) {
+                const unsigned long long ev =
+                    (unsigned long long)nn * (nn - 1) / 2 + (unsigned long long)nn * no;
+                atomicAdd(&s_evals, ev);
+                atomicAdd(&s_cands, (unsigned long long)(nn + no));
+                active[atomicAdd(&ctr->active, 1u)] = u;
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (s_evals) atomicAdd(&ctr->evals, s_evals);
+        if (s_cands) atomicAdd(&ctr->cands, s_cands);
+    }
+}
+
+inline uint32_t blocks_for(size_t items, uint32_t per_block) {
+    return uint32_t((items + per_block - 1) / per_block);
+}
+
+}  // namespace
+
+void launch_init_random(const GraphView& g, uint64_t seed, cudaStream_t s) {
+    init_random_kernel<<<blocks_for(size_t(g.n) * 32, 256), 256, 0, s>>>(
+        g, uint32_t(seed), uint32_t(seed >> 32));
+}
+
+void launch_load_rows(const GraphView& g, const uint32_t* ids, const float* dists,
+                      const uint8_t* flags, cudaStream_t s) {
+    load_rows_kernel<<<blocks_for(size_t(g.n) * 32, 256), 256, 0, s>>>(g, ids, dists, flags);
+}
+
+void launch_export_rows(const GraphView& g, uint32_t* ids, float* dists, uint8_t* flags,
+                        cudaStream_t s) {
+    export_rows_kernel<<<blocks_for(size_t(g.n) * g.k, 256), 256, 0, s>>>(g, ids, dists, flags);
+}
+
+void launch_indegree(const GraphView& g, uint32_t* indeg, cudaStream_t s) {
+    cudaMemsetAsync(indeg, 0, sizeof(uint32_t) * g.n, s);
+    indegree_kernel<<<blocks_for(size_t(g.n) * g.k, 256), 256, 0, s>>>(g, indeg);
+}
+
+void launch_reset_raw(const CandView& c, uint32_t n, cudaStream_t s) {
+    reset_raw_kernel<<<blocks_for(n, 256), 256, 0, s>>>(c, n);
+}
+
+void launch_sample(const GraphView& g, const CandView& c, const uint32_t* indeg, uint64_t seed,
+                   cudaStream_t s) {
+    sample_kernel<<<blocks_for(size_t(g.n) * g.k, 256), 256, 0, s>>>(
+        g, c, indeg, uint32_t(seed), uint32_t(seed >> 32));
+}
+
+void launch_finalize(const GraphView& g, const CandView& c, uint32_t* active,
+                     IterCounters* ctr, cudaStream_t s) {
+    finalize_kernel<<<blocks_for(g.n, kFinWarps), kFinWarps * 32, 0, s>>>(g, c, active, ctr);
+}
+
+}  // namespace knng_cuda

@@ -1,0 +1,269 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle.
+
+The checker is the plain-C restatement (oracle/knng_oracle.c), itself pinned
+bit-for-bit to the reference in tests/test_oracle_pins.py; where the reference
+harness is present its numbers are used directly for the recall gates.
+"""
+import numpy as np
+import pytest
+
+import paper_2112_06630_b200 as kg
+from paper_2112_06630_b200 import datasets
+
+pytestmark = pytest.mark.gpu
+
+
+def bits(a):
+    return np.asarray(a, np.float32).view(np.uint32)
+
+
+def make_data(kind, n, seed=0):
+    if kind == "C1":
+        return datasets.generate(datasets.CONFIGS["C1"], n)
+    if kind == "C2":
+        return datasets.generate(datasets.CONFIGS["C2"], n)
+    if kind == "C3":
+        rng = np.random.default_rng(seed)
+        c = rng.normal(0, 10, (20, 128)).astype(np.float32)
+        return (c[rng.integers(0, 20, n)] + rng.standard_normal((n, 128), dtype=np.float32))
+    if kind == "G24":
+        return np.random.default_rng(seed).standard_normal((n, 24), dtype=np.float32)
+    raise KeyError(kind)
+
+
+CASES = [  # kind, n, k, cap, seed, step
+    ("C1", 10000, 20, 20, 0, 1), ("C1", 10000, 20, 20, 0, 2), ("C1", 10000, 20, 20, 0, 5),
+    ("C2", 3000, 20, 50, 1, 1), ("C2", 3000, 20, 50, 1, 2), ("C2", 3000, 20, 50, 1, 6),
+    ("C3", 4000, 30, 50, 2, 1), ("C3", 4000, 30, 50, 2, 2), ("C3", 4000, 30, 50, 2, 4),
+    ("G24", 600, 8, 15, 11, 1),
+]
+
+
+def compare_step(gi, go_ref, g_gpu, rel=1e-5):
+    """Accepted-update-set comparison.  Returns stats; asserts
+    equality up to swaps between distances tied within `rel` at row ends."""
+    n, k = gi.ids.shape
+    mism = 0
+    tie_ok = 0
+    common = 0
+    exact = 0
+    flag_bad = 0
+    for u in range(n):
+        init = set(gi.ids[u].tolist())
+        ref = dict(zip(go_ref.ids[u].tolist(), go_ref.dists[u].tolist()))
+        ref_f = dict(zip(go_ref.ids[u].tolist(), go_ref.flags[u].tolist()))
+        gpu = dict(zip(g_gpu.ids[u].tolist(), g_gpu.dists[u].tolist()))
+        gpu_f = dict(zip(g_gpu.ids[u].tolist(), g_gpu.flags[u].tolist()))
+        acc_ref = set(ref) - init
+        acc_gpu = set(gpu) - init
+        diff = (set(ref) ^ set(gpu))
+        if diff:
+            # allowed only as ties at the row boundary
+            kth = max(max(ref.values()), max(gpu.values()))
+            for v in diff:
+                dv = ref.get(v, gpu.get(v))
+                if abs(dv - kth) <= rel * max(kth, 1e-30):
+                    tie_ok += 1
+                else:
+                    mism += 1
+        for v in set(ref) & set(gpu):
+            common += 1
+            a, b = np.float32(ref[v]), np.float32(gpu[v])
+            assert abs(float(a) - float(b)) <= rel * max(float(a), 1e-30), (u, v, a, b)
+            exact += int(a.view(np.uint32) == b.view(np.uint32))
+            flag_bad += int(ref_f[v] != gpu_f[v])
+        del acc_ref, acc_gpu
+    return dict(mismatch=mism, tie_swaps=tie_ok, common=common, bit_exact=exact,
+                flag_mismatch=flag_bad)
+
+
+@pytest.mark.parametrize("kind,n,k,cap,seed,t", CASES)
+def test_local_join_step_matches_oracle(gpu, restated, kind, n, k, cap, seed, t):
+    import oracle
+    data = make_data(kind, n, seed)
+    gi, c, go, ch_ref, ev_ref = restated.capture_step(data, k, cap, seed, t)
+    cands = kg.CandidateSet(c.ids, c.new_counts, c.old_counts)
+    g, rev, ch, ev = kg.compute_step(data, gi.ids, gi.dists, gi.flags, cands)
+    assert ev == ev_ref  # acceptance.cpp:358-381
+    st = compare_step(gi, go, g)
+    assert st["mismatch"] == 0, st
+    assert st["flag_mismatch"] == 0, st
+    assert st["bit_exact"] >= st["common"] - 2, st  # same-pair path differences only
+    # reverse_degree is k + in-degree of the result (graph.hpp:121-122)
+    assert np.array_equal(rev, g.reverse_degree())
+    # rows sorted by (dist, id), distinct, no self loops
+    assert np.all(np.diff(g.dists, axis=1) >= 0)
+    assert all(len(set(r)) == k for r in g.ids.tolist())
+    assert not np.any(g.ids == np.arange(n)[:, None])
+    # changes: order-dependent; same order of magnitude
+    assert ch > 0 or ch_ref == 0
+    del oracle
+
+
+@pytest.mark.parametrize("kind,n,k,cap,seed,t", [c for c in CASES if c[5] <= 2])
+def test_candidate_distances_bit_exact(gpu, restated, kind, n, k, cap, seed, t):
+    """Every new x new / new x old distance of the join equals the reference's
+    kernel path for that pair (tri/5x5 tiles fused, remainders unfused)."""
+    data = make_data(kind, n, seed)
+    _, c, _, _, _ = restated.capture_step(data, k, cap, seed, t)
+    cands = kg.CandidateSet(c.ids, c.new_counts, c.old_counts)
+    got = kg.candidate_distances(data, cands)
+    stride = (data.shape[1] + 7) // 8 * 8
+    pdata = np.zeros((n, stride), np.float32)
+    pdata[:, : data.shape[1]] = data
+    checked = 0
+    for u, D in list(got.items())[:: max(1, len(got) // 400)]:
+        nn, no = int(c.new_counts[u]), int(c.old_counts[u])
+        new = c.ids[u, :nn]
+        old = c.ids[u, cap: cap + no]
+        if nn >= 2:
+            mat, _ = restated.mutual_block(pdata[new])
+            iu = np.triu_indices(nn, 1)
+            assert np.array_equal(bits(D[:, :nn][iu]), bits(mat[iu])), u
+        for i0 in range(0, nn, 5):
+            for j0 in range(0, no, 5):
+                tile = restated.block_l2_sq(pdata[new[i0:i0 + 5]], pdata[old[j0:j0 + 5]])
+                assert np.array_equal(bits(D[i0:i0 + 5, nn + j0: nn + j0 + 5]), bits(tile)), u
+        checked += 1
+    assert checked > 0
+
+
+def test_init_random_properties(gpu, restated):
+    data = make_data("C1", 3000)
+    g, rev, ev = kg.init_random(data, 20, 77)
+    n, k = g.ids.shape
+    assert ev == n * k
+    assert not np.any(g.ids == np.arange(n)[:, None])
+    assert all(len(set(r)) == k for r in g.ids.tolist())
+    assert np.all(g.flags == 1)
+    assert np.all(np.diff(g.dists, axis=1) >= 0)
+    assert int(rev.sum()) == 2 * n * k  # test_graph.cpp:77-98
+    # distances are the reference's scalar (unfused) l2_sq, bit for bit
+    for u in range(0, n, 37):
+        for i in range(k):
+            want = restated.l2_sq(data[u], data[g.ids[u, i]])
+            assert bits(g.dists[u, i]) == bits(want)
+    # uniform: every id is picked ~k times on average
+    counts = np.bincount(g.ids.ravel(), minlength=n)
+    assert abs(counts.mean() - k) < 1e-9 and counts.max() < 4 * k
+
+
+def test_init_random_forced_complete_graph(gpu):
+    # test_graph.cpp:56-75: n=3, k=2 -> every node links the other two
+    data = np.random.default_rng(1).standard_normal((3, 8), dtype=np.float32)
+    g, _, ev = kg.init_random(data, 2, 9)
+    assert ev == 6
+    for u in range(3):
+        assert sorted(g.ids[u].tolist()) == [v for v in range(3) if v != u]
+
+
+def test_select_soundness_and_flags(gpu, restated):
+    data = make_data("G24", 2000, 5)
+    g0, _ = restated.init_random(data, 10, 99)
+    cands, flags_after = kg.select_turbo(g0.ids, g0.dists, g0.flags, 25, 1234)
+    n, k = g0.ids.shape
+    nbr = [set() for _ in range(n)]
+    for u in range(n):
+        for v in g0.ids[u].tolist():
+            nbr[u].add(v)
+            nbr[v].add(u)
+    for u in range(n):
+        new = cands.new_ids(u).tolist()
+        old = cands.old_ids(u).tolist()
+        assert len(new) <= 25 and len(old) <= 25
+        assert len(set(new) | set(old)) == len(new) + len(old)  # no duplicates anywhere
+        assert all(x in nbr[u] for x in new + old)  # test_selection.cpp:81-94
+        assert u not in new and u not in old
+        # flag_consumed: entries named in the new list are no longer new
+        for i, v in enumerate(g0.ids[u].tolist()):
+            if v in new:
+                assert flags_after[u, i] == 0
+            else:
+                assert flags_after[u, i] == g0.flags[u, i]
+    # initial graph: every edge is new, so old lists are empty
+    assert int(cands.old_counts.sum()) == 0
+
+
+def test_select_expectation(gpu, restated):
+    """acceptance.cpp:133-188 criterion 3: mean candidate count per node within
+    10% of min(|N(u)|, cap) over independent seeds."""
+    n, k, cap, trials = 2000, 20, 50, 60
+    data = make_data("G24", n, 5)
+    g0, _ = restated.init_random(data, k, 99)
+    members = [set() for _ in range(n)]
+    for u in range(n):
+        for v in g0.ids[u].tolist():
+            members[u].add(v)
+            members[v].add(u)
+    tot = np.zeros(n)
+    for t in range(trials):
+        c, _ = kg.select_turbo(g0.ids, g0.dists, g0.flags, cap, 500 + t)
+        tot += c.new_counts + c.old_counts
+    mean = tot / trials
+    expected = np.minimum([len(m) for m in members], cap)
+    rel = np.abs(mean - expected) / expected
+    assert rel.max() <= 0.10, rel.max()
+
+
+@pytest.mark.parametrize("kind,n,k,cap,seed", [
+    ("C1", 10000, 20, 20, 0),       # BASELINE config 1 exactly
+    ("C3", 20000, 30, 50, 3),
+    ("C2", 8000, 20, 50, 0),
+    ("G24", 4000, 10, 30, 4),
+])
+def test_recall_matches_reference(gpu, restated, kind, n, k, cap, seed):
+    """End-to-end recall@k within 0.5 pp of the reference's from the same seed
+    and parameters (north-star gate), against the exact K-NNG."""
+    data = make_data(kind, n, seed)
+    res = kg.run(data, kg.RunParams(k=k, max_candidates=cap, seed=seed))
+    ex_ids, _ = kg.brute_force_knng(data, k)
+    r_gpu = kg.recall(res.graph.ids, ex_ids)
+    ref = restated.run(data, k=k, cap=cap, seed=seed)
+    r_ref = kg.recall(ref.graph.ids, ex_ids)
+    assert r_gpu >= r_ref - 0.005, (r_gpu, r_ref)
+    # metrics bookkeeping (descent.hpp:237-251)
+    m = res.metrics
+    assert m.iterations[0].dist_evals == n * k
+    assert m.total_dist_evals == sum(it.dist_evals for it in m.iterations)
+    assert m.total_changes == sum(it.changes for it in m.iterations)
+    last = m.iterations[-1]
+    assert last.changes < 0.001 * n * k or len(m.iterations) == 31
+    assert np.all(np.diff(res.graph.dists, axis=1) >= 0)
+
+
+def test_reference_recall_gate_gaussian(gpu, restated):
+    # acceptance criterion 1 (d=8): gaussian-mixture n=16384, k=20, cap=50, seed 13
+    rng = np.random.default_rng(7)
+    n, d = 16384, 8
+    data = (rng.normal(0, np.sqrt(2), (n, d)).astype(np.float32))
+    data[np.arange(n), np.arange(n) % d] += 1.0
+    res = kg.run(data, kg.RunParams(k=20, max_candidates=50, seed=13))
+    ex, _ = kg.brute_force_knng(data, 20)
+    assert kg.recall(res.graph.ids, ex) >= 0.99
+
+
+@pytest.mark.parametrize("kind,n,k", [("G24", 3000, 7), ("C2", 2000, 20), ("C1", 4000, 20)])
+def test_bruteforce_index_exact(gpu, restated, kind, n, k):
+    data = make_data(kind, n, 3)
+    ids, dists = kg.brute_force_knng(data, k)
+    rids, rdists = restated.brute_force(data, k)
+    assert np.array_equal(ids, rids)
+    assert np.array_equal(dists, rdists)
+
+
+def test_bruteforce_tail_dimensions(gpu, restated):
+    data = np.random.default_rng(9).standard_normal((1500, 10), dtype=np.float32)
+    ids, dists = kg.brute_force_knng(data, 5)
+    rids, rdists = restated.brute_force(data, 5)
+    assert np.array_equal(ids, rids) and np.array_equal(dists, rdists)
+    q = np.array([0, 17, 1499], np.uint32)
+    qi, _ = kg.brute_force_knng(data, 5, queries=q)
+    assert np.array_equal(qi, rids[q])
+
+
+def test_nndescent_l2_entry(gpu):
+    data = make_data("C1", 5000)
+    ids, dists, m = kg.nndescent_l2(data, k=20, sample_rate=1.0, delta=0.001, seed=0)
+    assert ids.shape == (5000, 20) and m.total_dist_evals > 5000 * 20
+    with pytest.raises(kg.InvalidArgument):
+        kg.nndescent_l2(data, k=20, sample_rate=0.9)
