@@ -1,0 +1,360 @@
+#!/usr/bin/env python
+"""Benchmark: GPU NN-Descent K-NNG build (squared L2) — BASELINE.json's metric
+"K-NNG build time & distance evals/s at matched recall@k vs CPU ref".
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C2]
+
+A step is one complete K-NNG build (knng::run: random init + iterations to
+termination) of the config's synthetic dataset.  Default workload: config C2
+(BASELINE.json configs[1], n=70,000 x d=784 image-like, k=20, cap 50).
+
+`value` = distance evaluations per second over the K timed builds, whole job,
+inputs resident in HBM (device-pointer entry knng_cuda_run_device), device
+time from CUDA events, max over ranks.  `e2e` = the same metric through the
+host-pointer C-ABI (knng_cuda_run) with the pinned-host -> device copy of the
+data and the device -> host copy of the graph inside every step.
+`--impl reference` times the reference's own CPU code (oracle/_ref, the
+unmodified knng headers) on the host; it is single-threaded by contract.
+With N > 1 (torchrun) each rank builds its own instance (replicas; the
+sharded multi-GPU build is not part of this round).
+"""
+from __future__ import annotations
+
+import argparse
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2112_06630_b200 import datasets  # noqa: E402
+
+METRIC = "dist_evals_per_s"
+UNIT = "distance evaluations/s"
+PROFILE_TRAFFIC = os.path.join(ROOT, "profiles", "join_traffic.json")
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.25)
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = []
+        with open(self.path) as f:
+            for r in csv.reader(f):
+                if len(r) >= 9:
+                    rows.append([x.strip() for x in r])
+        os.unlink(self.path)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i] == "Active"})
+        loaded = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": float(np.median(loaded)), "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def ffma_peak_tflops(device: int):
+    import ctypes as C
+    path = os.path.join(ROOT, "paper_2112_06630_b200", "lib", "libknng_diag.so")
+    if not os.path.exists(path):
+        return None
+    lib = C.CDLL(path)
+    t = C.c_double(0)
+    t2 = C.c_double(0)
+    ms = C.c_double(0)
+    if lib.knng_diag_ffma_peak(device, C.byref(t), C.byref(ms)) != 0:
+        return None
+    if lib.knng_diag_ffma2_peak(device, C.byref(t2)) != 0:
+        t2.value = 0.0
+    return max(t.value, t2.value)
+
+
+def reference_recall_sample(data, k, cfg, ids_gpu, sample, reference_ids=None):
+    import paper_2112_06630_b200 as kg
+    ex, _ = kg.brute_force_knng(data, k, queries=sample)
+    out = {"gpu": round(kg.recall(ids_gpu[sample], ex), 5), "sample_nodes": int(len(sample))}
+    if reference_ids is not None:
+        out["reference"] = round(kg.recall(reference_ids[sample], ex), 5)
+    return out
+
+
+def run_ours(args, rank, world, local):
+    import torch
+    import paper_2112_06630_b200 as kg
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    cfg = datasets.CONFIGS[args.config]
+    # replicas: each rank builds its own seeded instance
+    cfg_r = datasets.Config(cfg.name, cfg.n, cfg.d, cfg.k, cfg.cap, cfg.delta, cfg.seed + rank,
+                            cfg.description)
+    data = datasets.generate(cfg_r)
+    n, d = data.shape
+    k, cap = cfg.k, cfg.cap
+    params = kg.RunParams(k=k, max_candidates=cap, termination_delta=cfg.delta, seed=cfg_r.seed,
+                          device=local, profile=True)
+    peak = ffma_peak_tflops(local)
+
+    d_data = torch.from_numpy(data).to(f"cuda:{local}")
+    d_ids = torch.empty((n, k), dtype=torch.int32, device=f"cuda:{local}")
+    d_dists = torch.empty((n, k), dtype=torch.float32, device=f"cuda:{local}")
+    stream = torch.cuda.current_stream().cuda_stream
+
+    def step():
+        return kg.run_device(d_data.data_ptr(), n, d, params, d_ids.data_ptr(),
+                             d_dists.data_ptr(), stream=stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clocks = Clocks(local)
+    clocks.start()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    mets = [step() for _ in range(args.steps)]
+    e1.record()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    evals = sum(m.total_dist_evals for m in mets)
+    iters = sum(len(m.iterations) - 1 for m in mets)
+    join_ms = sum(m.kernel_ms["join"] for m in mets)
+    join_launches = sum(m.kernel_launches["join"] for m in mets)
+    join_evals = sum(m.join_evals for m in mets)
+    join_cands = sum(m.join_candidates for m in mets)
+    launches = sum(2 + 5 * (len(m.iterations) - 1) for m in mets)
+    kernel_ms = {kname: sum(m.kernel_ms[kname] for m in mets) for kname in mets[0].kernel_ms}
+
+    # ---- e2e through the host-pointer C-ABI (pinned host data, graph back to host)
+    pinned = torch.empty((n, d), dtype=torch.float32, pin_memory=True)
+    pinned.numpy()[:] = data
+    host = pinned.numpy()
+    hp = kg.RunParams(k=k, max_candidates=cap, termination_delta=cfg.delta, seed=cfg_r.seed,
+                      device=local)
+    res = kg.run(host, hp)  # warm
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    e2e_evals = 0
+    h2d = d2h = 0
+    for _ in range(args.steps):
+        res = kg.run(host, hp)
+        e2e_evals += res.metrics.total_dist_evals
+        h2d += res.metrics.h2d_bytes
+        d2h += res.metrics.d2h_bytes
+    e2e_s = time.perf_counter() - t0
+
+    if dist:
+        t = torch.tensor([ms, e2e_s], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, e2e_s = float(t[0]), float(t[1])
+        c = torch.tensor([evals, e2e_evals], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(c, op=dist.ReduceOp.SUM)
+        evals_all, e2e_all = float(c[0]), float(c[1])
+    else:
+        evals_all, e2e_all = float(evals), float(e2e_evals)
+
+    out = None
+    if rank == 0:
+        stride = (d + 7) // 8 * 8
+        F = join_evals * (3 * d - 1)
+        Q = join_cands * (4 * stride + 8) + 12 * n * k * iters
+        t_join = join_ms * 1e-3
+        beta = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
+            if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+        pi = peak or 74.0
+        fp32_time = F / (pi * 1e12)
+        hbm_time = Q / (beta * 1e9)
+        traffic = None
+        if os.path.exists(PROFILE_TRAFFIC):
+            try:
+                traffic = json.load(open(PROFILE_TRAFFIC)).get(args.config)
+            except (OSError, ValueError):
+                traffic = None
+        if fp32_time >= hbm_time:
+            roof = {"bound": "fp32", "achieved": round(F / t_join / 1e12, 3), "peak": round(pi, 2),
+                    "unit": "TFLOP/s", "frac": round(F / t_join / 1e12 / pi, 4),
+                    "traffic": traffic,
+                    "peak_source": "measured FFMA microbenchmark (libknng_diag)" if peak else
+                    "fallback 74 TFLOP/s nominal"}
+        else:
+            roof = {"bound": "hbm", "achieved": round(Q / t_join / 1e9, 1), "peak": beta,
+                    "unit": "GB/s", "frac": round(Q / t_join / 1e9 / beta, 4), "traffic": traffic,
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+        roof.update({"kernel": "join_kernel (local join: distances + locked merges)",
+                     "algorithmic_flops_per_launch": int(F / max(1, join_launches)),
+                     "algorithmic_bytes_per_launch": int(Q / max(1, join_launches)),
+                     "avg_launch_ms": round(join_ms / max(1, join_launches), 4),
+                     "launches": int(join_launches),
+                     "share_of_step": round(join_ms / ms, 3)})
+
+        # matched recall on a node sample vs the reference (same data, same seed)
+        sample = np.random.default_rng(1).choice(n, size=min(n, args.recall_sample),
+                                                 replace=False).astype(np.uint32)
+        ids_gpu = d_ids.cpu().numpy().astype(np.uint32)
+        cpu_baseline = None
+        ref_ids = None
+        if world == 1 and not args.no_cpu_baseline:
+            import oracle
+            kind = "reference" if oracle.available("reference") else "restated"
+            O = oracle.load(kind)
+            r = O.run(data, k=k, cap=cap, delta=cfg.delta, seed=cfg_r.seed)
+            ref_ids = r.graph.ids
+            cpu_baseline = {"value": round(r.total_evals / r.total_wall, 1), "unit": UNIT,
+                            "cores": 1, "kind": "reference" if kind == "reference" else "port",
+                            "sample": f"one full {cfg.name} build (n={n}, d={d}, k={k}, cap={cap}), "
+                                      f"{r.iterations} iterations, {r.total_wall:.2f} s "
+                                      "RunMetrics.total_wall_time_s, single-threaded by contract",
+                            "build_time_s": round(r.total_wall, 3)}
+        rec = reference_recall_sample(data, k, cfg, ids_gpu, sample, ref_ids)
+        builds = args.steps * world
+        out = {
+            "metric": METRIC, "value": round(evals_all / (ms * 1e-3), 1), "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{cfg.name}: {cfg.description}", "n": n, "d": d, "k": k,
+                       "max_candidates": cap, "delta": cfg.delta, "seed": cfg.seed,
+                       "step": "one complete K-NNG build (init + iterations to termination)",
+                       "l2": "inputs larger than L2 (data %.1f MB > 126 MB)" % (n * d * 4 / 1e6),
+                       "parallelism": "replicas" if world > 1 else "single-gpu"},
+            "build_time_ms": round(ms / args.steps, 3),
+            "iterations_per_s": round(iters * world / (ms * 1e-3), 2),
+            "iterations_per_build": round(iters / args.steps, 2),
+            "recall_at_k": rec,
+            "e2e": {"value": round(e2e_all / e2e_s, 1), "unit": UNIT,
+                    "h2d_bytes_per_step": int(h2d / args.steps),
+                    "d2h_bytes_per_step": int(d2h / args.steps),
+                    "build_time_ms": round(e2e_s * 1e3 / args.steps, 3)},
+            "gpu_launches": int(launches),
+            "kernel_ms_per_step": {kk: round(v / args.steps, 3) for kk, v in kernel_ms.items()},
+            "roofline": roof,
+            "cpu_baseline": cpu_baseline,
+            "clocks": clk,
+            "builds_timed": builds,
+        }
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return out
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    import oracle
+    cfg = datasets.CONFIGS[args.config]
+    kind = "reference" if oracle.available("reference") else "restated"
+    O = oracle.load(kind)
+    data = datasets.generate(cfg)
+    n_s = min(cfg.n, args.reference_sample)
+    sample = data[:n_s]
+    for _ in range(args.warmup):
+        O.run(sample, k=cfg.k, cap=cfg.cap, delta=cfg.delta, seed=cfg.seed)
+    evals = 0
+    wall = 0.0
+    iters = 0
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        r = O.run(sample, k=cfg.k, cap=cfg.cap, delta=cfg.delta, seed=cfg.seed)
+        evals += r.total_evals
+        wall += r.total_wall
+        iters += r.iterations
+    elapsed = time.perf_counter() - t0
+    value = evals / wall
+    return {
+        "impl": "reference", "metric": METRIC, "value": round(value, 1), "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(wall * 1e3 / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: {cfg.description}", "n": cfg.n, "d": cfg.d,
+                   "k": cfg.k, "max_candidates": cfg.cap, "delta": cfg.delta,
+                   "sample_rows": n_s},
+        "cpu_baseline": {"value": round(value, 1), "unit": UNIT, "cores": 1,
+                         "kind": "reference" if kind == "reference" else "port",
+                         "sample": f"first {n_s} rows of {cfg.name}, full knng::run per step "
+                                   f"({iters / args.steps:.1f} iterations); the reference is "
+                                   "single-threaded by contract (SPEC.md:375)"},
+        "e2e": {"value": round(value, 1), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "wall_s": round(elapsed, 2),
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="C2", choices=sorted(datasets.CONFIGS))
+    ap.add_argument("--recall-sample", type=int, default=5000)
+    ap.add_argument("--reference-sample", type=int, default=10000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 0)
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        out = run_reference(args, rank, world)
+    else:
+        out = run_ours(args, rank, world, local)
+    if out is not None and rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -80,13 +80,15 @@ typedef struct knng_cuda_iteration {
 
 /* Per-kernel device time (CUDA events on the library's stream), filled when
  * params.profile != 0.  Index with the KNNG_CUDA_KERNEL_* constants. */
-#define KNNG_CUDA_KERNEL_INIT 0
-#define KNNG_CUDA_KERNEL_DEGREE 1
-#define KNNG_CUDA_KERNEL_SAMPLE 2
-#define KNNG_CUDA_KERNEL_FINALIZE 3
-#define KNNG_CUDA_KERNEL_JOIN 4
-#define KNNG_CUDA_KERNEL_REORDER 5
-#define KNNG_CUDA_KERNEL_COUNT 6
+#define KNNG_CUDA_KERNEL_INIT 0      /* init_random */
+#define KNNG_CUDA_KERNEL_DEGREE 1    /* in-degree histogram */
+#define KNNG_CUDA_KERNEL_SAMPLE 2    /* turbo offers */
+#define KNNG_CUDA_KERNEL_FINALIZE 3  /* dedup, flag_consumed, join bookkeeping */
+#define KNNG_CUDA_KERNEL_JOIN 4      /* local-join distance kernel */
+#define KNNG_CUDA_KERNEL_REORDER 5   /* locality permutation + gathers */
+#define KNNG_CUDA_KERNEL_MERGE 6     /* bounded sorted-list updates */
+#define KNNG_CUDA_KERNEL_INDEX 7     /* block offsets + reverse index */
+#define KNNG_CUDA_KERNEL_COUNT 8
 
 /* knng::RunMetrics (descent.hpp:45-68) plus device-side accounting.  The
  * caller provides `iterations` with room for `capacity` rows

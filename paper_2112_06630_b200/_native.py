@@ -23,7 +23,7 @@ NOT_IMPLEMENTED = 5
 MAX_K = 32
 MAX_CANDIDATES = 64
 
-KERNEL_NAMES = ("init", "degree", "sample", "finalize", "join", "reorder")
+KERNEL_NAMES = ("init", "degree", "sample", "finalize", "join", "reorder", "merge", "index")
 
 # every symbol include/knng_cuda.h declares
 EXPORTS = (
@@ -74,8 +74,8 @@ class Metrics(C.Structure):
         ("total_wall_time_s", C.c_double),
         ("total_dist_evals", C.c_uint64),
         ("total_changes", C.c_uint64),
-        ("kernel_ms", C.c_double * 6),
-        ("kernel_launches", C.c_uint64 * 6),
+        ("kernel_ms", C.c_double * 8),
+        ("kernel_launches", C.c_uint64 * 8),
         ("join_candidates", C.c_uint64),
         ("join_evals", C.c_uint64),
         ("h2d_bytes", C.c_uint64),

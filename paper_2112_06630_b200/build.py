@@ -19,8 +19,13 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(PKG, "build")
 LIB = os.path.join(PKG, "lib", "libknng_cuda.so")
+DIAG = os.path.join(PKG, "lib", "libknng_diag.so")  # FFMA peak probe (bench only)
 SOURCES = ["graph_kernels.cu", "join.cu", "bruteforce.cu", "reorder.cu", "api.cu"]
 HEADERS = ["common.cuh", "kernels.cuh"]
+# join.cu: no FMA contraction anywhere, so the unfused (multiply, then add)
+# distance path stays unfused at the SASS level; explicit fma intrinsics are
+# unaffected (SURVEY.md §8a-6 bit-exactness)
+PER_FILE = {"join.cu": ["--fmad=false"]}
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
          "-I", os.path.join(ROOT, "include")]
@@ -50,7 +55,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
         o = os.path.join(OBJ, src.replace(".cu", ".o"))
         objs.append(o)
         if force or _stale(o, [s] + hdrs):
-            cmd = [nvcc(), *ARCH, *FLAGS, "-c", s, "-o", o]
+            cmd = [nvcc(), *ARCH, *FLAGS, *PER_FILE.get(src, []), "-c", s, "-o", o]
             if verbose:
                 cmd.insert(1, "-Xptxas=-v")
                 print(" ".join(cmd), flush=True)
@@ -59,6 +64,10 @@ def build(verbose: bool = False, force: bool = False) -> str:
         cmd = [nvcc(), *ARCH, "-shared", "-o", LIB, *objs, "-cudart", "static"]
         if verbose:
             print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+    diag_src = os.path.join(CSRC, "diag.cu")
+    if force or _stale(DIAG, [diag_src]):
+        cmd = [nvcc(), *ARCH, *FLAGS, "-shared", "-o", DIAG, diag_src, "-cudart", "static"]
         subprocess.run(cmd, check=True)
     return LIB
 

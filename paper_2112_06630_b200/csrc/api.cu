@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <new>
 #include <random>
 #include <string>
 #include <vector>
@@ -133,39 +134,44 @@ struct StreamHolder {
 struct KernelTimer {
     bool on;
     cudaStream_t s;
-    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> open;
+    std::vector<cudaEvent_t> pool;       // reused across flushes
+    std::vector<std::pair<int, size_t>> open;  // (kernel, first event index)
+    size_t used = 0;
     knng_cuda_metrics* m;
     KernelTimer(bool enabled, cudaStream_t stream, knng_cuda_metrics* metrics)
         : on(enabled && metrics), s(stream), m(metrics) {}
+    cudaEvent_t next() {
+        if (used == pool.size()) {
+            cudaEvent_t e;
+            CK(cudaEventCreate(&e));
+            pool.push_back(e);
+        }
+        return pool[used++];
+    }
     int begin(int kernel) {
         if (!on) return -1;
-        cudaEvent_t a, b;
-        CK(cudaEventCreate(&a));
-        CK(cudaEventCreate(&b));
-        CK(cudaEventRecord(a, s));
-        open.push_back({kernel, {a, b}});
+        const size_t i = used;
+        CK(cudaEventRecord(next(), s));
+        next();
+        open.push_back({kernel, i});
         return int(open.size()) - 1;
     }
     void end(int h) {
         if (h < 0) return;
-        CK(cudaEventRecord(open[size_t(h)].second.second, s));
+        CK(cudaEventRecord(pool[open[size_t(h)].second + 1], s));
     }
     void flush() {  // after a stream sync
         for (auto& e : open) {
             float ms = 0.0f;
-            CK(cudaEventElapsedTime(&ms, e.second.first, e.second.second));
+            CK(cudaEventElapsedTime(&ms, pool[e.second], pool[e.second + 1]));
             m->kernel_ms[e.first] += ms;
             m->kernel_launches[e.first] += 1;
-            cudaEventDestroy(e.second.first);
-            cudaEventDestroy(e.second.second);
         }
         open.clear();
+        used = 0;
     }
     ~KernelTimer() {
-        for (auto& e : open) {
-            cudaEventDestroy(e.second.first);
-            cudaEventDestroy(e.second.second);
-        }
+        for (cudaEvent_t e : pool) cudaEventDestroy(e);
     }
 };
 
@@ -200,7 +206,15 @@ struct Engine {
     cudaMemPool_t pool;
     DevBuf<float> data, maxd;
     DevBuf<uint64_t> keys;
-    DevBuf<uint32_t> flags, locks, indeg, cand, raw_new, raw_old, nc, oc, active;
+    DevBuf<uint32_t> flags, indeg, cand, raw_new, raw_old, nc, oc, active;
+    DevBuf<uint64_t> dsz, doff;
+    DevBuf<uint32_t> revcnt, roff, rcur;
+    DevBuf<unsigned char> scan_tmp;
+    size_t scan_bytes = 0;
+    // grow-only per-iteration buffers: reverse index and distance blocks
+    DevBuf<uint64_t> rev;
+    DevBuf<float> dblocks;
+    size_t rev_cap = 0, d_cap = 0;
     DevBuf<IterCounters> ctr;
     IterCounters* h_ctr = nullptr;
     uint64_t h2d = 0, d2h = 0;
@@ -212,7 +226,6 @@ struct Engine {
         keys.alloc(size_t(n) * k, pool, s);
         flags.alloc(n, pool, s);
         maxd.alloc(n, pool, s);
-        locks.alloc(n, pool, s);
         indeg.alloc(n, pool, s);
         ctr.alloc(1, pool, s);
         if (cap) {
@@ -222,19 +235,41 @@ struct Engine {
             nc.alloc(n, pool, s);
             oc.alloc(n, pool, s);
             active.alloc(n, pool, s);
+            dsz.alloc(n, pool, s);
+            doff.alloc(n, pool, s);
+            revcnt.alloc(n, pool, s);
+            roff.alloc(n, pool, s);
+            rcur.alloc(n, pool, s);
+            scan_bytes = join_scan_scratch(n);
+            scan_tmp.alloc(scan_bytes, pool, s);
         }
         CK(cudaMallocHost(reinterpret_cast<void**>(&h_ctr), sizeof(IterCounters)));
-        CK(cudaMemsetAsync(locks.p, 0, sizeof(uint32_t) * n, s));
         CK(cudaMemsetAsync(ctr.p, 0, sizeof(IterCounters), s));
     }
     ~Engine() {
         if (h_ctr) cudaFreeHost(h_ctr);
     }
 
-    GraphView gv() const {
-        return GraphView{data.p, n, k, stride, keys.p, flags.p, maxd.p, locks.p};
+    GraphView gv() const { return GraphView{data.p, n, k, stride, keys.p, flags.p, maxd.p}; }
+    CandView cv() const {
+        return CandView{cap,   cand.p,   raw_new.p, raw_old.p, nc.p, oc.p, dsz.p,
+                        doff.p, revcnt.p, roff.p,   rcur.p,    rev.p, dblocks.p};
     }
-    CandView cv() const { return CandView{cap, cand.p, raw_new.p, raw_old.p, nc.p, oc.p}; }
+
+    void reserve_join(uint64_t rev_entries, uint64_t dfloats) {
+        if (rev_entries > rev_cap) {
+            rev.~DevBuf();
+            new (&rev) DevBuf<uint64_t>();
+            rev_cap = rev_entries + rev_entries / 4 + 1024;
+            rev.alloc(rev_cap, pool, s);
+        }
+        if (dfloats > d_cap) {
+            dblocks.~DevBuf();
+            new (&dblocks) DevBuf<float>();
+            d_cap = dfloats + dfloats / 4 + 4096;
+            dblocks.alloc(d_cap, pool, s);
+        }
+    }
 
     // Rows padded to ceil8(d) with zeros (dataset.hpp:72-77).
     void upload(const float* src, bool src_on_device) {
@@ -268,9 +303,25 @@ struct Engine {
         CK(cudaGetLastError());
     }
 
-    void join(KernelTimer& timer) {
-        const int h = timer.begin(KNNG_CUDA_KERNEL_JOIN);
-        launch_join(gv(), cv(), active.p, n, ctr.p, s);
+    // The local join after finalize/bookkeeping: read the counters (active
+    // nodes, block and index sizes), size the buffers, build offsets and the
+    // reverse index, then the distance and merge stages.
+    void join(KernelTimer& timer, bool distances_only = false) {
+        read_counters();
+        const IterCounters c0 = *h_ctr;
+        if (c0.active == 0) return;
+        reserve_join(c0.rev, c0.dfloats);
+        int h = timer.begin(KNNG_CUDA_KERNEL_INDEX);
+        launch_join_offsets(cv(), n, scan_tmp.p, scan_bytes, s);
+        launch_scatter_rev(cv(), active.p, ctr.p, c0.active, n, s);
+        timer.end(h);
+        h = timer.begin(KNNG_CUDA_KERNEL_JOIN);
+        launch_join_distances(gv(), cv(), active.p, ctr.p, c0.active, s);
+        timer.end(h);
+        CK(cudaGetLastError());
+        if (distances_only) return;
+        h = timer.begin(KNNG_CUDA_KERNEL_MERGE);
+        launch_join_merge(gv(), cv(), ctr.p, s);
         timer.end(h);
         CK(cudaGetLastError());
     }
@@ -529,24 +580,12 @@ int knng_cuda_local_join(const float* data, uint32_t n, uint32_t d, uint32_t k, 
                            cudaMemcpyHostToDevice, e.s));
         CK(cudaMemcpyAsync(e.nc.p, new_counts, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, e.s));
         CK(cudaMemcpyAsync(e.oc.p, old_counts, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, e.s));
-        // active list + eval count from the injected counts (finalize's bookkeeping)
-        std::vector<uint32_t> act;
-        uint64_t ev = 0;
-        for (uint32_t u = 0; u < n; ++u)
-            if (new_counts[u] > 0) {
-                act.push_back(u);
-                ev += uint64_t(new_counts[u]) * (new_counts[u] - 1) / 2 +
-                      uint64_t(new_counts[u]) * old_counts[u];
-            }
-        IterCounters hc = {};
-        hc.active = uint32_t(act.size());
-        CK(cudaMemcpyAsync(e.ctr.p, &hc, sizeof hc, cudaMemcpyHostToDevice, e.s));
-        if (!act.empty())
-            CK(cudaMemcpyAsync(e.active.p, act.data(), sizeof(uint32_t) * act.size(),
-                               cudaMemcpyHostToDevice, e.s));
+        // finalize's bookkeeping on the injected lists, then the join stages
+        launch_bookkeeping(e.gv(), e.cv(), e.active.p, e.ctr.p, e.s);
         KernelTimer timer(false, e.s, nullptr);
         e.join(timer);
         e.read_counters();
+        const uint64_t ev = e.h_ctr->evals;
         e.export_rows(ids.p, dists.p, fl.p);
         to_host(out_ids, ids.p, nk, e);
         to_host(out_dists, dists.p, nk, e);
@@ -588,24 +627,23 @@ int knng_cuda_candidate_distances(const float* data, uint32_t n, uint32_t d, uin
                            cudaMemcpyHostToDevice, e.s));
         CK(cudaMemcpyAsync(e.nc.p, new_counts, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, e.s));
         CK(cudaMemcpyAsync(e.oc.p, old_counts, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, e.s));
-        std::vector<uint32_t> act;
-        for (uint32_t u = 0; u < n; ++u)
-            if (new_counts[u] > 0) act.push_back(u);
-        IterCounters hc = {};
-        hc.active = uint32_t(act.size());
-        CK(cudaMemcpyAsync(e.ctr.p, &hc, sizeof hc, cudaMemcpyHostToDevice, e.s));
-        if (!act.empty())
-            CK(cudaMemcpyAsync(e.active.p, act.data(), sizeof(uint32_t) * act.size(),
-                               cudaMemcpyHostToDevice, e.s));
-        DevBuf<uint64_t> off;
-        DevBuf<float> out;
-        to_device(off, offsets, n, e);
-        out.alloc(total, e.pool, e.s);
-        CK(cudaMemcpyAsync(out.p, out_dists, sizeof(float) * total, cudaMemcpyHostToDevice, e.s));
-        launch_join_distances(e.gv(), e.cv(), e.active.p, n, off.p, out.p, e.s, e.ctr.p);
-        CK(cudaGetLastError());
-        to_host(out_dists, out.p, total, e);
+        launch_bookkeeping(e.gv(), e.cv(), e.active.p, e.ctr.p, e.s);
+        KernelTimer timer(false, e.s, nullptr);
+        e.join(timer, /*distances_only=*/true);
+        // the first nn*m floats of each distance block are the nn x m matrix
+        const uint64_t dtotal = e.h_ctr->dfloats;
+        std::vector<float> blocks(dtotal);
+        std::vector<uint64_t> doff(n);
+        if (dtotal) to_host(blocks.data(), e.dblocks.p, dtotal, e);
+        to_host(doff.data(), e.doff.p, n, e);
         CK(cudaStreamSynchronize(e.s));
+        for (uint32_t u = 0; u < n; ++u) {
+            const uint64_t nn = new_counts[u], m = nn + old_counts[u];
+            if (!nn) continue;
+            for (uint64_t i = 0; i < nn; ++i)
+                for (uint64_t j = 0; j < m; ++j)
+                    if (j != i) out_dists[offsets[u] + i * m + j] = blocks[doff[u] + i * m + j];
+        }
     });
 }
 

@@ -92,7 +92,6 @@ __global__ void __launch_bounds__(256) init_random_kernel(GraphView g, uint32_t 
     if (lane == 0) {
         g.flags[u] = full_mask_k(k);
         g.maxd[u] = key_dist(last);
-        g.locks[u] = 0u;
     }
 }
 
@@ -124,7 +123,6 @@ __global__ void __launch_bounds__(256) load_rows_kernel(GraphView g, const uint3
     if (lane == 0) {
         g.flags[u] = mask;
         g.maxd[u] = key_dist(last);
-        g.locks[u] = 0u;
     }
 }
 
@@ -200,17 +198,52 @@ __global__ void reset_raw_kernel(CandView c, uint32_t n) {
 constexpr uint32_t kFinWarps = 8;
 constexpr uint32_t kTomb = 0xffffffffu;
 
+struct BlockCounters {
+    unsigned long long evals, cands, dfloats, rev;
+};
+
+// The join's per-node accounting (one full warp): evaluation count
+// C(nn,2) + nn*no (acceptance.cpp:369-374), the size of the node's distance
+// block nn*(m + no) (join.cu), its entry in the active list, and one
+// reverse-index count for every candidate its lists name.
+__device__ __forceinline__ void join_bookkeeping(const CandView& c, uint32_t u, uint32_t nn,
+                                                 uint32_t no, uint32_t* active,
+                                                 IterCounters* ctr, BlockCounters& acc) {
+    const uint32_t lane = lane_id(), m = nn + no;
+    if (lane == 0) c.dsz[u] = nn ? uint64_t(nn) * (m + no) : 0ull;
+    if (nn == 0) return;
+    const uint32_t* list = c.ids + size_t(u) * 2 * c.cap;
+    for (uint32_t p = lane; p < m; p += 32) {
+        const uint32_t x = p < nn ? list[p] : list[c.cap + p - nn];
+        atomicAdd(c.revcnt + x, 1u);
+    }
+    if (lane == 0) {
+        atomicAdd(&acc.evals, (unsigned long long)nn * (nn - 1) / 2 + (unsigned long long)nn * no);
+        atomicAdd(&acc.cands, (unsigned long long)m);
+        atomicAdd(&acc.dfloats, (unsigned long long)nn * (m + no));
+        atomicAdd(&acc.rev, (unsigned long long)m);
+        active[atomicAdd(&ctr->active, 1u)] = u;
+    }
+}
+
+__device__ __forceinline__ void flush_block_counters(const BlockCounters& acc,
+                                                     IterCounters* ctr) {
+    if (threadIdx.x == 0) {
+        if (acc.evals) atomicAdd(&ctr->evals, acc.evals);
+        if (acc.cands) atomicAdd(&ctr->cands, acc.cands);
+        if (acc.dfloats) atomicAdd(&ctr->dfloats, acc.dfloats);
+        if (acc.rev) atomicAdd(&ctr->rev, acc.rev);
+    }
+}
+
 __global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(GraphView g, CandView c,
                                                                   uint32_t* active,
                                                                   IterCounters* ctr) {
     __shared__ uint32_t s_new[kFinWarps][kMaxCap];
     __shared__ uint32_t s_old[kFinWarps][kMaxCap];
     __shared__ uint32_t s_hid[kFinWarps][kMaxK];
-    __shared__ unsigned long long s_evals, s_cands;
-    if (threadIdx.x == 0) {
-        s_evals = 0;
-        s_cands = 0;
-    }
+    __shared__ BlockCounters acc;
+    if (threadIdx.x == 0) acc = BlockCounters{0, 0, 0, 0};
     __syncthreads();
     const uint32_t w = threadIdx.x >> 5, lane = lane_id();
     const uint32_t u = blockIdx.x * kFinWarps + w;
@@ -293,20 +326,25 @@ __global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(GraphView g, C
             c.nc[u] = nn;
             c.oc[u] = no;
             g.flags[u] = hflags & ~clear;
-            if (nn > 0) {
-                const unsigned long long ev =
-                    (unsigned long long)nn * (nn - 1) / 2 + (unsigned long long)nn * no;
-                atomicAdd(&s_evals, ev);
-                atomicAdd(&s_cands, (unsigned long long)(nn + no));
-                active[atomicAdd(&ctr->active, 1u)] = u;
-            }
         }
+        join_bookkeeping(c, u, nn, no, active, ctr, acc);
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        if (s_evals) atomicAdd(&ctr->evals, s_evals);
-        if (s_cands) atomicAdd(&ctr->cands, s_cands);
-    }
+    flush_block_counters(acc, ctr);
+}
+
+// Bookkeeping only, for candidate lists supplied from outside (the
+// fixed-state local-join entry): same accounting as finalize.
+__global__ void __launch_bounds__(kFinWarps * 32) bookkeeping_kernel(GraphView g, CandView c,
+                                                                     uint32_t* active,
+                                                                     IterCounters* ctr) {
+    __shared__ BlockCounters acc;
+    if (threadIdx.x == 0) acc = BlockCounters{0, 0, 0, 0};
+    __syncthreads();
+    const uint32_t u = blockIdx.x * kFinWarps + (threadIdx.x >> 5);
+    if (u < g.n) join_bookkeeping(c, u, c.nc[u], c.oc[u], active, ctr, acc);
+    __syncthreads();
+    flush_block_counters(acc, ctr);
 }
 
 inline uint32_t blocks_for(size_t items, uint32_t per_block) {
@@ -347,7 +385,14 @@ void launch_sample(const GraphView& g, const CandView& c, const uint32_t* indeg,
 
 void launch_finalize(const GraphView& g, const CandView& c, uint32_t* active,
                      IterCounters* ctr, cudaStream_t s) {
+    cudaMemsetAsync(c.revcnt, 0, sizeof(uint32_t) * g.n, s);
     finalize_kernel<<<blocks_for(g.n, kFinWarps), kFinWarps * 32, 0, s>>>(g, c, active, ctr);
+}
+
+void launch_bookkeeping(const GraphView& g, const CandView& c, uint32_t* active,
+                        IterCounters* ctr, cudaStream_t s) {
+    cudaMemsetAsync(c.revcnt, 0, sizeof(uint32_t) * g.n, s);
+    bookkeeping_kernel<<<blocks_for(g.n, kFinWarps), kFinWarps * 32, 0, s>>>(g, c, active, ctr);
 }
 
 }  // namespace knng_cuda

@@ -1,97 +1,334 @@
-// The local join (compute_step, reference descent.hpp:82-153) on sm_100a.
+// The local join (compute_step, reference descent.hpp:82-153) on sm_100a, in
+// two stages per iteration.
 //
-// One CTA owns one active node u at a time (persistent grid, nodes handed out
-// by an atomic work counter).  For u's new list N (nn ids) and old list O (no
-// ids) it
-//   1. evaluates every new x new unordered pair and every new x old pair
-//      (the same C(nn,2) + nn*no evaluations as compute_step) into a
-//      distance matrix D in shared memory, and then
-//   2. for every candidate t in N u O gathers the partners whose distance
-//      beats t's cached row maximum (the stale-upwards prefilter of
-//      descent.hpp:97-102,134-147) and merges them into t's bounded sorted
-//      row under t's lock with try_insert's semantics (graph.hpp:116-129):
-//      strict improvement over the current maximum, id dedup, evict the max.
+// 1. join_distances_kernel — the FP32 hot loop.  One CTA (128 threads = 16
+//    groups of 8) evaluates, for one active node u at a time, every
+//    new x new unordered pair and every new x old pair of u's candidate lists
+//    (the same C(nn,2) + nn*no evaluations as compute_step) and writes them
+//    to u's distance block in HBM.  Candidate rows stream through shared
+//    memory in 32-float slabs (cp.async, double-buffered); each group owns an
+//    8x8 pair tile, thread l8 of the group being reference lane l8.
+// 2. join_merge_kernel — the bounded list updates.  One warp per target t
+//    walks the reverse index (every (u, position) whose lists name t), reads
+//    t's row of each distance block, and inserts the partners that beat t's
+//    current maximum into t's sorted row with try_insert's semantics
+//    (graph.hpp:116-129: strict improvement, id dedup, evict the max).  A
+//    target is owned by exactly one warp, so there are no locks and no
+//    atomics on graph rows; the result is the reference's (the k smallest
+//    distinct candidates, order-invariant up to exact ties).
 //
 // Distances are bit-identical to the reference's compiled kernels.  The
 // reference sums (a_j - b_j)^2 in eight strided lanes (lane l owns elements
 // 8c + l) and reduces them as ((0+1)+(2+3))+((4+5)+(6+7)) (distance.hpp:29-51).
-// Pairs that fall into a full 5x5 or triangular tile (block_core /
-// tri_core5) are accumulated with a fused multiply-add, the rest (remainder
-// rows of mutual_block_distances, partial new x old tiles) unfused
-// (pinned in tests/test_oracle_pins.py).  Here a group of 8
-// threads is one pair-tile and thread l8 of the group is reference lane l8:
-// it accumulates elements 8c + l8 of a 4x4 pair tile with the path of each
-// pair, and the group combines lanes with shfl_xor 1, 2, 4 — exactly the
-// reference tree — as a reduce-scatter (14 shuffles for 16 pairs).
+// Pairs inside a full 5x5 or triangular tile (block_core / tri_core5) are
+// accumulated with a fused multiply-add, the rest (remainder rows of
+// mutual_block_distances, partial new x old tiles) unfused (
+// pinned in tests/test_oracle_pins.py).  Rows and columns of u's pair matrix
+// are laid out in "slots" so that every 8x8 tile is entirely fused or entirely
+// unfused: rows = [new 0..fullN) pad8 [new fullN..nn) pad8, columns =
+// [new 0..fullN) [old 0..fullO) pad8 [new fullN..nn) [old fullO..no) pad8,
+// with fullN = nn - nn%5, fullO = no - no%5.  Zero padding of the last slab is
+// exact (0 - 0 contributes +0 to either form).
+//
+// Distance block of u (nn new, no old, m = nn + no candidates), nn*(m + no)
+// floats at doff[u]: row r < nn (new r) holds m entries indexed by combined
+// position (new j, then old at nn + j'); row r >= nn (old r - nn) holds nn
+// entries indexed by new position.  Every pair is written to both rows.
+#include <cub/device/device_scan.cuh>
+
 #include "kernels.cuh"
 
 namespace knng_cuda {
 
 namespace {
 
-constexpr uint32_t kTileR = 4;
-constexpr uint32_t kTileC = 4;
-constexpr uint32_t kTilePairs = kTileR * kTileC;
+constexpr uint32_t kThreads = 128;       // 4 warps, 16 groups of 8 lanes
+constexpr uint32_t kGroups = kThreads / 8;
+constexpr uint32_t kSlab = 32;           // floats per row per smem stage
+constexpr uint32_t kStages = 3;          // cp.async pipeline depth
+constexpr uint32_t kMaxM = 2 * kMaxCap;  // candidates per node
+constexpr uint32_t kMaxRowSlots = kMaxCap + 16;
+constexpr uint32_t kMaxColSlots = kMaxM + 16;
+constexpr uint32_t kMaxTiles = (kMaxRowSlots / 8) * (kMaxColSlots / 8) + 4;
+constexpr uint16_t kDeadTile = 0xffffu;
+constexpr uint32_t kInvalid = 0xffu;
 
-enum TileMode : int { kFused = 0, kUnfused = 1, kMixed = 2 };
+// Candidate rows are staged in COLUMN-slot order (every candidate has a column
+// slot; a new candidate's row slot maps to a column slot of the same 8-block
+// offset, see a_block below), 32 floats per row per stage.  The four 8-float
+// segments of a row are XOR-swizzled by the row's 8-block index so that the
+// four 8-lane groups of a warp, reading the same element of rows from
+// different 8-blocks, hit four different bank octets.
+struct DistShared {
+    float slab[kStages][kMaxColSlots * kSlab];
+    uint32_t colrow[kMaxColSlots];   // col slot -> data row id (0xffffffff: padding)
+    uint8_t rowmap[kMaxRowSlots];    // row slot -> new index
+    uint8_t colmap[kMaxColSlots];    // col slot -> combined index
+    uint16_t tiles[kMaxTiles];       // (rb << 8) | cb, in (rb, cb) order
+    uint32_t n_tiles;
+    uint32_t node;
+};
 
-template <int MODE>
-__device__ __forceinline__ void tile_accumulate(const float* const (&pa)[kTileR],
-                                                const float* const (&pb)[kTileC],
-                                                uint32_t stride, uint32_t l8,
-                                                float (&acc)[kTilePairs], uint32_t fused_mask) {
-#pragma unroll 2
-    for (uint32_t c = l8; c < stride; c += 8) {
-        float a[kTileR], b[kTileC];
+__device__ __forceinline__ void cp_async16(float* smem_dst, const float* gmem_src) {
+    const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(gmem_src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_0() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+__device__ __forceinline__ uint32_t swz(uint32_t slot, uint32_t seg) {
+    return slot * kSlab + ((seg ^ ((slot >> 3) & 3u)) << 3);
+}
+
+// Stage slab `s` (elements [32 s, 32 s + 32) of every column-slot row) into
+// buffer `buf` with 16-byte cp.async; chunks past the row stride are zero
+// (exact: they contribute +0 under either accumulation).
+__device__ __forceinline__ void stage_slab(DistShared& sh, const float* __restrict__ data,
+                                           uint32_t stride, uint32_t ncols, uint32_t s,
+                                           uint32_t buf) {
+    const uint32_t e0 = s * kSlab;
+    float* dst = sh.slab[buf];
+    for (uint32_t i = threadIdx.x; i < ncols * (kSlab / 4); i += kThreads) {
+        const uint32_t slot = i >> 3, j = i & 7u;
+        const uint32_t row = sh.colrow[slot];
+        if (row == 0xffffffffu) continue;
+        float* p = dst + swz(slot, j >> 1) + (j & 1u) * 4;
+        const uint32_t e = e0 + 4 * j;
+        if (e < stride)
+            cp_async16(p, data + size_t(row) * stride + e);
+        else
+            *reinterpret_cast<float4*>(p) = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+}
+
+// One 32-float slab of an 8x8 pair tile: rows of A-block a_blk against rows of
+// B-block b_blk; lane l8 accumulates elements 8 s + l8 (reference lane l8).
+// The packed FP32x2 pipe (FFMA2 / FMUL2 / FADD2, sm_100) evaluates two pairs
+// per instruction, each element with the scalar instruction's IEEE rounding:
+// diff = fma(b, -1, a) == a - b exactly (b * -1 is exact, one rounding), then
+// acc = fma(diff, diff, acc) on fused tiles or acc + (diff * diff) on unfused
+// ones.  acc[4 x + j] holds pairs (x, 2j) and (x, 2j + 1).
+template <bool kFusedTile>
+__device__ __forceinline__ void tile_slab(const float* __restrict__ slab, uint32_t a_blk,
+                                          uint32_t b_blk, uint32_t l8, float2 (&acc)[32]) {
+    const float2 minus_one = make_float2(-1.0f, -1.0f);
 #pragma unroll
-        for (uint32_t x = 0; x < kTileR; ++x) a[x] = __ldg(pa[x] + c);
+    for (uint32_t s = 0; s < kSlab / 8; ++s) {
+        const float* pa = slab + swz(a_blk * 8, s) + l8;
+        const float* pb = slab + swz(b_blk * 8, s) + l8;
+        float a[8];
+        float2 b[4];
 #pragma unroll
-        for (uint32_t y = 0; y < kTileC; ++y) b[y] = __ldg(pb[y] + c);
+        for (uint32_t x = 0; x < 8; ++x) a[x] = pa[x * kSlab];
 #pragma unroll
-        for (uint32_t x = 0; x < kTileR; ++x) {
+        for (uint32_t j = 0; j < 4; ++j) {
+            b[j].x = pb[(2 * j) * kSlab];
+            b[j].y = pb[(2 * j + 1) * kSlab];
+        }
 #pragma unroll
-            for (uint32_t y = 0; y < kTileC; ++y) {
-                const uint32_t p = x * kTileC + y;
-                const float diff = __fsub_rn(a[x], b[y]);
-                if (MODE == kFused) {
-                    acc[p] = __fmaf_rn(diff, diff, acc[p]);
-                } else if (MODE == kUnfused) {
-                    acc[p] = __fadd_rn(acc[p], __fmul_rn(diff, diff));
-                } else {
-                    const float fused = __fmaf_rn(diff, diff, acc[p]);
-                    const float plain = __fadd_rn(acc[p], __fmul_rn(diff, diff));
-                    acc[p] = ((fused_mask >> p) & 1u) ? fused : plain;
+        for (uint32_t x = 0; x < 8; ++x) {
+            const float2 ax = make_float2(a[x], a[x]);
+#pragma unroll
+            for (uint32_t j = 0; j < 4; ++j) {
+                const float2 diff = __ffma2_rn(b[j], minus_one, ax);
+                if (kFusedTile)
+                    acc[4 * x + j] = __ffma2_rn(diff, diff, acc[4 * x + j]);
+                else
+                {
+                    // unfused: scalar FMUL then packed FADD2.  ptxas (CUDA 12.9)
+                    // contracts a packed mul.rn.f32x2 + add.rn.f32x2 pair into
+                    // FFMA2 even under --fmad=false; a scalar product feeding
+                    // the packed add stays two roundings (checked in SASS).
+                    float2 sq;
+                    sq.x = __fmul_rn(diff.x, diff.x);
+                    sq.y = __fmul_rn(diff.y, diff.y);
+                    acc[4 * x + j] = __fadd2_rn(acc[4 * x + j], sq);
                 }
             }
         }
     }
 }
 
-// Reduce-scatter of 16 per-lane partial sums over the 8 lanes of a group in
-// the reference's tree order.  Lane l8 = b0 + 2 b1 + 4 b2 ends with the full
-// sums of pairs base, base+1 where base = 8 b0 + 4 b1 + 2 b2.
-__device__ __forceinline__ void group_reduce(const float (&acc)[kTilePairs], uint32_t l8,
-                                             float (&out)[2]) {
+__device__ __forceinline__ float acc_at(const float2 (&acc)[32], uint32_t p) {
+    return (p & 1u) ? acc[p >> 1].y : acc[p >> 1].x;
+}
+
+// Reduce-scatter of the 64 per-lane partial sums over the group's 8 lanes in
+// the reference's tree order ((0+1)+(2+3))+((4+5)+(6+7)); lane
+// l8 = b0 + 2 b1 + 4 b2 ends with the 8 sums of tile row x = 4 b0 + 2 b1 + b2.
+__device__ __forceinline__ void group_reduce64(const float2 (&acc)[32], uint32_t l8,
+                                               float (&row)[8]) {
     const bool b0 = l8 & 1u, b1 = (l8 >> 1) & 1u, b2 = (l8 >> 2) & 1u;
-    float r8[8];
+    float r32[32];
+#pragma unroll
+    for (uint32_t j = 0; j < 32; ++j) {
+        const float send = b0 ? acc_at(acc, j) : acc_at(acc, 32 + j);
+        const float keep = b0 ? acc_at(acc, 32 + j) : acc_at(acc, j);
+        r32[j] = __fadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 1));
+    }
+    float r16[16];
+#pragma unroll
+    for (uint32_t j = 0; j < 16; ++j) {
+        const float send = b1 ? r32[j] : r32[16 + j];
+        const float keep = b1 ? r32[16 + j] : r32[j];
+        r16[j] = __fadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 2));
+    }
 #pragma unroll
     for (uint32_t j = 0; j < 8; ++j) {
-        const float send = b0 ? acc[j] : acc[8 + j];
-        const float keep = b0 ? acc[8 + j] : acc[j];
-        r8[j] = __fadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 1));
+        const float send = b2 ? r16[j] : r16[8 + j];
+        const float keep = b2 ? r16[8 + j] : r16[j];
+        row[j] = __fadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 4));
     }
-    float r4[4];
+}
+
+__global__ void __launch_bounds__(kThreads) join_distances_kernel(
+    GraphView g, CandView c, const uint32_t* __restrict__ active, IterCounters* ctr) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    DistShared& sh = *reinterpret_cast<DistShared*>(smem_raw);
+    const uint32_t tid = threadIdx.x, group = tid >> 3, l8 = tid & 7u;
+    const uint32_t stride = g.stride, cap = c.cap;
+    const uint32_t n_active = ctr->active;
+    const uint32_t n_slabs = (stride + kSlab - 1) / kSlab;
+
+    while (true) {
+        __syncthreads();
+        if (tid == 0) {
+            const uint32_t a = atomicAdd(&ctr->work, 1u);
+            sh.node = a < n_active ? active[a] : 0xffffffffu;
+        }
+        __syncthreads();
+        const uint32_t u = sh.node;
+        if (u == 0xffffffffu) break;
+        const uint32_t nn = c.nc[u], no = c.oc[u], m = nn + no;
+        const uint32_t fn = nn - nn % 5, fo = no - no % 5;
+        const uint32_t rf = (fn + 7) & ~7u, rs = (nn - fn + 7) & ~7u;
+        const uint32_t cf = (fn + fo + 7) & ~7u, cs = (nn - fn + no - fo + 7) & ~7u;
+        const uint32_t rbs = (rf + rs) / 8, cbs = (cf + cs) / 8;
+        const uint32_t* list = c.ids + size_t(u) * 2 * cap;
+        for (uint32_t sl = tid; sl < rf + rs; sl += kThreads) {
+            uint32_t v = kInvalid;
+            if (sl < fn) v = sl;
+            else if (sl >= rf && sl - rf < nn - fn) v = fn + (sl - rf);
+            sh.rowmap[sl] = uint8_t(v);
+        }
+        for (uint32_t sl = tid; sl < cf + cs; sl += kThreads) {
+            uint32_t v = kInvalid;
+            if (sl < fn) v = sl;
+            else if (sl < fn + fo) v = nn + (sl - fn);
+            else if (sl >= cf && sl - cf < nn - fn) v = fn + (sl - cf);
+            else if (sl >= cf + (nn - fn) && sl - cf - (nn - fn) < no - fo)
+                v = nn + fo + (sl - cf - (nn - fn));
+            sh.colmap[sl] = uint8_t(v);
+            sh.colrow[sl] = v == kInvalid ? 0xffffffffu : (v < nn ? list[v] : list[cap + v - nn]);
+        }
+        if (tid == 0) sh.n_tiles = 0;
+        __syncthreads();
+        // live tiles (any valid pair): fused tiles, padding to a whole warp
+        // (4 groups), then unfused tiles, so every warp runs one path; each
+        // phase in (rb, cb) order so a warp's groups mostly share the A block
+        __shared__ uint32_t warp_cnt[kThreads / 32];
+        for (uint32_t phase = 0; phase < 2; ++phase) {
+            for (uint32_t t0 = 0; t0 < rbs * cbs; t0 += kThreads) {
+                const uint32_t t = t0 + tid;
+                bool live = false;
+                if (t < rbs * cbs) {
+                    const uint32_t rb = t / cbs, cb = t % cbs;
+                    const bool fused_tile = rb * 8 < rf && cb * 8 < cf;
+                    if (fused_tile == (phase == 0)) {
+                        uint32_t imin = kInvalid;
+                        for (uint32_t x = 0; x < 8; ++x)
+                            imin = min(imin, uint32_t(sh.rowmap[rb * 8 + x]));
+                        if (imin != kInvalid)
+                            for (uint32_t y = 0; y < 8; ++y) {
+                                const uint32_t col = sh.colmap[cb * 8 + y];
+                                live |= col != kInvalid && (col >= nn || col > imin);
+                            }
+                    }
+                }
+                // order-preserving compaction: warp ballots + per-warp offsets
+                const uint32_t mask = __ballot_sync(0xffffffffu, live);
+                if ((tid & 31u) == 0) warp_cnt[tid >> 5] = __popc(mask);
+                __syncthreads();
+                uint32_t base = sh.n_tiles;
+                for (uint32_t w = 0; w < (tid >> 5); ++w) base += warp_cnt[w];
+                if (live) {
+                    const uint32_t rb = t / cbs, cb = t % cbs;
+                    sh.tiles[base + __popc(mask & ((1u << (tid & 31u)) - 1u))] =
+                        uint16_t((rb << 8) | cb);
+                }
+                __syncthreads();
+                if (tid == 0) {
+                    uint32_t tot = 0;
+                    for (uint32_t w = 0; w < kThreads / 32; ++w) tot += warp_cnt[w];
+                    sh.n_tiles += tot;
+                }
+                __syncthreads();
+            }
+            if (phase == 0) {  // pad the fused run to whole warps with dead tiles
+                const uint32_t nt = sh.n_tiles, padded = (nt + 3u) & ~3u;
+                if (tid < padded - nt) sh.tiles[nt + tid] = kDeadTile;
+                __syncthreads();
+                if (tid == 0) sh.n_tiles = padded;
+                __syncthreads();
+            }
+        }
+        const uint32_t n_tiles = sh.n_tiles;
+        const uint32_t ncols = cf + cs;
+        float* const D = c.D + c.doff[u];
+
+        for (uint32_t t0 = 0; t0 < n_tiles; t0 += kGroups) {
+            const uint32_t t = t0 + group;
+            const uint32_t tile0 = t < n_tiles ? sh.tiles[t] : kDeadTile;
+            const bool live = tile0 != kDeadTile;
+            const uint32_t tile = live ? tile0 : 0u;
+            const uint32_t rb = tile >> 8, cb = tile & 0xffu;
+            const bool fused = rb * 8 < rf && cb * 8 < cf;
+            // row slot block -> column slot block holding the same new candidates
+            const uint32_t a_blk = rb * 8 < rf ? rb : cf / 8 + (rb - rf / 8);
+            float2 acc[32];
 #pragma unroll
-    for (uint32_t j = 0; j < 4; ++j) {
-        const float send = b1 ? r8[j] : r8[4 + j];
-        const float keep = b1 ? r8[4 + j] : r8[j];
-        r4[j] = __fadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 2));
-    }
+            for (uint32_t p = 0; p < 32; ++p) acc[p] = make_float2(0.0f, 0.0f);
+
+            // 3-stage cp.async pipeline, one barrier per slab
+            for (uint32_t p = 0; p < kStages - 1; ++p) {
+                if (p < n_slabs) stage_slab(sh, g.data, stride, ncols, p, p);
+                cp_async_commit();
+            }
+            for (uint32_t s = 0; s < n_slabs; ++s) {
+                cp_async_wait_1();
+                __syncthreads();
+                if (s + kStages - 1 < n_slabs)
+                    stage_slab(sh, g.data, stride, ncols, s + kStages - 1,
+                               (s + kStages - 1) % kStages);
+                cp_async_commit();
+                const float* slab = sh.slab[s % kStages];
+                if (live) {
+                    if (fused)
+                        tile_slab<true>(slab, a_blk, cb, l8, acc);
+                    else
+                        tile_slab<false>(slab, a_blk, cb, l8, acc);
+                }
+            }
+            cp_async_wait_0();
+            __syncthreads();
+            float row[8];
+            group_reduce64(acc, l8, row);
+            const uint32_t x = 4u * (l8 & 1u) + 2u * ((l8 >> 1) & 1u) + ((l8 >> 2) & 1u);
+            const uint32_t i = live ? sh.rowmap[rb * 8 + x] : kInvalid;
+            if (i != kInvalid) {
 #pragma unroll
-    for (uint32_t j = 0; j < 2; ++j) {
-        const float send = b2 ? r4[j] : r4[2 + j];
-        const float keep = b2 ? r4[2 + j] : r4[j];
-        out[j] = __fadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 4));
+                for (uint32_t y = 0; y < 8; ++y) {
+                    const uint32_t col = sh.colmap[cb * 8 + y];
+                    if (col == kInvalid || !(col >= nn || col > i)) continue;
+                    D[size_t(i) * m + col] = row[y];
+                    if (col < nn)
+                        D[size_t(col) * m + i] = row[y];
+                    else
+                        D[size_t(nn) * m + size_t(col - nn) * nn + i] = row[y];
+                }
+            }
+        }
     }
 }
 
@@ -113,198 +350,117 @@ __device__ __forceinline__ bool warp_try_insert(uint64_t& key, uint32_t& flags, 
     return true;
 }
 
-struct JoinShared {
-    uint32_t node;
-    uint32_t nn, no;
-    unsigned long long changes;
-};
+constexpr uint32_t kMergeWarps = 8;
 
-template <uint32_t kThreads, bool kDistOnly>
-__global__ void __launch_bounds__(kThreads) join_kernel(GraphView g, CandView c,
-                                                        const uint32_t* __restrict__ active,
-                                                        uint32_t* work_counter,
-                                                        IterCounters* ctr,
-                                                        const uint64_t* offsets, float* out) {
-    constexpr uint32_t kWarps = kThreads / 32;
-    constexpr uint32_t kGroups = kThreads / 8;
-    extern __shared__ float s_D[];               // nn x m, m = nn + no (<= cap x 2cap)
-    __shared__ uint32_t s_ids[2 * kMaxCap];
-    __shared__ JoinShared sh;
-
-    const uint32_t tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
-    const uint32_t group = tid >> 3, l8 = tid & 7u;
-    const uint32_t k = g.k, cap = c.cap, stride = g.stride;
-    const uint32_t n_active = ctr->active;
-    if (tid == 0) sh.changes = 0;
-
-    while (true) {
-        __syncthreads();
-        if (tid == 0) {
-            const uint32_t a = atomicAdd(work_counter, 1u);
-            sh.node = a < n_active ? active[a] : 0xffffffffu;
-            if (a < n_active) {
-                sh.nn = c.nc[sh.node];
-                sh.no = c.oc[sh.node];
+__global__ void __launch_bounds__(kMergeWarps * 32) join_merge_kernel(GraphView g, CandView c,
+                                                                     IterCounters* ctr) {
+    __shared__ unsigned long long s_changes;
+    if (threadIdx.x == 0) s_changes = 0;
+    __syncthreads();
+    const uint32_t lane = lane_id();
+    const uint32_t t = blockIdx.x * kMergeWarps + (threadIdx.x >> 5);
+    const uint32_t k = g.k, cap = c.cap;
+    const uint32_t cnt = t < g.n ? c.revcnt[t] : 0u;
+    if (cnt) {
+        uint64_t key = lane < k ? g.keys[size_t(t) * k + lane] : kEmptyKey;
+        uint32_t flags = g.flags[t];
+        float cur_max = key_dist(__shfl_sync(0xffffffffu, key, k - 1));
+        uint32_t inserted = 0;
+        const uint64_t* rv = c.rev + c.roff[t];
+        for (uint32_t e0 = 0; e0 < cnt; e0 += 32) {
+            // metadata of 32 entries at once, one per lane
+            uint32_t mu = 0, mp = 0, mnn = 0, mm = 0;
+            uint64_t moff = 0;
+            if (e0 + lane < cnt) {
+                const uint64_t r = rv[e0 + lane];
+                mu = uint32_t(r >> 8);
+                mp = uint32_t(r & 0xffu);
+                mnn = c.nc[mu];
+                mm = mnn + c.oc[mu];
+                moff = c.doff[mu];
             }
-        }
-        __syncthreads();
-        const uint32_t u = sh.node;
-        if (u == 0xffffffffu) break;
-        const uint32_t nn = sh.nn, no = sh.no, m = nn + no;
-        const uint32_t* list = c.ids + size_t(u) * 2 * cap;
-        for (uint32_t i = tid; i < nn; i += kThreads) s_ids[i] = list[i];
-        for (uint32_t i = tid; i < no; i += kThreads) s_ids[nn + i] = list[cap + i];
-        __syncthreads();
-
-        // ---- 1. distances -------------------------------------------------
-        const uint32_t full_n = nn - nn % 5, full_o = no - no % 5;
-        const uint32_t rb = (nn + kTileR - 1) / kTileR, ob = (no + kTileC - 1) / kTileC;
-        const uint32_t t_nn = rb * (rb + 1) / 2, t_all = t_nn + rb * ob;
-        for (uint32_t t = group; t < t_all; t += kGroups) {
-            uint32_t bi, col0;
-            bool col_new;
-            if (t < t_nn) {
-                uint32_t tt = t;
-                bi = 0;
-                while (tt >= rb - bi) {
-                    tt -= rb - bi;
-                    ++bi;
-                }
-                col0 = (bi + tt) * kTileC;
-                col_new = true;
-            } else {
-                const uint32_t tt = t - t_nn;
-                bi = tt / ob;
-                col0 = nn + (tt % ob) * kTileC;
-                col_new = false;
-            }
-            const uint32_t row0 = bi * kTileR;
-            const float* pa[kTileR];
-            const float* pb[kTileC];
-            uint32_t valid_mask = 0, fused_mask = 0;
-#pragma unroll
-            for (uint32_t x = 0; x < kTileR; ++x) {
-                const uint32_t r = row0 + x;
-                pa[x] = g.data + size_t(s_ids[r < nn ? r : 0]) * stride;
-            }
-#pragma unroll
-            for (uint32_t y = 0; y < kTileC; ++y) {
-                const uint32_t cc = col0 + y;
-                const bool cvalid = col_new ? cc < nn : cc < m;
-                pb[y] = g.data + size_t(s_ids[cvalid ? cc : 0]) * stride;
-                const bool cfused = col_new ? cc < full_n : (cc - nn) < full_o;
-#pragma unroll
-                for (uint32_t x = 0; x < kTileR; ++x) {
-                    const uint32_t r = row0 + x;
-                    const bool valid = r < nn && cvalid && (!col_new || cc > r);
-                    const bool fused = r < full_n && cfused;
-                    valid_mask |= uint32_t(valid) << (x * kTileC + y);
-                    fused_mask |= uint32_t(fused) << (x * kTileC + y);
-                }
-            }
-            float acc[kTilePairs];
-#pragma unroll
-            for (uint32_t p = 0; p < kTilePairs; ++p) acc[p] = 0.0f;
-            if ((fused_mask & valid_mask) == valid_mask)
-                tile_accumulate<kFused>(pa, pb, stride, l8, acc, fused_mask);
-            else if ((fused_mask & valid_mask) == 0u)
-                tile_accumulate<kUnfused>(pa, pb, stride, l8, acc, fused_mask);
-            else
-                tile_accumulate<kMixed>(pa, pb, stride, l8, acc, fused_mask);
-            float res[2];
-            group_reduce(acc, l8, res);
-            const uint32_t base = 8u * (l8 & 1u) + 4u * ((l8 >> 1) & 1u) + 2u * ((l8 >> 2) & 1u);
-#pragma unroll
-            for (uint32_t j = 0; j < 2; ++j) {
-                const uint32_t p = base + j;
-                if ((valid_mask >> p) & 1u) {
-                    const uint32_t x = p / kTileC, y = p % kTileC;
-                    s_D[(row0 + x) * m + col0 + y] = res[j];
-                }
-            }
-        }
-        __syncthreads();
-
-        if (kDistOnly) {
-            float* dst = out + offsets[u];
-            for (uint32_t e = tid; e < nn * m; e += kThreads) {
-                const uint32_t i = e / m, j = e % m;
-                if (j >= nn || j > i) dst[e] = s_D[e];
-            }
-            continue;
-        }
-
-        // ---- 2. proposals + locked merges -----------------------------------
-        for (uint32_t r = warp; r < m; r += kWarps) {
-            const uint32_t t = s_ids[r];
-            const float mx = ld_cg_f32(g.maxd + t);
-            const uint32_t P = r < nn ? (nn - 1 + no) : nn;
-            auto partner = [&](uint32_t q, float& dist, uint32_t& cand) {
-                if (r < nn) {
-                    if (q + 1 < nn) {
-                        const uint32_t j = q < r ? q : q + 1;
-                        dist = r < j ? s_D[r * m + j] : s_D[j * m + r];
-                        cand = s_ids[j];
-                    } else {
-                        const uint32_t jj = q + 1;  // nn + (q - (nn - 1))
-                        dist = s_D[r * m + jj];
-                        cand = s_ids[jj];
-                    }
-                } else {
-                    dist = s_D[q * m + r];
-                    cand = s_ids[q];
-                }
+            const uint32_t batch = min(32u, cnt - e0);
+            // (entry, 32-partner chunk) steps, each step's loads issued one
+            // step ahead so the D-row / id fetch overlaps the inserts
+            struct Step {
+                float dist;
+                uint32_t cand;
+                bool valid;
             };
-            bool any = false;
-            for (uint32_t q0 = 0; q0 < P; q0 += 32) {
+            auto fetch = [&](uint32_t e, uint32_t q0, uint32_t& P_out) {
+                const uint32_t u = __shfl_sync(0xffffffffu, mu, e);
+                const uint32_t p = __shfl_sync(0xffffffffu, mp, e);
+                const uint32_t nn = __shfl_sync(0xffffffffu, mnn, e);
+                const uint32_t m = __shfl_sync(0xffffffffu, mm, e);
+                const uint64_t off = __shfl_sync(0xffffffffu, moff, e);
+                const bool is_new = p < nn;
+                const uint32_t P = is_new ? m : nn;
+                P_out = P;
                 const uint32_t q = q0 + lane;
-                float dist = 0.0f;
-                uint32_t cand = 0;
-                if (q < P) partner(q, dist, cand);
-                any |= __ballot_sync(0xffffffffu, q < P && dist < mx) != 0u;
-            }
-            if (!any) continue;
-
-            if (lane == 0) {
-                while (atomicCAS(g.locks + t, 0u, 1u) != 0u) __nanosleep(20);
-                __threadfence();
-            }
-            __syncwarp();
-            uint64_t key = lane < k ? ld_cg_u64(g.keys + size_t(t) * k + lane) : kEmptyKey;
-            uint32_t flags = ld_cg_u32(g.flags + t);
-            uint32_t inserted = 0;
-            for (uint32_t q0 = 0; q0 < P; q0 += 32) {
-                const uint32_t q = q0 + lane;
-                float dist = 0.0f;
-                uint32_t cand = 0;
-                if (q < P) partner(q, dist, cand);
-                uint32_t pass = __ballot_sync(0xffffffffu, q < P && dist < mx);
+                Step st{0.0f, 0u, q < P && q != p};
+                if (st.valid) {
+                    const float* row = c.D + off + (is_new ? size_t(p) * m
+                                                           : size_t(nn) * m + size_t(p - nn) * nn);
+                    const uint32_t* list = c.ids + size_t(u) * 2 * cap;
+                    st.dist = row[q];
+                    st.cand = q < nn ? list[q] : list[cap + q - nn];
+                }
+                return st;
+            };
+            uint32_t e = 0, q0 = 0, P = 0;
+            Step cur = fetch(0, 0, P);
+            while (e < batch) {
+                // advance to the next step and start its loads
+                uint32_t ne = e, nq0 = q0 + 32, nP = P;
+                if (nq0 >= P) {
+                    ne = e + 1;
+                    nq0 = 0;
+                }
+                Step nxt{0.0f, 0u, false};
+                if (ne < batch) nxt = fetch(ne, nq0, nP);
+                uint32_t pass = __ballot_sync(0xffffffffu, cur.valid && cur.dist < cur_max);
                 while (pass) {
                     const uint32_t src = __ffs(pass) - 1u;
                     pass &= pass - 1u;
-                    const float dd = __shfl_sync(0xffffffffu, dist, src);
-                    const uint32_t cc = __shfl_sync(0xffffffffu, cand, src);
-                    inserted += warp_try_insert(key, flags, k, dd, cc) ? 1u : 0u;
+                    const float dd = __shfl_sync(0xffffffffu, cur.dist, src);
+                    const uint32_t cc = __shfl_sync(0xffffffffu, cur.cand, src);
+                    if (dd < cur_max && warp_try_insert(key, flags, k, dd, cc)) {
+                        ++inserted;
+                        cur_max = key_dist(__shfl_sync(0xffffffffu, key, k - 1));
+                    }
                 }
+                cur = nxt;
+                e = ne;
+                q0 = nq0;
+                P = nP;
             }
-            if (inserted) {
-                if (lane < k) st_cg_u64(g.keys + size_t(t) * k + lane, key);
-                const uint64_t last = __shfl_sync(0xffffffffu, key, k - 1);
-                if (lane == 0) {
-                    st_cg_u32(g.flags + t, flags);
-                    st_cg_f32(g.maxd + t, key_dist(last));
-                }
-            }
-            __threadfence();
-            __syncwarp();
+        }
+        if (inserted) {
+            if (lane < k) g.keys[size_t(t) * k + lane] = key;
             if (lane == 0) {
-                atomicExch(g.locks + t, 0u);
-                if (inserted) atomicAdd(&sh.changes, (unsigned long long)inserted);
+                g.flags[t] = flags;
+                g.maxd[t] = cur_max;
+                atomicAdd(&s_changes, (unsigned long long)inserted);
             }
         }
     }
     __syncthreads();
-    if (!kDistOnly && tid == 0 && sh.changes) atomicAdd(&ctr->changes, sh.changes);
+    if (threadIdx.x == 0 && s_changes) atomicAdd(&ctr->changes, s_changes);
+}
+
+// One warp per active node: (u, position) into each named candidate's bucket.
+__global__ void scatter_rev_kernel(CandView c, const uint32_t* __restrict__ active,
+                                   IterCounters* ctr) {
+    const uint32_t a = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (a >= ctr->active) return;
+    const uint32_t u = active[a], lane = lane_id();
+    const uint32_t nn = c.nc[u], no = c.oc[u], m = nn + no;
+    const uint32_t* list = c.ids + size_t(u) * 2 * c.cap;
+    for (uint32_t p = lane; p < m; p += 32) {
+        const uint32_t x = p < nn ? list[p] : list[c.cap + p - nn];
+        const uint32_t slot = c.roff[x] + atomicAdd(c.rcur + x, 1u);
+        c.rev[slot] = (uint64_t(u) << 8) | p;
+    }
 }
 
 uint32_t g_sm_count = 0;
@@ -319,45 +475,50 @@ uint32_t sm_count() {
     return g_sm_count;
 }
 
-template <uint32_t kThreads, bool kDistOnly>
-void launch_join_impl(const GraphView& g, const CandView& c, const uint32_t* active,
-                      uint32_t max_active, IterCounters* ctr, const uint64_t* offsets, float* out,
-                      uint32_t* work_counter, cudaStream_t s) {
-    const size_t smem = join_smem_bytes(c.cap);
-    auto kern = join_kernel<kThreads, kDistOnly>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, int(kThreads), smem);
-    if (per_sm < 1) per_sm = 1;
-    uint32_t grid = sm_count() * uint32_t(per_sm);
-    if (grid > max_active) grid = max_active;
-    if (grid == 0) return;
-    cudaMemsetAsync(work_counter, 0, sizeof(uint32_t), s);
-    kern<<<grid, kThreads, smem, s>>>(g, c, active, work_counter, ctr, offsets, out);
-}
-
 }  // namespace
 
-size_t join_smem_bytes(uint32_t cap) { return size_t(cap) * 2 * cap * sizeof(float); }
+size_t join_scan_scratch(uint32_t n) {
+    size_t a = 0, b = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, a, (const uint64_t*)nullptr, (uint64_t*)nullptr, int(n));
+    cub::DeviceScan::ExclusiveSum(nullptr, b, (const uint32_t*)nullptr, (uint32_t*)nullptr, int(n));
+    return a > b ? a : b;
+}
 
-// The work counter lives in the IterCounters' padding word.
-void launch_join(const GraphView& g, const CandView& c, const uint32_t* active,
-                 uint32_t max_active, IterCounters* ctr, cudaStream_t s) {
-    uint32_t* wc = &ctr->pad;
-    if (c.cap <= 32)
-        launch_join_impl<128, false>(g, c, active, max_active, ctr, nullptr, nullptr, wc, s);
-    else
-        launch_join_impl<256, false>(g, c, active, max_active, ctr, nullptr, nullptr, wc, s);
+void launch_join_offsets(const CandView& c, uint32_t n, void* scratch, size_t scratch_bytes,
+                         cudaStream_t s) {
+    size_t bytes = scratch_bytes;
+    cub::DeviceScan::ExclusiveSum(scratch, bytes, c.dsz, c.doff, int(n), s);
+    bytes = scratch_bytes;
+    cub::DeviceScan::ExclusiveSum(scratch, bytes, c.revcnt, c.roff, int(n), s);
+}
+
+void launch_scatter_rev(const CandView& c, const uint32_t* active, IterCounters* ctr,
+                        uint32_t max_active, uint32_t n, cudaStream_t s) {
+    if (!max_active) return;
+    cudaMemsetAsync(c.rcur, 0, sizeof(uint32_t) * n, s);
+    scatter_rev_kernel<<<uint32_t((size_t(max_active) * 32 + 255) / 256), 256, 0, s>>>(c, active,
+                                                                                       ctr);
 }
 
 void launch_join_distances(const GraphView& g, const CandView& c, const uint32_t* active,
-                           uint32_t max_active, const uint64_t* offsets, float* out,
-                           cudaStream_t s, IterCounters* ctr) {
-    uint32_t* wc = &ctr->pad;
-    if (c.cap <= 32)
-        launch_join_impl<128, true>(g, c, active, max_active, ctr, offsets, out, wc, s);
-    else
-        launch_join_impl<256, true>(g, c, active, max_active, ctr, offsets, out, wc, s);
+                           IterCounters* ctr, uint32_t max_active, cudaStream_t s) {
+    if (!max_active) return;
+    const size_t smem = sizeof(DistShared);
+    cudaFuncSetAttribute(join_distances_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(smem));
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, join_distances_kernel, int(kThreads),
+                                                  smem);
+    uint32_t grid = sm_count() * uint32_t(per_sm < 1 ? 1 : per_sm);
+    if (grid > max_active) grid = max_active;
+    cudaMemsetAsync(&ctr->work, 0, sizeof(uint32_t), s);
+    join_distances_kernel<<<grid, kThreads, smem, s>>>(g, c, active, ctr);
+}
+
+void launch_join_merge(const GraphView& g, const CandView& c, IterCounters* ctr,
+                       cudaStream_t s) {
+    join_merge_kernel<<<(g.n + kMergeWarps - 1) / kMergeWarps, kMergeWarps * 32, 0, s>>>(g, c,
+                                                                                         ctr);
 }
 
 }  // namespace knng_cuda

@@ -9,35 +9,46 @@
 namespace knng_cuda {
 
 // The K-NN graph in HBM.  Per node u: k keys sorted ascending (see pack_key),
-// a bitmask of is_new flags (bit i <-> key i), the cached row maximum used by
-// the join's stale-upwards prefilter (descent.hpp:97-102), and a lock word.
+// a bitmask of is_new flags (bit i <-> key i), and the cached row maximum
+// (the reference's row_max_, graph.hpp:216-221).
 struct GraphView {
     const float* data;  // n x stride, rows zero-padded to stride = ceil8(d)
     uint32_t n, k, stride;
     uint64_t* keys;     // n x k
     uint32_t* flags;    // n
     float* maxd;        // n
-    uint32_t* locks;    // n
 };
 
 // Per-iteration candidate lists (CandidateSet layout, selection.hpp:22-49):
-// per node 2*cap ids, new list first, old list second.
+// per node 2*cap ids, new list first, old list second; plus the join's
+// bookkeeping: the size and offset of each active node's distance block, and
+// the reverse index (for every candidate t, the (node, position) pairs whose
+// lists name t) that lets one warp per target pull its proposals.
 struct CandView {
     uint32_t cap;
-    uint32_t* ids;      // n x 2cap
-    uint32_t* raw_new;  // n, atomic append counters during sampling
-    uint32_t* raw_old;  // n
-    uint32_t* nc;       // n, final new counts
-    uint32_t* oc;       // n, final old counts
+    uint32_t* ids;       // n x 2cap
+    uint32_t* raw_new;   // n, atomic append counters during sampling
+    uint32_t* raw_old;   // n
+    uint32_t* nc;        // n, final new counts
+    uint32_t* oc;        // n, final old counts
+    uint64_t* dsz;       // n, floats in u's distance block (0 when nn == 0)
+    uint64_t* doff;      // n, exclusive prefix sum of dsz
+    uint32_t* revcnt;    // n, how many active lists name t
+    uint32_t* roff;      // n, exclusive prefix sum of revcnt
+    uint32_t* rcur;      // n, scatter cursors
+    uint64_t* rev;       // total entries: (u << 8) | position of t in u's list
+    float* D;            // distance blocks, see join.cu
 };
 
 // Device counters for one iteration.
 struct IterCounters {
     unsigned long long changes;
     unsigned long long evals;
-    unsigned long long cands;   // sum of (nn + no) over active nodes
-    uint32_t active;            // number of nodes with nn > 0
-    uint32_t pad;
+    unsigned long long cands;    // sum of (nn + no) over active nodes
+    unsigned long long dfloats;  // total distance-block floats
+    unsigned long long rev;      // total reverse-index entries
+    uint32_t active;             // number of nodes with nn > 0
+    uint32_t work;               // dynamic work counter
 };
 
 // --- graph_kernels.cu ------------------------------------------------------
@@ -49,20 +60,28 @@ void launch_export_rows(const GraphView& g, uint32_t* ids, float* dists, uint8_t
 void launch_indegree(const GraphView& g, uint32_t* indeg, cudaStream_t s);
 void launch_sample(const GraphView& g, const CandView& c, const uint32_t* indeg, uint64_t seed,
                    cudaStream_t s);
+// dedup + flag_consumed + join bookkeeping (active list, block sizes, reverse counts)
 void launch_finalize(const GraphView& g, const CandView& c, uint32_t* active,
                      IterCounters* ctr, cudaStream_t s);
+// join bookkeeping only, for externally supplied candidate lists (fixed-state entries)
+void launch_bookkeeping(const GraphView& g, const CandView& c, uint32_t* active,
+                        IterCounters* ctr, cudaStream_t s);
 void launch_reset_raw(const CandView& c, uint32_t n, cudaStream_t s);
 
 // --- join.cu ---------------------------------------------------------------
-// Local join of every active node (compute_step, descent.hpp:82-153).  The
-// active count is read on the device from ctr->active (<= max_active).
-void launch_join(const GraphView& g, const CandView& c, const uint32_t* active,
-                 uint32_t max_active, IterCounters* ctr, cudaStream_t s);
-// Distance stage only, writing each active node's D matrix to out + offsets[u].
+// Exclusive scans dsz -> doff and revcnt -> roff (CUB); scratch sizing.
+size_t join_scan_scratch(uint32_t n);
+void launch_join_offsets(const CandView& c, uint32_t n, void* scratch, size_t scratch_bytes,
+                         cudaStream_t s);
+// Reverse index scatter (one warp per active node).
+void launch_scatter_rev(const CandView& c, const uint32_t* active, IterCounters* ctr,
+                        uint32_t max_active, uint32_t n, cudaStream_t s);
+// Distance stage of the local join: every active node's distance block.
 void launch_join_distances(const GraphView& g, const CandView& c, const uint32_t* active,
-                           uint32_t max_active, const uint64_t* offsets, float* out,
-                           cudaStream_t s, IterCounters* ctr);
-size_t join_smem_bytes(uint32_t cap);
+                           IterCounters* ctr, uint32_t max_active, cudaStream_t s);
+// Update stage: one warp per target pulls and merges its proposals.
+void launch_join_merge(const GraphView& g, const CandView& c, IterCounters* ctr,
+                       cudaStream_t s);
 
 // --- bruteforce.cu ---------------------------------------------------------
 // Exact k nearest neighbours of the listed query rows among all n rows.

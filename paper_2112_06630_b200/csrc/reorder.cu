@@ -142,7 +142,6 @@ __global__ void remap_kernel(GraphView in, GraphView out, const uint32_t* __rest
     if (lane == 0) {
         out.flags[dst_row] = bits;
         out.maxd[dst_row] = in.maxd[u];
-        out.locks[dst_row] = 0u;
     }
 }
 

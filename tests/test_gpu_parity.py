@@ -39,14 +39,31 @@ CASES = [  # kind, n, k, cap, seed, step
 ]
 
 
-def compare_step(gi, go_ref, g_gpu, rel=1e-5):
+def reference_path_values(restated, data, u, v):
+    """The two values the reference's kernels can produce for pair (u, v): the
+    fused tile path (block_core / tri_core5) and the unfused scalar path."""
+    stride = (data.shape[1] + 7) // 8 * 8
+    a = np.zeros((5, stride), np.float32)
+    b = np.zeros((5, stride), np.float32)
+    a[:, : data.shape[1]] = data[u]
+    b[:, : data.shape[1]] = data[v]
+    fused = restated.block_l2_sq(a, b)[0, 0]
+    unfused = restated.block_l2_sq(a[:1], b[:1])[0, 0]
+    return {int(np.float32(fused).view(np.uint32)), int(np.float32(unfused).view(np.uint32))}
+
+
+def compare_step(gi, go_ref, g_gpu, rel=1e-5, restated=None, data=None):
     """Accepted-update-set comparison.  Returns stats; asserts
-    equality up to swaps between distances tied within `rel` at row ends."""
+    equality up to swaps between distances tied within `rel` at row ends, and
+    that every stored distance that is not bit-identical to the reference's
+    stored one is bit-identical to the reference's other kernel path for that
+    pair."""
     n, k = gi.ids.shape
     mism = 0
     tie_ok = 0
     common = 0
     exact = 0
+    other_path = 0
     flag_bad = 0
     for u in range(n):
         init = set(gi.ids[u].tolist())
@@ -70,11 +87,16 @@ def compare_step(gi, go_ref, g_gpu, rel=1e-5):
             common += 1
             a, b = np.float32(ref[v]), np.float32(gpu[v])
             assert abs(float(a) - float(b)) <= rel * max(float(a), 1e-30), (u, v, a, b)
-            exact += int(a.view(np.uint32) == b.view(np.uint32))
+            same = a.view(np.uint32) == b.view(np.uint32)
+            exact += int(same)
+            if not same and restated is not None:
+                assert int(b.view(np.uint32)) in reference_path_values(restated, data, u, v), \
+                    (u, v, a, b)
+                other_path += 1
             flag_bad += int(ref_f[v] != gpu_f[v])
         del acc_ref, acc_gpu
     return dict(mismatch=mism, tie_swaps=tie_ok, common=common, bit_exact=exact,
-                flag_mismatch=flag_bad)
+                other_path=other_path, flag_mismatch=flag_bad)
 
 
 @pytest.mark.parametrize("kind,n,k,cap,seed,t", CASES)
@@ -85,10 +107,17 @@ def test_local_join_step_matches_oracle(gpu, restated, kind, n, k, cap, seed, t)
     cands = kg.CandidateSet(c.ids, c.new_counts, c.old_counts)
     g, rev, ch, ev = kg.compute_step(data, gi.ids, gi.dists, gi.flags, cands)
     assert ev == ev_ref  # acceptance.cpp:358-381
-    st = compare_step(gi, go, g)
+    st = compare_step(gi, go, g, restated=restated, data=data)
     assert st["mismatch"] == 0, st
     assert st["flag_mismatch"] == 0, st
-    assert st["bit_exact"] >= st["common"] - 2, st  # same-pair path differences only
+    # Every evaluated distance is bit-identical to the reference path for that
+    # pair in that join (test_candidate_distances_bit_exact); a stored value can
+    # still differ by an ulp when the same (t, v) pair is proposed from two joins
+    # whose paths differ (fused tile vs unfused remainder) and the two builds
+    # accept a different proposal first — compare_step checks such values are
+    # exactly the reference's other path for the pair.
+    assert st["bit_exact"] + st["other_path"] == st["common"], st
+    assert st["bit_exact"] >= 0.95 * st["common"], st
     # reverse_degree is k + in-degree of the result (graph.hpp:121-122)
     assert np.array_equal(rev, g.reverse_degree())
     # rows sorted by (dist, id), distinct, no self loops
