@@ -66,7 +66,7 @@ class Clocks:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "200"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
@@ -111,6 +111,70 @@ def ffma_peak_tflops(device: int):
     if lib.knng_diag_ffma2_peak(device, C.byref(t2)) != 0:
         t2.value = 0.0
     return max(t.value, t2.value)
+
+
+def join_roofline(mets, n, d, k, peak_tflops, config):
+    """Roofline of the local-join distance kernel (join_distances_kernel).
+
+    Per launch (one per iteration) the algorithmic work is, after SURVEY.md
+    §8d: F = evals * (3d - 1) credited flops (distance.hpp:19-21) and
+    Q = sum_u (nn_u + no_u) * (4 * stride + 8) + 12 n k gather bytes.  Its
+    roofline time is t* = max(F / pi_fp32, Q / beta_hbm); the reported
+    fraction is sum(t*) / sum(t) over every timed launch, so iterations that
+    are FP32-bound (early, large lists) and HBM-bound (late) both count.
+    """
+    stride = (d + 7) // 8 * 8
+    beta = 6650.0
+    beta_src = "fallback 6650 GB/s (B200_PROFILING.md)"
+    mp = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(mp):
+        beta = float(json.load(open(mp))["hbm_gbs"])
+        beta_src = "MEASURED_PEAKS.json hbm_gbs (measured)"
+    pi = peak_tflops or 74.0
+    pi_src = ("measured FFMA/FFMA2 microbenchmark (libknng_diag), this box" if peak_tflops
+              else "fallback 74 TFLOP/s nominal")
+    F = Q = t = t_star = t_fp = t_hbm = 0.0
+    launches = 0
+    for m in mets:
+        for it in m.iterations[1:]:
+            if it.join_ms <= 0:
+                continue
+            f = it.dist_evals * (3 * d - 1)
+            q = it.join_candidates * (4 * stride + 8) + 12 * n * k
+            tf, th = f / (pi * 1e12), q / (beta * 1e9)
+            F += f
+            Q += q
+            t += it.join_ms * 1e-3
+            t_fp += tf
+            t_hbm += th
+            t_star += max(tf, th)
+            launches += 1
+    traffic = None
+    if os.path.exists(PROFILE_TRAFFIC):
+        try:
+            traffic = json.load(open(PROFILE_TRAFFIC)).get(config)
+        except (OSError, ValueError):
+            traffic = None
+    frac = t_star / t if t else 0.0
+    if t_fp >= t_hbm:
+        roof = {"bound": "fp32", "achieved": round(frac * pi, 3), "peak": round(pi, 2),
+                "unit": "TFLOP/s", "peak_source": pi_src}
+    else:
+        roof = {"bound": "hbm", "achieved": round(frac * beta, 1), "peak": beta, "unit": "GB/s",
+                "peak_source": beta_src}
+    roof.update({
+        "frac": round(frac, 4), "traffic": traffic,
+        "kernel": "join_distances_kernel (local-join distance stage)",
+        "frac_definition": "sum over launches of max(F/pi, Q/beta) / sum of launch times",
+        "fp32_tflops_achieved": round(F / t / 1e12, 3) if t else None,
+        "gather_gbs_achieved": round(Q / t / 1e9, 1) if t else None,
+        "algorithmic_flops_per_launch": int(F / max(1, launches)),
+        "algorithmic_bytes_per_launch": int(Q / max(1, launches)),
+        "avg_launch_ms": round(t * 1e3 / max(1, launches), 4),
+        "launches": launches,
+        "fp32_peak_tflops": round(pi, 2), "hbm_peak_gbs": beta,
+    })
+    return roof
 
 
 def reference_recall_sample(data, k, cfg, ids_gpu, sample, reference_ids=None):
@@ -175,7 +239,10 @@ def run_ours(args, rank, world, local):
     join_launches = sum(m.kernel_launches["join"] for m in mets)
     join_evals = sum(m.join_evals for m in mets)
     join_cands = sum(m.join_candidates for m in mets)
-    launches = sum(2 + 5 * (len(m.iterations) - 1) for m in mets)
+    # our kernels per build: init + export, and per iteration indegree,
+    # reset, sample, finalize, capacity check, reverse scatter, distances,
+    # merge (the two CUB scans per iteration are library kernels, not counted)
+    launches = sum(2 + 8 * (len(m.iterations) - 1) for m in mets)
     kernel_ms = {kname: sum(m.kernel_ms[kname] for m in mets) for kname in mets[0].kernel_ms}
 
     # ---- e2e through the host-pointer C-ABI (pinned host data, graph back to host)
@@ -210,37 +277,8 @@ def run_ours(args, rank, world, local):
 
     out = None
     if rank == 0:
-        stride = (d + 7) // 8 * 8
-        F = join_evals * (3 * d - 1)
-        Q = join_cands * (4 * stride + 8) + 12 * n * k * iters
-        t_join = join_ms * 1e-3
-        beta = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
-            if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
-        pi = peak or 74.0
-        fp32_time = F / (pi * 1e12)
-        hbm_time = Q / (beta * 1e9)
-        traffic = None
-        if os.path.exists(PROFILE_TRAFFIC):
-            try:
-                traffic = json.load(open(PROFILE_TRAFFIC)).get(args.config)
-            except (OSError, ValueError):
-                traffic = None
-        if fp32_time >= hbm_time:
-            roof = {"bound": "fp32", "achieved": round(F / t_join / 1e12, 3), "peak": round(pi, 2),
-                    "unit": "TFLOP/s", "frac": round(F / t_join / 1e12 / pi, 4),
-                    "traffic": traffic,
-                    "peak_source": "measured FFMA microbenchmark (libknng_diag)" if peak else
-                    "fallback 74 TFLOP/s nominal"}
-        else:
-            roof = {"bound": "hbm", "achieved": round(Q / t_join / 1e9, 1), "peak": beta,
-                    "unit": "GB/s", "frac": round(Q / t_join / 1e9 / beta, 4), "traffic": traffic,
-                    "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
-        roof.update({"kernel": "join_kernel (local join: distances + locked merges)",
-                     "algorithmic_flops_per_launch": int(F / max(1, join_launches)),
-                     "algorithmic_bytes_per_launch": int(Q / max(1, join_launches)),
-                     "avg_launch_ms": round(join_ms / max(1, join_launches), 4),
-                     "launches": int(join_launches),
-                     "share_of_step": round(join_ms / ms, 3)})
+        roof = join_roofline(mets, n, d, k, peak, args.config)
+        roof["share_of_step"] = round(join_ms / ms, 3)
 
         # matched recall on a node sample vs the reference (same data, same seed)
         sample = np.random.default_rng(1).choice(n, size=min(n, args.recall_sample),

@@ -76,6 +76,8 @@ typedef struct knng_cuda_iteration {
     double wall_time_s;
     uint64_t dist_evals;
     uint64_t changes;
+    uint64_t join_candidates;  /* sum of (nn_u + no_u) over the iteration's joins */
+    double join_ms;            /* distance-kernel device time (params.profile only) */
 } knng_cuda_iteration;
 
 /* Per-kernel device time (CUDA events on the library's stream), filled when

@@ -11,7 +11,7 @@ import os
 import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "lib", "libknng_cuda.so")
+LIB_PATH = os.environ.get("KNNG_CUDA_LIB") or os.path.join(PKG, "lib", "libknng_cuda.so")
 
 OK = 0
 INVALID_ARGUMENT = 1
@@ -63,6 +63,8 @@ class Iteration(C.Structure):
         ("wall_time_s", C.c_double),
         ("dist_evals", C.c_uint64),
         ("changes", C.c_uint64),
+        ("join_candidates", C.c_uint64),
+        ("join_ms", C.c_double),
     ]
 
 

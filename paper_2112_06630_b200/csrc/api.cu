@@ -111,23 +111,25 @@ struct DeviceGuard {
     ~DeviceGuard() { cudaSetDevice(prev); }
 };
 
+// The caller's stream, or this host thread's cached library stream for the
+// current device.  Reusing one stream per (thread, device) keeps the pool's
+// freed blocks immediately reusable by the next call (stream-ordered reuse)
+// instead of growing the pool for every new stream.
 struct StreamHolder {
     cudaStream_t s = nullptr;
-    bool own = false;
     explicit StreamHolder(void* user) {
         if (user) {
             s = static_cast<cudaStream_t>(user);
-        } else {
-            CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-            own = true;
+            return;
         }
+        thread_local cudaStream_t cached[64] = {};
+        int dev = 0;
+        CK(cudaGetDevice(&dev));
+        if (dev < 0 || dev >= 64) raise(KNNG_CUDA_INVALID_ARGUMENT, "device ordinal out of range");
+        if (!cached[dev]) CK(cudaStreamCreateWithFlags(&cached[dev], cudaStreamNonBlocking));
+        s = cached[dev];
     }
-    ~StreamHolder() {
-        if (own) {
-            cudaStreamSynchronize(s);
-            cudaStreamDestroy(s);
-        }
-    }
+    ~StreamHolder() { cudaStreamSynchronize(s); }
 };
 
 // Per-kernel CUDA-event timing on the library stream (params.profile).
@@ -160,12 +162,15 @@ struct KernelTimer {
         if (h < 0) return;
         CK(cudaEventRecord(pool[open[size_t(h)].second + 1], s));
     }
+    double last_join_ms = 0.0;  // distance-kernel time of the last flushed iteration
     void flush() {  // after a stream sync
+        last_join_ms = 0.0;
         for (auto& e : open) {
             float ms = 0.0f;
             CK(cudaEventElapsedTime(&ms, pool[e.second], pool[e.second + 1]));
             m->kernel_ms[e.first] += ms;
             m->kernel_launches[e.first] += 1;
+            if (e.first == KNNG_CUDA_KERNEL_JOIN) last_join_ms += ms;
         }
         open.clear();
         used = 0;
@@ -242,12 +247,17 @@ struct Engine {
             rcur.alloc(n, pool, s);
             scan_bytes = join_scan_scratch(n);
             scan_tmp.alloc(scan_bytes, pool, s);
+            // every active list names at most 2 cap candidates
+            reserve_join(uint64_t(n) * 2 * cap, uint64_t(n) * 4 * k * k);
         }
-        CK(cudaMallocHost(reinterpret_cast<void**>(&h_ctr), sizeof(IterCounters)));
+        // pinned counter slot, cached per host thread (cudaMallocHost is slow)
+        thread_local IterCounters* pinned = nullptr;
+        if (!pinned) CK(cudaMallocHost(reinterpret_cast<void**>(&pinned), sizeof(IterCounters)));
+        h_ctr = pinned;
         CK(cudaMemsetAsync(ctr.p, 0, sizeof(IterCounters), s));
     }
     ~Engine() {
-        if (h_ctr) cudaFreeHost(h_ctr);
+        h_ctr = nullptr;  // the pinned slot is reused by the thread's next call
     }
 
     GraphView gv() const { return GraphView{data.p, n, k, stride, keys.p, flags.p, maxd.p}; }
@@ -303,20 +313,32 @@ struct Engine {
         CK(cudaGetLastError());
     }
 
-    // The local join after finalize/bookkeeping: read the counters (active
-    // nodes, block and index sizes), size the buffers, build offsets and the
-    // reverse index, then the distance and merge stages.
+    // The local join after finalize/bookkeeping, with no host round trip:
+    // block offsets, a device-side capacity check, the reverse index, then
+    // the distance and merge stages.  Ends with the iteration's one counter
+    // read; when the distance blocks outgrew their buffer (the stages skipped
+    // themselves) the buffer grows and the stages run again.
     void join(KernelTimer& timer, bool distances_only = false) {
-        read_counters();
-        const IterCounters c0 = *h_ctr;
-        if (c0.active == 0) return;
-        reserve_join(c0.rev, c0.dfloats);
         int h = timer.begin(KNNG_CUDA_KERNEL_INDEX);
         launch_join_offsets(cv(), n, scan_tmp.p, scan_bytes, s);
-        launch_scatter_rev(cv(), active.p, ctr.p, c0.active, n, s);
+        timer.end(h);
+        join_stages(timer, distances_only);
+        read_counters();
+        if (h_ctr->overflow) {
+            reserve_join(h_ctr->rev, h_ctr->dfloats);
+            CK(cudaMemsetAsync(&ctr.p->overflow, 0, sizeof(uint32_t), s));
+            join_stages(timer, distances_only);
+            read_counters();
+        }
+    }
+
+    void join_stages(KernelTimer& timer, bool distances_only) {
+        launch_check_capacity(ctr.p, d_cap, s);
+        int h = timer.begin(KNNG_CUDA_KERNEL_INDEX);
+        launch_scatter_rev(cv(), active.p, ctr.p, n, n, s);
         timer.end(h);
         h = timer.begin(KNNG_CUDA_KERNEL_JOIN);
-        launch_join_distances(gv(), cv(), active.p, ctr.p, c0.active, s);
+        launch_join_distances(gv(), cv(), active.p, ctr.p, n, s);
         timer.end(h);
         CK(cudaGetLastError());
         if (distances_only) return;
@@ -324,6 +346,45 @@ struct Engine {
         launch_join_merge(gv(), cv(), ctr.p, s);
         timer.end(h);
         CK(cudaGetLastError());
+    }
+
+    // ---- locality reorder (reorder.hpp:22-50, dataset.hpp:237-245,
+    //      graph.hpp:150-166)
+    DevBuf<uint32_t> sigma, sigma_inv;
+
+    // KnnGraph::remap: row u -> row perm[u], ids renamed, rows re-sorted
+    void remap_graph(const uint32_t* perm) {
+        DevBuf<uint64_t> keys2;
+        DevBuf<uint32_t> flags2;
+        DevBuf<float> maxd2;
+        keys2.alloc(size_t(n) * k, pool, s);
+        flags2.alloc(n, pool, s);
+        maxd2.alloc(n, pool, s);
+        GraphView out = gv();
+        out.keys = keys2.p;
+        out.flags = flags2.p;
+        out.maxd = maxd2.p;
+        launch_remap_graph(gv(), out, perm, s);
+        CK(cudaGetLastError());
+        std::swap(keys.p, keys2.p);
+        std::swap(flags.p, flags2.p);
+        std::swap(maxd.p, maxd2.p);
+    }
+
+    // sigma from the current graph, rows gathered, graph relabelled
+    void reorder() {
+        sigma.alloc(n, pool, s);
+        sigma_inv.alloc(n, pool, s);
+        const size_t scratch_bytes = locality_permutation_scratch(n);
+        DevBuf<unsigned char> scratch;
+        scratch.alloc(scratch_bytes, pool, s);
+        launch_locality_permutation(gv(), sigma.p, sigma_inv.p, scratch.p, scratch_bytes, s);
+        CK(cudaGetLastError());
+        DevBuf<float> data2;
+        data2.alloc(size_t(n) * stride, pool, s);
+        launch_permute_rows(data.p, data2.p, sigma.p, n, stride, s);
+        std::swap(data.p, data2.p);
+        remap_graph(sigma.p);
     }
 
     void export_rows(uint32_t* ids, float* dists, uint8_t* fl) {
@@ -354,10 +415,11 @@ void metrics_reset(knng_cuda_metrics* m) {
 }
 
 void metrics_push(knng_cuda_metrics* m, uint32_t iteration, double wall, uint64_t evals,
-                  uint64_t changes) {
+                  uint64_t changes, uint64_t cands = 0, double join_ms = 0.0) {
     if (!m) return;
     if (m->iterations && m->n_rows < m->capacity)
-        m->iterations[m->n_rows] = knng_cuda_iteration{iteration, wall, evals, changes};
+        m->iterations[m->n_rows] =
+            knng_cuda_iteration{iteration, wall, evals, changes, cands, join_ms};
     ++m->n_rows;
     m->total_wall_time_s += wall;
     m->total_dist_evals += evals;
@@ -367,9 +429,10 @@ void metrics_push(knng_cuda_metrics* m, uint32_t iteration, double wall, uint64_
 // knng::run (descent.hpp:193-255) on one GPU; data already on the device or
 // on the host per data_on_device; outputs device pointers.
 void run_engine(Engine& e, const float* data, bool data_on_device, const knng_cuda_params& p,
-                uint32_t* d_ids, float* d_dists, uint8_t* d_flags, knng_cuda_metrics* m) {
-    if (p.reorder) raise(KNNG_CUDA_NOT_IMPLEMENTED, "reorder is not available in this build yet");
+                uint32_t* d_ids, float* d_dists, uint8_t* d_flags, knng_cuda_metrics* m,
+                uint32_t* d_sigma = nullptr) {
     KernelTimer timer(p.profile != 0, e.s, m);
+    bool reordered = false;
     std::mt19937_64 master(p.seed);
     double t0 = now_s();
     e.upload(data, data_on_device);
@@ -389,17 +452,32 @@ void run_engine(Engine& e, const float* data, bool data_on_device, const knng_cu
         const uint64_t iter_seed = master();
         CK(cudaMemsetAsync(e.ctr.p, 0, sizeof(IterCounters), e.s));
         e.select(iter_seed, timer);
-        e.join(timer);
-        e.read_counters();
+        e.join(timer);  // ends with the iteration's counter read
+        const IterCounters c = *e.h_ctr;
+        // the locality reorder runs once, after iteration reorder_after_iteration
+        // (descent.hpp:230-235); the rest of the run works in permuted ids
+        if (p.reorder && !reordered && iter == p.reorder_after_iteration) {
+            const int h = timer.begin(KNNG_CUDA_KERNEL_REORDER);
+            e.reorder();
+            timer.end(h);
+            reordered = true;
+        }
+        CK(cudaStreamSynchronize(e.s));
         timer.flush();
         t1 = now_s();
-        const IterCounters c = *e.h_ctr;
-        metrics_push(m, iter, t1 - t0, c.evals, c.changes);
+        metrics_push(m, iter, t1 - t0, c.evals, c.changes, c.cands, timer.last_join_ms);
         if (m) {
             m->join_candidates += c.cands;
             m->join_evals += c.evals;
         }
         if (double(c.changes) < threshold) break;
+    }
+    if (reordered) {
+        // back to the caller's ids (descent.hpp:245)
+        e.remap_graph(e.sigma_inv.p);
+        if (d_sigma)
+            CK(cudaMemcpyAsync(d_sigma, e.sigma.p, sizeof(uint32_t) * e.n,
+                               cudaMemcpyDeviceToDevice, e.s));
     }
     e.export_rows(d_ids, d_dists, d_flags);
     CK(cudaStreamSynchronize(e.s));
@@ -502,22 +580,25 @@ int knng_cuda_run(const float* data, uint32_t n, uint32_t d, const knng_cuda_par
             raise(KNNG_CUDA_INVALID_ARGUMENT, "null argument");
         const knng_cuda_params p = *params;
         validate_params(n, d, p);
-        (void)out_sigma;
         DeviceGuard dg(p.device);
         StreamHolder sh(nullptr);
         metrics_reset(out_metrics);
         Engine e(p.device, n, d, p.k, p.max_candidates, sh.s);
-        DevBuf<uint32_t> ids;
+        DevBuf<uint32_t> ids, sig;
         DevBuf<float> dists;
         DevBuf<uint8_t> fl;
         const size_t nk = size_t(n) * p.k;
         ids.alloc(nk, e.pool, e.s);
         dists.alloc(nk, e.pool, e.s);
         if (out_flags) fl.alloc(nk, e.pool, e.s);
-        run_engine(e, data, false, p, ids.p, dists.p, out_flags ? fl.p : nullptr, out_metrics);
+        const bool want_sigma = out_sigma && p.reorder;
+        if (want_sigma) sig.alloc(n, e.pool, e.s);
+        run_engine(e, data, false, p, ids.p, dists.p, out_flags ? fl.p : nullptr, out_metrics,
+                   want_sigma ? sig.p : nullptr);
         to_host(out_ids, ids.p, nk, e);
         to_host(out_dists, dists.p, nk, e);
         if (out_flags) to_host(out_flags, fl.p, nk, e);
+        if (want_sigma) to_host(out_sigma, sig.p, n, e);
         CK(cudaStreamSynchronize(e.s));
         if (out_metrics) {
             out_metrics->h2d_bytes = e.h2d;
@@ -777,9 +858,35 @@ int knng_cuda_bruteforce_knng(const float* data, uint32_t n, uint32_t d, uint32_
 int knng_cuda_locality_permutation(uint32_t n, uint32_t k, const uint32_t* ids,
                                    const float* dists, uint32_t* sigma, uint32_t* sigma_inv,
                                    int device) {
-    (void)n; (void)k; (void)ids; (void)dists; (void)sigma; (void)sigma_inv; (void)device;
-    g_err = "locality permutation is not available in this build yet";
-    return KNNG_CUDA_NOT_IMPLEMENTED;
+    return guarded([&] {
+        if (!ids || !dists || !sigma || !sigma_inv)
+            raise(KNNG_CUDA_INVALID_ARGUMENT, "null argument");
+        validate_shape(n, 1, k);
+        validate_rows(n, k, ids);
+        DeviceGuard dg(device);
+        StreamHolder sh(nullptr);
+        Engine e(device, n, 1, k, 0, sh.s);
+        const size_t nk = size_t(n) * k;
+        DevBuf<uint32_t> d_ids;
+        DevBuf<float> d_dists;
+        DevBuf<uint8_t> d_fl;
+        to_device(d_ids, ids, nk, e);
+        to_device(d_dists, dists, nk, e);
+        d_fl.alloc(nk, e.pool, e.s);
+        CK(cudaMemsetAsync(d_fl.p, 0, nk, e.s));
+        launch_load_rows(e.gv(), d_ids.p, d_dists.p, d_fl.p, e.s);
+        e.sigma.alloc(n, e.pool, e.s);
+        e.sigma_inv.alloc(n, e.pool, e.s);
+        const size_t scratch_bytes = locality_permutation_scratch(n);
+        DevBuf<unsigned char> scratch;
+        scratch.alloc(scratch_bytes, e.pool, e.s);
+        launch_locality_permutation(e.gv(), e.sigma.p, e.sigma_inv.p, scratch.p, scratch_bytes,
+                                    e.s);
+        CK(cudaGetLastError());
+        to_host(sigma, e.sigma.p, n, e);
+        to_host(sigma_inv, e.sigma_inv.p, n, e);
+        CK(cudaStreamSynchronize(e.s));
+    });
 }
 
 }  // extern "C"

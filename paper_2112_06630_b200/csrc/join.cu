@@ -42,7 +42,10 @@ namespace knng_cuda {
 
 namespace {
 
-constexpr uint32_t kThreads = 128;       // 4 warps, 16 groups of 8 lanes
+#ifndef KNNG_JOIN_THREADS
+#define KNNG_JOIN_THREADS 128
+#endif
+constexpr uint32_t kThreads = KNNG_JOIN_THREADS;  // 128: 4 warps, 16 groups of 8 lanes
 constexpr uint32_t kGroups = kThreads / 8;
 constexpr uint32_t kSlab = 32;           // floats per row per smem stage
 constexpr uint32_t kStages = 3;          // cp.async pipeline depth
@@ -67,6 +70,9 @@ struct DistShared {
     uint16_t tiles[kMaxTiles];       // (rb << 8) | cb, in (rb, cb) order
     uint32_t n_tiles;
     uint32_t node;
+    uint32_t blkmask;                // column-slot 8-blocks read by the current pass
+    uint32_t nblk;
+    uint8_t blklist[kMaxColSlots / 8];
 };
 
 __device__ __forceinline__ void cp_async16(float* smem_dst, const float* gmem_src) {
@@ -81,16 +87,17 @@ __device__ __forceinline__ uint32_t swz(uint32_t slot, uint32_t seg) {
     return slot * kSlab + ((seg ^ ((slot >> 3) & 3u)) << 3);
 }
 
-// Stage slab `s` (elements [32 s, 32 s + 32) of every column-slot row) into
-// buffer `buf` with 16-byte cp.async; chunks past the row stride are zero
-// (exact: they contribute +0 under either accumulation).
+// Stage slab `s` (elements [32 s, 32 s + 32)) of the rows of the column-slot
+// 8-blocks the current pass reads (sh.blklist) into buffer `buf` with 16-byte
+// cp.async; chunks past the row stride are zero (exact: they contribute +0
+// under either accumulation).
 __device__ __forceinline__ void stage_slab(DistShared& sh, const float* __restrict__ data,
-                                           uint32_t stride, uint32_t ncols, uint32_t s,
+                                           uint32_t stride, uint32_t nblk, uint32_t s,
                                            uint32_t buf) {
     const uint32_t e0 = s * kSlab;
     float* dst = sh.slab[buf];
-    for (uint32_t i = threadIdx.x; i < ncols * (kSlab / 4); i += kThreads) {
-        const uint32_t slot = i >> 3, j = i & 7u;
+    for (uint32_t i = threadIdx.x; i < nblk * 64u; i += kThreads) {
+        const uint32_t slot = sh.blklist[i >> 6] * 8u + ((i >> 3) & 7u), j = i & 7u;
         const uint32_t row = sh.colrow[slot];
         if (row == 0xffffffffu) continue;
         float* p = dst + swz(slot, j >> 1) + (j & 1u) * 4;
@@ -188,6 +195,7 @@ __global__ void __launch_bounds__(kThreads) join_distances_kernel(
     DistShared& sh = *reinterpret_cast<DistShared*>(smem_raw);
     const uint32_t tid = threadIdx.x, group = tid >> 3, l8 = tid & 7u;
     const uint32_t stride = g.stride, cap = c.cap;
+    if (ctr->overflow) return;
     const uint32_t n_active = ctr->active;
     const uint32_t n_slabs = (stride + kSlab - 1) / kSlab;
 
@@ -274,7 +282,6 @@ __global__ void __launch_bounds__(kThreads) join_distances_kernel(
             }
         }
         const uint32_t n_tiles = sh.n_tiles;
-        const uint32_t ncols = cf + cs;
         float* const D = c.D + c.doff[u];
 
         for (uint32_t t0 = 0; t0 < n_tiles; t0 += kGroups) {
@@ -286,20 +293,36 @@ __global__ void __launch_bounds__(kThreads) join_distances_kernel(
             const bool fused = rb * 8 < rf && cb * 8 < cf;
             // row slot block -> column slot block holding the same new candidates
             const uint32_t a_blk = rb * 8 < rf ? rb : cf / 8 + (rb - rf / 8);
+            // stage only the 8-blocks this pass reads (a partial last pass
+            // needs a fraction of the rows)
+            if (tid == 0) sh.blkmask = 0;
+            __syncthreads();
+            if (live && l8 == 0) atomicOr(&sh.blkmask, (1u << a_blk) | (1u << cb));
+            __syncthreads();
+            if (tid == 0) {
+                uint32_t msk = sh.blkmask, nb = 0;
+                while (msk) {
+                    sh.blklist[nb++] = uint8_t(__ffs(msk) - 1);
+                    msk &= msk - 1u;
+                }
+                sh.nblk = nb;
+            }
+            __syncthreads();
+            const uint32_t nblk = sh.nblk;
             float2 acc[32];
 #pragma unroll
             for (uint32_t p = 0; p < 32; ++p) acc[p] = make_float2(0.0f, 0.0f);
 
             // 3-stage cp.async pipeline, one barrier per slab
             for (uint32_t p = 0; p < kStages - 1; ++p) {
-                if (p < n_slabs) stage_slab(sh, g.data, stride, ncols, p, p);
+                if (p < n_slabs) stage_slab(sh, g.data, stride, nblk, p, p);
                 cp_async_commit();
             }
             for (uint32_t s = 0; s < n_slabs; ++s) {
                 cp_async_wait_1();
                 __syncthreads();
                 if (s + kStages - 1 < n_slabs)
-                    stage_slab(sh, g.data, stride, ncols, s + kStages - 1,
+                    stage_slab(sh, g.data, stride, nblk, s + kStages - 1,
                                (s + kStages - 1) % kStages);
                 cp_async_commit();
                 const float* slab = sh.slab[s % kStages];
@@ -355,6 +378,7 @@ constexpr uint32_t kMergeWarps = 8;
 __global__ void __launch_bounds__(kMergeWarps * 32) join_merge_kernel(GraphView g, CandView c,
                                                                      IterCounters* ctr) {
     __shared__ unsigned long long s_changes;
+    if (ctr->overflow) return;
     if (threadIdx.x == 0) s_changes = 0;
     __syncthreads();
     const uint32_t lane = lane_id();
@@ -379,45 +403,56 @@ __global__ void __launch_bounds__(kMergeWarps * 32) join_merge_kernel(GraphView 
                 mm = mnn + c.oc[mu];
                 moff = c.doff[mu];
             }
-            const uint32_t batch = min(32u, cnt - e0);
-            // (entry, 32-partner chunk) steps, each step's loads issued one
-            // step ahead so the D-row / id fetch overlaps the inserts
+            // The batch's partners, flattened: entry e contributes P_e
+            // partners (new target: the other m - 1 candidates; old target:
+            // the nn new ones), so every lane of every step has work even
+            // when lists are short.  Each step's loads are issued one step
+            // ahead so the D-row / id fetch overlaps the inserts.
+            const uint32_t pe = e0 + lane < cnt ? (mp < mnn ? mm - 1 : mnn) : 0u;
+            uint32_t incl = pe;
+#pragma unroll
+            for (uint32_t o = 1; o < 32; o <<= 1) {
+                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            const uint32_t excl = incl - pe;
+            const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
             struct Step {
                 float dist;
                 uint32_t cand;
                 bool valid;
             };
-            auto fetch = [&](uint32_t e, uint32_t q0, uint32_t& P_out) {
+            auto fetch = [&](uint32_t f0) {
+                const uint32_t f = f0 + lane;
+                // entry holding flattened partner f: last e with excl[e] <= f
+                uint32_t e = 0;
+#pragma unroll
+                for (uint32_t step = 16; step > 0; step >>= 1) {
+                    const uint32_t probe = __shfl_sync(0xffffffffu, excl, (e + step) & 31u);
+                    if (e + step < 32 && probe <= f) e += step;
+                }
                 const uint32_t u = __shfl_sync(0xffffffffu, mu, e);
                 const uint32_t p = __shfl_sync(0xffffffffu, mp, e);
                 const uint32_t nn = __shfl_sync(0xffffffffu, mnn, e);
                 const uint32_t m = __shfl_sync(0xffffffffu, mm, e);
                 const uint64_t off = __shfl_sync(0xffffffffu, moff, e);
-                const bool is_new = p < nn;
-                const uint32_t P = is_new ? m : nn;
-                P_out = P;
-                const uint32_t q = q0 + lane;
-                Step st{0.0f, 0u, q < P && q != p};
+                const uint32_t q = f - __shfl_sync(0xffffffffu, excl, e);
+                Step st{0.0f, 0u, f < total};
                 if (st.valid) {
+                    const bool is_new = p < nn;
+                    const uint32_t qq = is_new && q >= p ? q + 1 : q;  // skip self
                     const float* row = c.D + off + (is_new ? size_t(p) * m
                                                            : size_t(nn) * m + size_t(p - nn) * nn);
                     const uint32_t* list = c.ids + size_t(u) * 2 * cap;
-                    st.dist = row[q];
-                    st.cand = q < nn ? list[q] : list[cap + q - nn];
+                    st.dist = row[qq];
+                    st.cand = qq < nn ? list[qq] : list[cap + qq - nn];
                 }
                 return st;
             };
-            uint32_t e = 0, q0 = 0, P = 0;
-            Step cur = fetch(0, 0, P);
-            while (e < batch) {
-                // advance to the next step and start its loads
-                uint32_t ne = e, nq0 = q0 + 32, nP = P;
-                if (nq0 >= P) {
-                    ne = e + 1;
-                    nq0 = 0;
-                }
+            Step cur = fetch(0);
+            for (uint32_t f0 = 0; f0 < total; f0 += 32) {
                 Step nxt{0.0f, 0u, false};
-                if (ne < batch) nxt = fetch(ne, nq0, nP);
+                if (f0 + 32 < total) nxt = fetch(f0 + 32);
                 uint32_t pass = __ballot_sync(0xffffffffu, cur.valid && cur.dist < cur_max);
                 while (pass) {
                     const uint32_t src = __ffs(pass) - 1u;
@@ -430,9 +465,6 @@ __global__ void __launch_bounds__(kMergeWarps * 32) join_merge_kernel(GraphView 
                     }
                 }
                 cur = nxt;
-                e = ne;
-                q0 = nq0;
-                P = nP;
             }
         }
         if (inserted) {
@@ -452,7 +484,7 @@ __global__ void __launch_bounds__(kMergeWarps * 32) join_merge_kernel(GraphView 
 __global__ void scatter_rev_kernel(CandView c, const uint32_t* __restrict__ active,
                                    IterCounters* ctr) {
     const uint32_t a = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (a >= ctr->active) return;
+    if (a >= ctr->active || ctr->overflow) return;
     const uint32_t u = active[a], lane = lane_id();
     const uint32_t nn = c.nc[u], no = c.oc[u], m = nn + no;
     const uint32_t* list = c.ids + size_t(u) * 2 * c.cap;
@@ -461,6 +493,10 @@ __global__ void scatter_rev_kernel(CandView c, const uint32_t* __restrict__ acti
         const uint32_t slot = c.roff[x] + atomicAdd(c.rcur + x, 1u);
         c.rev[slot] = (uint64_t(u) << 8) | p;
     }
+}
+
+__global__ void check_capacity_kernel(IterCounters* ctr, unsigned long long capacity) {
+    ctr->overflow = ctr->dfloats > capacity ? 1u : 0u;
 }
 
 uint32_t g_sm_count = 0;
@@ -492,6 +528,10 @@ void launch_join_offsets(const CandView& c, uint32_t n, void* scratch, size_t sc
     cub::DeviceScan::ExclusiveSum(scratch, bytes, c.revcnt, c.roff, int(n), s);
 }
 
+void launch_check_capacity(IterCounters* ctr, unsigned long long capacity, cudaStream_t s) {
+    check_capacity_kernel<<<1, 1, 0, s>>>(ctr, capacity);
+}
+
 void launch_scatter_rev(const CandView& c, const uint32_t* active, IterCounters* ctr,
                         uint32_t max_active, uint32_t n, cudaStream_t s) {
     if (!max_active) return;
@@ -504,12 +544,15 @@ void launch_join_distances(const GraphView& g, const CandView& c, const uint32_t
                            IterCounters* ctr, uint32_t max_active, cudaStream_t s) {
     if (!max_active) return;
     const size_t smem = sizeof(DistShared);
-    cudaFuncSetAttribute(join_distances_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(smem));
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, join_distances_kernel, int(kThreads),
-                                                  smem);
-    uint32_t grid = sm_count() * uint32_t(per_sm < 1 ? 1 : per_sm);
+    static int per_sm = 0;  // occupancy is a property of the kernel: query once
+    if (!per_sm) {
+        cudaFuncSetAttribute(join_distances_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(smem));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, join_distances_kernel,
+                                                      int(kThreads), smem);
+        if (per_sm < 1) per_sm = 1;
+    }
+    uint32_t grid = sm_count() * uint32_t(per_sm);
     if (grid > max_active) grid = max_active;
     cudaMemsetAsync(&ctr->work, 0, sizeof(uint32_t), s);
     join_distances_kernel<<<grid, kThreads, smem, s>>>(g, c, active, ctr);

@@ -49,6 +49,8 @@ struct IterCounters {
     unsigned long long rev;      // total reverse-index entries
     uint32_t active;             // number of nodes with nn > 0
     uint32_t work;               // dynamic work counter
+    uint32_t overflow;           // distance blocks exceed the buffer: join skipped
+    uint32_t pad;
 };
 
 // --- graph_kernels.cu ------------------------------------------------------
@@ -73,6 +75,10 @@ void launch_reset_raw(const CandView& c, uint32_t n, cudaStream_t s);
 size_t join_scan_scratch(uint32_t n);
 void launch_join_offsets(const CandView& c, uint32_t n, void* scratch, size_t scratch_bytes,
                          cudaStream_t s);
+// Sets ctr->overflow when the distance blocks need more than `capacity` floats
+// (the join stages then return at once; the host grows the buffer and
+// relaunches them), so an iteration needs no host round trip before its join.
+void launch_check_capacity(IterCounters* ctr, unsigned long long capacity, cudaStream_t s);
 // Reverse index scatter (one warp per active node).
 void launch_scatter_rev(const CandView& c, const uint32_t* active, IterCounters* ctr,
                         uint32_t max_active, uint32_t n, cudaStream_t s);

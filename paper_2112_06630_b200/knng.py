@@ -77,6 +77,8 @@ class IterationMetrics:
     wall_time_s: float
     dist_evals: int
     changes: int
+    join_candidates: int = 0
+    join_ms: float = 0.0
 
 
 @dataclass
@@ -108,7 +110,8 @@ class RunMetrics:
         for i in range(min(m.n_rows, m.capacity)):
             r = rows[i]
             out.iterations.append(IterationMetrics(int(r.iteration), float(r.wall_time_s),
-                                                   int(r.dist_evals), int(r.changes)))
+                                                   int(r.dist_evals), int(r.changes),
+                                                   int(r.join_candidates), float(r.join_ms)))
         out.total_wall_time_s = float(m.total_wall_time_s)
         out.total_dist_evals = int(m.total_dist_evals)
         out.total_changes = int(m.total_changes)

@@ -296,3 +296,52 @@ def test_nndescent_l2_entry(gpu):
     assert ids.shape == (5000, 20) and m.total_dist_evals > 5000 * 20
     with pytest.raises(kg.InvalidArgument):
         kg.nndescent_l2(data, k=20, sample_rate=0.9)
+
+
+# ---------------------------------------------------------------- reorder (§8a-9)
+def clustered(n, d, c, seed):
+    """Reference-style clustered data: means on scaled basis vectors
+    (gen_clustered, dataset.hpp:116-154), shuffled order, labels returned."""
+    rng = np.random.default_rng(seed)
+    lab = rng.integers(0, c, n)
+    x = rng.standard_normal((n, d), dtype=np.float32)
+    x[np.arange(n), lab % d] += 10.0 * np.sqrt(d) * (1 + lab // d)
+    return x, lab
+
+
+def test_locality_permutation_is_bijection_and_groups_clusters(gpu, restated):
+    n, c, window = 16384, 8, 2000
+    data, lab = clustered(n, 8, c, 42)
+    g0, _ = restated.init_random(data, 20, 9)
+    c1, _ = restated.select_turbo(g0, 50, 3)
+    g1, _, _ = restated.compute_step(data, g0, c1)
+    sigma, sigma_inv = kg.locality_permutation(g1.ids, g1.dists)
+    assert np.array_equal(np.sort(sigma), np.arange(n))
+    assert np.array_equal(sigma_inv[sigma], np.arange(n))
+    # window_cluster_fraction (reorder.hpp:61-86) over the first quarter of
+    # positions; acceptance criterion 5 locks min >= 0.35, mean >= 0.5
+    order = lab[sigma_inv]
+    fr = []
+    for p in range(0, n // 4 - window + 1, window // 4):
+        fr.append(np.bincount(order[p:p + window], minlength=c).max() / window)
+    assert min(fr) >= 0.35 and np.mean(fr) >= 0.5, (min(fr), np.mean(fr))
+
+
+def test_reordered_run_returns_original_ids_and_recall(gpu):
+    # test_descent.cpp:192-224: graph in original ids with exact distances;
+    # recall within 0.01 of the run without reordering
+    data, _ = clustered(6000, 16, 12, 5)
+    base = kg.run(data, kg.RunParams(k=10, max_candidates=25, seed=5))
+    reo = kg.run(data, kg.RunParams(k=10, max_candidates=25, seed=5, reorder=True))
+    assert reo.permutation is not None
+    assert np.array_equal(np.sort(reo.permutation), np.arange(6000))
+    ex, _ = kg.brute_force_knng(data, 10)
+    r0 = kg.recall(base.graph.ids, ex)
+    r1 = kg.recall(reo.graph.ids, ex)
+    assert r1 >= r0 - 0.01, (r0, r1)
+    # distances belong to the original-id pairs
+    u = np.repeat(np.arange(6000), 10)
+    v = reo.graph.ids.ravel()
+    want = ((data[u].astype(np.float64) - data[v]) ** 2).sum(1)
+    assert np.allclose(reo.graph.dists.ravel(), want, rtol=1e-5)
+    assert not np.any(reo.graph.ids == np.arange(6000)[:, None])
