@@ -149,11 +149,18 @@ def join_roofline(mets, n, d, k, peak_tflops, config):
             t_hbm += th
             t_star += max(tf, th)
             launches += 1
-    traffic = None
+    traffic = traffic_note = None
     if os.path.exists(PROFILE_TRAFFIC):
         try:
-            traffic = json.load(open(PROFILE_TRAFFIC)).get(config)
-        except (OSError, ValueError):
+            tr = json.load(open(PROFILE_TRAFFIC)).get(config)
+            if isinstance(tr, dict):
+                traffic = tr.get("bytes_per_launch")
+                traffic_note = (f"ncu dram bytes of the {tr.get('launch')} launch; algorithmic "
+                                f"bytes of that launch {tr.get('algorithmic_bytes_same_launch'):.4g}"
+                                f" ({tr.get('source')})")
+            else:
+                traffic = tr
+        except (OSError, ValueError, TypeError):
             traffic = None
     frac = t_star / t if t else 0.0
     if t_fp >= t_hbm:
@@ -163,7 +170,7 @@ def join_roofline(mets, n, d, k, peak_tflops, config):
         roof = {"bound": "hbm", "achieved": round(frac * beta, 1), "peak": beta, "unit": "GB/s",
                 "peak_source": beta_src}
     roof.update({
-        "frac": round(frac, 4), "traffic": traffic,
+        "frac": round(frac, 4), "traffic": traffic, "traffic_note": traffic_note,
         "kernel": "join_distances_kernel (local-join distance stage)",
         "frac_definition": "sum over launches of max(F/pi, Q/beta) / sum of launch times",
         "fp32_tflops_achieved": round(F / t / 1e12, 3) if t else None,

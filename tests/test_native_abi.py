@@ -67,3 +67,27 @@ def test_no_gpu_fails_loudly(native):
     data = np.random.default_rng(0).standard_normal((100, 8), dtype=np.float32)
     with pytest.raises(kg.KnngCudaError):
         kg.run(data, kg.RunParams(k=5, max_candidates=10))
+
+
+DROPIN = os.path.join(ROOT, "tests", "cpp", "build", "dropin_check")
+
+
+@pytest.mark.skipif(not os.path.isdir("/root/reference/proj/include"),
+                    reason="reference headers absent")
+def test_cpp_dropin_builds_against_reference_headers(native):
+    import subprocess
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp")], check=True)
+    out = subprocess.run([DROPIN], capture_output=True, text=True)
+    # no GPU here: the wrapper must fail loudly with std::runtime_error (rc 3),
+    # after mapping the parameter error to std::invalid_argument
+    assert out.returncode in (0, 3), out.stdout + out.stderr
+    assert out.stdout.startswith("dropin ")
+
+
+@pytest.mark.gpu
+def test_cpp_dropin_on_gpu(gpu):
+    import subprocess
+    if not os.path.exists(DROPIN):
+        pytest.skip("drop-in check not built (needs the reference headers at build time)")
+    out = subprocess.run([DROPIN], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and "dropin OK" in out.stdout, out.stdout + out.stderr
