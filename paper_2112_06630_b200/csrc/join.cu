@@ -47,8 +47,14 @@ namespace {
 #endif
 constexpr uint32_t kThreads = KNNG_JOIN_THREADS;  // 128: 4 warps, 16 groups of 8 lanes
 constexpr uint32_t kGroups = kThreads / 8;
-constexpr uint32_t kSlab = 32;           // floats per row per smem stage
-constexpr uint32_t kStages = 3;          // cp.async pipeline depth
+#ifndef KNNG_JOIN_SLAB
+#define KNNG_JOIN_SLAB 32
+#endif
+#ifndef KNNG_JOIN_STAGES
+#define KNNG_JOIN_STAGES 3
+#endif
+constexpr uint32_t kSlab = KNNG_JOIN_SLAB;      // floats per row per smem stage
+constexpr uint32_t kStages = KNNG_JOIN_STAGES;  // cp.async pipeline depth
 constexpr uint32_t kMaxM = 2 * kMaxCap;  // candidates per node
 constexpr uint32_t kMaxRowSlots = kMaxCap + 16;
 constexpr uint32_t kMaxColSlots = kMaxM + 16;
@@ -80,7 +86,10 @@ __device__ __forceinline__ void cp_async16(float* smem_dst, const float* gmem_sr
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(gmem_src));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+template <uint32_t kPending>
+__device__ __forceinline__ void cp_async_wait_pending() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(kPending));
+}
 __device__ __forceinline__ void cp_async_wait_0() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
 __device__ __forceinline__ uint32_t swz(uint32_t slot, uint32_t seg) {
@@ -94,10 +103,11 @@ __device__ __forceinline__ uint32_t swz(uint32_t slot, uint32_t seg) {
 __device__ __forceinline__ void stage_slab(DistShared& sh, const float* __restrict__ data,
                                            uint32_t stride, uint32_t nblk, uint32_t s,
                                            uint32_t buf) {
+    constexpr uint32_t kC4 = kSlab / 4;  // 16-byte chunks per row per slab
     const uint32_t e0 = s * kSlab;
     float* dst = sh.slab[buf];
-    for (uint32_t i = threadIdx.x; i < nblk * 64u; i += kThreads) {
-        const uint32_t slot = sh.blklist[i >> 6] * 8u + ((i >> 3) & 7u), j = i & 7u;
+    for (uint32_t i = threadIdx.x; i < nblk * 8u * kC4; i += kThreads) {
+        const uint32_t slot = sh.blklist[i / (8u * kC4)] * 8u + ((i / kC4) & 7u), j = i % kC4;
         const uint32_t row = sh.colrow[slot];
         if (row == 0xffffffffu) continue;
         float* p = dst + swz(slot, j >> 1) + (j & 1u) * 4;
@@ -319,7 +329,7 @@ __global__ void __launch_bounds__(kThreads) join_distances_kernel(
                 cp_async_commit();
             }
             for (uint32_t s = 0; s < n_slabs; ++s) {
-                cp_async_wait_1();
+                cp_async_wait_pending<kStages - 2>();  // slab s has landed
                 __syncthreads();
                 if (s + kStages - 1 < n_slabs)
                     stage_slab(sh, g.data, stride, nblk, s + kStages - 1,
