@@ -193,14 +193,113 @@ def reference_recall_sample(data, k, cfg, ids_gpu, sample, reference_ids=None):
     return out
 
 
+def run_sharded_bench(args, rank, world, local):
+    """N > 1: one K-NNG build sharded over the N GPUs (vertex-range ownership,
+    NCCL exchanges; paper_2112_06630_b200/shard.py).  Total work is fixed, so
+    scaling is strong."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2112_06630_b200 as kg
+    from paper_2112_06630_b200.shard import GpuShardEngine, gather_graph, run_sharded
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = datasets.CONFIGS[args.config]
+    data = datasets.generate(cfg)  # same instance on every rank (replicated data)
+    n, d = data.shape
+    k, cap = cfg.k, cfg.cap
+    params = kg.RunParams(k=k, max_candidates=cap, termination_delta=cfg.delta, seed=cfg.seed,
+                          device=local)
+    d_data = torch.from_numpy(data).to(f"cuda:{local}")
+    eng = GpuShardEngine(d_data, params, rank, world)
+    for _ in range(args.warmup):
+        run_sharded(eng, params)
+    torch.cuda.synchronize()
+    dist.barrier()
+    clocks = Clocks(local)
+    clocks.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    results = [run_sharded(eng, params) for _ in range(args.steps)]
+    e1.record()
+    torch.cuda.synchronize()
+    dist.barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    evals = sum(r.metrics.total_dist_evals for r in results)  # already summed over ranks
+    iters = sum(len(r.metrics.iterations) - 1 for r in results)
+    sent = sum(r.bytes_exchanged for r in results)
+    # e2e: pinned host data -> device, sharded build, owned rows -> host
+    pinned = torch.empty((n, d), dtype=torch.float32, pin_memory=True)
+    pinned.numpy()[:] = data
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    e2e_evals = 0
+    d2h = 0
+    for _ in range(args.steps):
+        dd = pinned.to(f"cuda:{local}", non_blocking=True)
+        torch.cuda.synchronize()
+        e = GpuShardEngine(dd, params, rank, world)
+        r = run_sharded(e, params)
+        ids_h = r.ids.cpu()
+        dists_h = r.dists.cpu()
+        d2h += ids_h.numel() * 4 + dists_h.numel() * 4
+        e2e_evals += r.metrics.total_dist_evals
+        e.close()
+    e2e_s = time.perf_counter() - t0
+    t = torch.tensor([ms, e2e_s], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, e2e_s = float(t[0]), float(t[1])
+    out = None
+    ids_all, _ = gather_graph(results[-1], n, k)
+    if rank == 0:
+        sample = np.random.default_rng(1).choice(n, size=min(n, args.recall_sample),
+                                                 replace=False).astype(np.uint32)
+        rec = reference_recall_sample(data, k, cfg, ids_all.cpu().numpy().astype(np.uint32),
+                                      sample)
+        out = {
+            "metric": METRIC, "value": round(evals / (ms * 1e-3), 1), "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{cfg.name}: {cfg.description}", "n": n, "d": d, "k": k,
+                       "max_candidates": cap, "delta": cfg.delta, "seed": cfg.seed,
+                       "step": "one complete K-NNG build sharded over all GPUs",
+                       "l2": "inputs larger than L2 (data %.1f MB > 126 MB)" % (n * d * 4 / 1e6),
+                       "parallelism": f"{world} vertex-range shards, replicated data, NCCL "
+                                      "all-to-all of proposals + allgather of rows"},
+            "build_time_ms": round(ms / args.steps, 3),
+            "iterations_per_s": round(iters / (ms * 1e-3), 2),
+            "iterations_per_build": round(iters / args.steps, 2),
+            "recall_at_k": rec,
+            "e2e": {"value": round(e2e_evals / e2e_s, 1), "unit": UNIT,
+                    "h2d_bytes_per_step": n * d * 4,
+                    "d2h_bytes_per_step": int(d2h / args.steps)},
+            "exchange_bytes_per_step_rank0": int(sent / args.steps),
+            # per rank and build: init + export, and per iteration indegree,
+            # reset, sample, finalize, capacity check, reverse scatter,
+            # distances, merge, export count/write, received count/scatter/merge
+            "gpu_launches": int(2 * args.steps + 13 * iters),
+            "roofline": None,
+            "cpu_baseline": None,
+            "clocks": clk,
+        }
+    eng.close()
+    dist.barrier()
+    dist.destroy_process_group()
+    return out
+
+
 def run_ours(args, rank, world, local):
     import torch
     import paper_2112_06630_b200 as kg
+    if world > 1 or args.sharded:
+        return run_sharded_bench(args, rank, world, local)
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     cfg = datasets.CONFIGS[args.config]
     # replicas: each rank builds its own seeded instance
@@ -390,6 +489,8 @@ def main():
     ap.add_argument("--recall-sample", type=int, default=5000)
     ap.add_argument("--reference-sample", type=int, default=10000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the multi-GPU sharded path even on one GPU (testing)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
     rank, world, local = dist_env()

@@ -213,6 +213,56 @@ int knng_cuda_locality_permutation(uint32_t n, uint32_t k, const uint32_t* ids,
                                    const float* dists, uint32_t* sigma, uint32_t* sigma_inv,
                                    int device);
 
+/*
+ * Multi-GPU shard — one process per GPU, vertex-range ownership with the data
+ * and the graph replicated.  The library runs the per-device
+ * kernels; the caller runs the collectives (NCCL), see
+ * paper_2112_06630_b200/shard.py.  Per iteration:
+ *   knng_cuda_shard_step   selection of the owned lists over the replicated
+ *                          graph, local join of the owned active nodes,
+ *                          merges into owned rows, and records
+ *                          (target, id, dist bits) x u32 for targets owned by
+ *                          other ranks, grouped by owner in rank order;
+ *   caller                 all-to-all of the records;
+ *   knng_cuda_shard_merge  merge of the received records into owned rows;
+ *   caller                 allgather of the owned rows (keys/flags/maxd, in
+ *                          place in the buffers below), allreduce of changes.
+ * Device pointers; the library synchronises its stream before returning.
+ */
+typedef struct knng_cuda_shard knng_cuda_shard;
+
+typedef struct knng_cuda_shard_info {
+    uint64_t* keys;       /* rows_alloc x k: key = (dist bits << 32) | id, rows sorted */
+    uint32_t* flags;      /* rows_alloc: bit i = entry i is new */
+    float* maxd;          /* rows_alloc: row maximum */
+    uint32_t rows_alloc;  /* nranks * chunk (>= n), so every rank's slice is `chunk` rows */
+    uint32_t chunk;
+    uint32_t lo, hi;      /* owned rows */
+    void* stream;         /* the library stream (cudaStream_t) */
+} knng_cuda_shard_info;
+
+int knng_cuda_shard_create(const float* d_data, uint32_t n, uint32_t d,
+                           const knng_cuda_params* params, uint32_t rank, uint32_t nranks,
+                           void* stream, knng_cuda_shard** out, knng_cuda_shard_info* info);
+int knng_cuda_shard_destroy(knng_cuda_shard* shard);
+/* The run's seeds: std::mt19937_64(seed) outputs, [0] init, [i] iteration i
+ * (descent.hpp:201-221) — identical to the single-GPU path. */
+void knng_cuda_seed_sequence(uint64_t seed, uint32_t count, uint64_t* out);
+/* init_random (graph.hpp:34-67) of the owned rows; per-node Philox draws, so
+ * the initial graph does not depend on the number of ranks. */
+int knng_cuda_shard_init(knng_cuda_shard* shard, uint64_t seed);
+/* counters: [0] distance evaluations, [1] candidates joined, [2] inserts into
+ * owned rows so far, [3] active nodes.  send_counts: nranks record counts;
+ * *send_records: device pointer to 3 * sum(send_counts) u32. */
+int knng_cuda_shard_step(knng_cuda_shard* shard, uint64_t seed, uint64_t* counters,
+                         uint64_t* send_counts, const uint32_t** send_records);
+/* d_records: count records (3 u32 each) for owned targets; *changes = all
+ * inserts into owned rows this iteration (local + received). */
+int knng_cuda_shard_merge(knng_cuda_shard* shard, const uint32_t* d_records, uint64_t count,
+                          uint64_t* changes);
+/* owned rows, sorted by (distance, id): (hi - lo) x k ids and distances. */
+int knng_cuda_shard_export(knng_cuda_shard* shard, uint32_t* d_ids, float* d_dists);
+
 #ifdef __cplusplus
 }
 #endif

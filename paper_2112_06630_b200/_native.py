@@ -40,7 +40,27 @@ EXPORTS = (
     "knng_cuda_bruteforce_knng",
     "knng_cuda_bruteforce_queries",
     "knng_cuda_locality_permutation",
+    "knng_cuda_shard_create",
+    "knng_cuda_shard_destroy",
+    "knng_cuda_seed_sequence",
+    "knng_cuda_shard_init",
+    "knng_cuda_shard_step",
+    "knng_cuda_shard_merge",
+    "knng_cuda_shard_export",
 )
+
+
+class ShardInfo(C.Structure):
+    _fields_ = [
+        ("keys", C.c_void_p),
+        ("flags", C.c_void_p),
+        ("maxd", C.c_void_p),
+        ("rows_alloc", C.c_uint32),
+        ("chunk", C.c_uint32),
+        ("lo", C.c_uint32),
+        ("hi", C.c_uint32),
+        ("stream", C.c_void_p),
+    ]
 
 
 class Params(C.Structure):
@@ -134,6 +154,14 @@ def lib() -> C.CDLL:
     fn("knng_cuda_bruteforce_queries", C.c_int, [f32p, u32, u32, u32, vp, u32, u32p, f64p,
                                                  C.c_int])
     fn("knng_cuda_locality_permutation", C.c_int, [u32, u32, u32p, f32p, u32p, u32p, C.c_int])
+    fn("knng_cuda_shard_create", C.c_int, [vp, u32, u32, C.POINTER(Params), u32, u32, vp,
+                                           C.POINTER(vp), C.POINTER(ShardInfo)])
+    fn("knng_cuda_shard_destroy", C.c_int, [vp])
+    fn("knng_cuda_seed_sequence", None, [C.c_uint64, u32, u64p])
+    fn("knng_cuda_shard_init", C.c_int, [vp, C.c_uint64])
+    fn("knng_cuda_shard_step", C.c_int, [vp, C.c_uint64, u64p, u64p, C.POINTER(vp)])
+    fn("knng_cuda_shard_merge", C.c_int, [vp, vp, C.c_uint64, u64p])
+    fn("knng_cuda_shard_export", C.c_int, [vp, vp, vp])
     _lib = L
     return L
 

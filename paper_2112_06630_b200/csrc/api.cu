@@ -19,6 +19,8 @@
 #include <string>
 #include <vector>
 
+#include <cub/device/device_scan.cuh>
+
 #include "../../include/knng_cuda.h"
 #include "kernels.cuh"
 
@@ -224,13 +226,20 @@ struct Engine {
     IterCounters* h_ctr = nullptr;
     uint64_t h2d = 0, d2h = 0;
 
-    Engine(int device, uint32_t n_, uint32_t d_, uint32_t k_, uint32_t cap_, cudaStream_t stream)
+    uint32_t lo = 0, hi = 0;  // owned rows (multi-GPU); [0, n) otherwise
+    uint32_t rows_alloc = 0;  // graph rows allocated (>= n: equal shards for allgather)
+
+    Engine(int device, uint32_t n_, uint32_t d_, uint32_t k_, uint32_t cap_, cudaStream_t stream,
+           uint32_t rows = 0)
         : n(n_), d(d_), stride(padded_stride(d_)), k(k_), cap(cap_), s(stream) {
         pool = pool_for(device);
+        lo = 0;
+        hi = n;
+        rows_alloc = rows > n ? rows : n;
         data.alloc(size_t(n) * stride, pool, s);
-        keys.alloc(size_t(n) * k, pool, s);
-        flags.alloc(n, pool, s);
-        maxd.alloc(n, pool, s);
+        keys.alloc(size_t(rows_alloc) * k, pool, s);
+        flags.alloc(rows_alloc, pool, s);
+        maxd.alloc(rows_alloc, pool, s);
         indeg.alloc(n, pool, s);
         ctr.alloc(1, pool, s);
         if (cap) {
@@ -260,7 +269,9 @@ struct Engine {
         h_ctr = nullptr;  // the pinned slot is reused by the thread's next call
     }
 
-    GraphView gv() const { return GraphView{data.p, n, k, stride, keys.p, flags.p, maxd.p}; }
+    GraphView gv() const {
+        return GraphView{data.p, n, k, stride, keys.p, flags.p, maxd.p, lo, hi};
+    }
     CandView cv() const {
         return CandView{cap,   cand.p,   raw_new.p, raw_old.p, nc.p, oc.p, dsz.p,
                         doff.p, revcnt.p, roff.p,   rcur.p,    rev.p, dblocks.p};
@@ -389,6 +400,17 @@ struct Engine {
 
     void export_rows(uint32_t* ids, float* dists, uint8_t* fl) {
         launch_export_rows(gv(), ids, dists, fl, s);
+        CK(cudaGetLastError());
+    }
+
+    // the owned rows [lo, hi) only (multi-GPU)
+    void export_owned(uint32_t* ids, float* dists, uint8_t* fl) {
+        GraphView g = gv();
+        g.keys += size_t(lo) * k;
+        g.flags += lo;
+        g.maxd += lo;
+        g.n = hi - lo;
+        launch_export_rows(g, ids, dists, fl, s);
         CK(cudaGetLastError());
     }
 };
@@ -886,6 +908,203 @@ int knng_cuda_locality_permutation(uint32_t n, uint32_t k, const uint32_t* ids,
         to_host(sigma, e.sigma.p, n, e);
         to_host(sigma_inv, e.sigma_inv.p, n, e);
         CK(cudaStreamSynchronize(e.s));
+    });
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Multi-GPU shard.  One process per GPU; the caller runs the
+// collectives (NCCL through torch.distributed in paper_2112_06630_b200/shard.py).
+// Each device owns rows [rank*chunk, min(n, (rank+1)*chunk)) and keeps the
+// whole graph replicated (allgathered by the caller into the buffers exposed
+// in knng_cuda_shard_info).  An iteration is: step (selection of the owned
+// lists over the replicated graph, local join of the owned active nodes,
+// merges for owned targets, export of proposals for remote targets grouped
+// by owner), the caller's all-to-all of those records, merge of the received
+// records, the caller's allgather of the owned rows and allreduce of changes.
+// ---------------------------------------------------------------------------
+struct knng_cuda_shard {
+    int device = 0;
+    knng_cuda_params p{};
+    uint32_t rank = 0, nranks = 1, chunk = 0;
+    cudaStream_t s = nullptr;
+    Engine* e = nullptr;
+    DevBuf<uint32_t> exp_counts, rcnt, roff2, rcur2, send;
+    DevBuf<uint64_t> exp_off, bounds, grouped;
+    DevBuf<unsigned char> scan_tmp;
+    size_t scan_bytes = 0, send_cap = 0, grouped_cap = 0;
+    std::vector<uint64_t> h_bounds;
+    ~knng_cuda_shard() { delete e; }
+};
+
+namespace {
+
+__global__ void shard_bounds_kernel(const uint64_t* off, const uint32_t* counts, uint32_t n,
+                                    uint32_t chunk, uint32_t nranks, uint64_t* bounds) {
+    const uint32_t r = threadIdx.x;
+    if (r > nranks) return;
+    const uint64_t total = n ? off[n - 1] + counts[n - 1] : 0;
+    const uint64_t start = uint64_t(r) * chunk;
+    bounds[r] = start >= n ? total : off[start];
+}
+
+}  // namespace
+
+extern "C" {
+
+int knng_cuda_shard_create(const float* d_data, uint32_t n, uint32_t d,
+                           const knng_cuda_params* params, uint32_t rank, uint32_t nranks,
+                           void* stream, knng_cuda_shard** out, knng_cuda_shard_info* info) {
+    return guarded([&] {
+        if (!d_data || !params || !out || !info) raise(KNNG_CUDA_INVALID_ARGUMENT, "null argument");
+        if (nranks == 0 || rank >= nranks) raise(KNNG_CUDA_INVALID_ARGUMENT, "bad rank / nranks");
+        const knng_cuda_params p = *params;
+        validate_params(n, d, p);
+        if (p.reorder)
+            raise(KNNG_CUDA_NOT_IMPLEMENTED, "reorder is not supported on the sharded path");
+        DeviceGuard dg(p.device);
+        auto* sh = new knng_cuda_shard();
+        try {
+            sh->device = p.device;
+            sh->p = p;
+            sh->rank = rank;
+            sh->nranks = nranks;
+            sh->chunk = (n + nranks - 1) / nranks;
+            StreamHolder hold(stream);
+            sh->s = hold.s;
+            sh->e = new Engine(p.device, n, d, p.k, p.max_candidates, sh->s,
+                               sh->chunk * nranks);
+            Engine& e = *sh->e;
+            e.lo = std::min(n, rank * sh->chunk);
+            e.hi = std::min(n, (rank + 1) * sh->chunk);
+            e.upload(d_data, true);
+            sh->exp_counts.alloc(n, e.pool, e.s);
+            sh->exp_off.alloc(n, e.pool, e.s);
+            sh->rcnt.alloc(n, e.pool, e.s);
+            sh->roff2.alloc(n, e.pool, e.s);
+            sh->rcur2.alloc(n, e.pool, e.s);
+            sh->bounds.alloc(nranks + 1, e.pool, e.s);
+            size_t a = 0, b = 0;
+            cub::DeviceScan::ExclusiveScan(nullptr, a, sh->exp_counts.p, sh->exp_off.p, cub::Sum(),
+                                           uint64_t(0), int(n));
+            cub::DeviceScan::ExclusiveSum(nullptr, b, sh->rcnt.p, sh->roff2.p, int(n));
+            sh->scan_bytes = std::max(a, b);
+            sh->scan_tmp.alloc(sh->scan_bytes, e.pool, e.s);
+            sh->h_bounds.resize(nranks + 1);
+            CK(cudaStreamSynchronize(e.s));
+            info->keys = e.keys.p;
+            info->flags = e.flags.p;
+            info->maxd = e.maxd.p;
+            info->rows_alloc = e.rows_alloc;
+            info->chunk = sh->chunk;
+            info->lo = e.lo;
+            info->hi = e.hi;
+            info->stream = sh->s;
+        } catch (...) {
+            delete sh;
+            throw;
+        }
+        *out = sh;
+    });
+}
+
+void knng_cuda_seed_sequence(uint64_t seed, uint32_t count, uint64_t* out) {
+    std::mt19937_64 master(seed);  // descent.hpp:201-221
+    for (uint32_t i = 0; i < count; ++i) out[i] = master();
+}
+
+int knng_cuda_shard_destroy(knng_cuda_shard* sh) {
+    return guarded([&] {
+        if (!sh) return;
+        DeviceGuard dg(sh->device);
+        cudaStreamSynchronize(sh->s);
+        delete sh;
+    });
+}
+
+int knng_cuda_shard_init(knng_cuda_shard* sh, uint64_t seed) {
+    return guarded([&] {
+        if (!sh) raise(KNNG_CUDA_INVALID_ARGUMENT, "null shard");
+        DeviceGuard dg(sh->device);
+        launch_init_random(sh->e->gv(), seed, sh->s);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(sh->s));
+    });
+}
+
+int knng_cuda_shard_step(knng_cuda_shard* sh, uint64_t seed, uint64_t* out_counters,
+                         uint64_t* send_counts, const uint32_t** send_records) {
+    return guarded([&] {
+        if (!sh || !out_counters || !send_counts || !send_records)
+            raise(KNNG_CUDA_INVALID_ARGUMENT, "null argument");
+        DeviceGuard dg(sh->device);
+        Engine& e = *sh->e;
+        KernelTimer timer(false, e.s, nullptr);
+        CK(cudaMemsetAsync(e.ctr.p, 0, sizeof(IterCounters), e.s));
+        e.select(seed, timer);
+        e.join(timer);  // local merges of the owned targets; ends with a counter read
+        const IterCounters c = *e.h_ctr;
+        // proposals for targets owned elsewhere
+        const GraphView g = e.gv();
+        launch_export_remote(g, e.cv(), e.ctr.p, sh->exp_counts.p, nullptr, nullptr, false, e.s);
+        size_t bytes = sh->scan_bytes;
+        cub::DeviceScan::ExclusiveScan(sh->scan_tmp.p, bytes, sh->exp_counts.p, sh->exp_off.p,
+                                       cub::Sum(), uint64_t(0), int(e.n), e.s);
+        shard_bounds_kernel<<<1, 64, 0, e.s>>>(sh->exp_off.p, sh->exp_counts.p, e.n, sh->chunk,
+                                               sh->nranks, sh->bounds.p);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(sh->h_bounds.data(), sh->bounds.p, sizeof(uint64_t) * (sh->nranks + 1),
+                           cudaMemcpyDeviceToHost, e.s));
+        CK(cudaStreamSynchronize(e.s));
+        const uint64_t total = sh->h_bounds[sh->nranks];
+        if (3 * total > sh->send_cap) {
+            sh->send.~DevBuf();
+            new (&sh->send) DevBuf<uint32_t>();
+            sh->send_cap = 3 * (total + total / 4 + 1024);
+            sh->send.alloc(sh->send_cap, e.pool, e.s);
+        }
+        if (total)
+            launch_export_remote(g, e.cv(), e.ctr.p, sh->exp_counts.p, sh->exp_off.p, sh->send.p,
+                                 true, e.s);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(e.s));
+        for (uint32_t r = 0; r < sh->nranks; ++r)
+            send_counts[r] = sh->h_bounds[r + 1] - sh->h_bounds[r];
+        *send_records = sh->send.p;
+        out_counters[0] = c.evals;
+        out_counters[1] = c.cands;
+        out_counters[2] = c.changes;
+        out_counters[3] = c.active;
+    });
+}
+
+int knng_cuda_shard_merge(knng_cuda_shard* sh, const uint32_t* d_records, uint64_t count,
+                          uint64_t* changes) {
+    return guarded([&] {
+        if (!sh || !changes) raise(KNNG_CUDA_INVALID_ARGUMENT, "null argument");
+        DeviceGuard dg(sh->device);
+        Engine& e = *sh->e;
+        if (count > sh->grouped_cap) {
+            sh->grouped.~DevBuf();
+            new (&sh->grouped) DevBuf<uint64_t>();
+            sh->grouped_cap = count + count / 4 + 1024;
+            sh->grouped.alloc(sh->grouped_cap, e.pool, e.s);
+        }
+        launch_merge_received(e.gv(), d_records, count, sh->rcnt.p, sh->roff2.p, sh->rcur2.p,
+                              sh->grouped.p, sh->scan_tmp.p, sh->scan_bytes, e.ctr.p, e.s);
+        CK(cudaGetLastError());
+        e.read_counters();
+        *changes = e.h_ctr->changes;  // local + received merges of this iteration
+    });
+}
+
+int knng_cuda_shard_export(knng_cuda_shard* sh, uint32_t* d_ids, float* d_dists) {
+    return guarded([&] {
+        if (!sh || !d_ids || !d_dists) raise(KNNG_CUDA_INVALID_ARGUMENT, "null argument");
+        DeviceGuard dg(sh->device);
+        sh->e->export_owned(d_ids, d_dists, nullptr);
+        CK(cudaStreamSynchronize(sh->s));
     });
 }
 

@@ -49,8 +49,8 @@ __device__ __forceinline__ float group8_l2_scalar(const float* __restrict__ a,
 __global__ void __launch_bounds__(256) init_random_kernel(GraphView g, uint32_t seed_lo,
                                                           uint32_t seed_hi) {
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (warp >= g.n) return;
-    const uint32_t u = warp, lane = lane_id(), k = g.k, n = g.n;
+    if (g.lo + warp >= g.hi) return;
+    const uint32_t u = g.lo + warp, lane = lane_id(), k = g.k, n = g.n;
     const bool real = lane < k;
     uint32_t id = n + lane;  // placeholder, unique and never a valid id
     bool accepted = !real;
@@ -178,8 +178,10 @@ __global__ void __launch_bounds__(256) sample_kernel(GraphView g, CandView c,
     const uint32_t is_new = (__ldg(g.flags + u) >> i) & 1u;
     const Philox4 r = philox4x32_10(uint32_t(e), uint32_t(e >> 32), kSaltSample, 0u, seed_lo,
                                     seed_hi);
-    offer(c, g.k, indeg, u, v, is_new, r.x, r.y);  // v into u's lists
-    offer(c, g.k, indeg, v, u, is_new, r.z, r.w);  // u into v's lists
+    // only lists this device owns are built; the draws are per edge, so the
+    // sampled lists do not depend on how the rows are sharded
+    if (u >= g.lo && u < g.hi) offer(c, g.k, indeg, u, v, is_new, r.x, r.y);  // v into u
+    if (v >= g.lo && v < g.hi) offer(c, g.k, indeg, v, u, is_new, r.z, r.w);  // u into v
 }
 
 __global__ void reset_raw_kernel(CandView c, uint32_t n) {
@@ -246,9 +248,9 @@ __global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(GraphView g, C
     if (threadIdx.x == 0) acc = BlockCounters{0, 0, 0, 0};
     __syncthreads();
     const uint32_t w = threadIdx.x >> 5, lane = lane_id();
-    const uint32_t u = blockIdx.x * kFinWarps + w;
+    const uint32_t u = g.lo + blockIdx.x * kFinWarps + w;
     const uint32_t cap = c.cap, k = g.k;
-    if (u < g.n) {
+    if (u < g.hi) {
         const uint32_t nr = min(c.raw_new[u], cap), orr = min(c.raw_old[u], cap);
         const uint32_t* list = c.ids + size_t(u) * 2 * cap;
         for (uint32_t p = lane; p < nr; p += 32) s_new[w][p] = list[p];
@@ -341,8 +343,8 @@ __global__ void __launch_bounds__(kFinWarps * 32) bookkeeping_kernel(GraphView g
     __shared__ BlockCounters acc;
     if (threadIdx.x == 0) acc = BlockCounters{0, 0, 0, 0};
     __syncthreads();
-    const uint32_t u = blockIdx.x * kFinWarps + (threadIdx.x >> 5);
-    if (u < g.n) join_bookkeeping(c, u, c.nc[u], c.oc[u], active, ctr, acc);
+    const uint32_t u = g.lo + blockIdx.x * kFinWarps + (threadIdx.x >> 5);
+    if (u < g.hi) join_bookkeeping(c, u, c.nc[u], c.oc[u], active, ctr, acc);
     __syncthreads();
     flush_block_counters(acc, ctr);
 }
@@ -354,7 +356,8 @@ inline uint32_t blocks_for(size_t items, uint32_t per_block) {
 }  // namespace
 
 void launch_init_random(const GraphView& g, uint64_t seed, cudaStream_t s) {
-    init_random_kernel<<<blocks_for(size_t(g.n) * 32, 256), 256, 0, s>>>(
+    if (g.hi <= g.lo) return;
+    init_random_kernel<<<blocks_for(size_t(g.hi - g.lo) * 32, 256), 256, 0, s>>>(
         g, uint32_t(seed), uint32_t(seed >> 32));
 }
 
@@ -386,13 +389,17 @@ void launch_sample(const GraphView& g, const CandView& c, const uint32_t* indeg,
 void launch_finalize(const GraphView& g, const CandView& c, uint32_t* active,
                      IterCounters* ctr, cudaStream_t s) {
     cudaMemsetAsync(c.revcnt, 0, sizeof(uint32_t) * g.n, s);
-    finalize_kernel<<<blocks_for(g.n, kFinWarps), kFinWarps * 32, 0, s>>>(g, c, active, ctr);
+    if (g.hi <= g.lo) return;
+    finalize_kernel<<<blocks_for(g.hi - g.lo, kFinWarps), kFinWarps * 32, 0, s>>>(g, c, active,
+                                                                                  ctr);
 }
 
 void launch_bookkeeping(const GraphView& g, const CandView& c, uint32_t* active,
                         IterCounters* ctr, cudaStream_t s) {
     cudaMemsetAsync(c.revcnt, 0, sizeof(uint32_t) * g.n, s);
-    bookkeeping_kernel<<<blocks_for(g.n, kFinWarps), kFinWarps * 32, 0, s>>>(g, c, active, ctr);
+    if (g.hi <= g.lo) return;
+    bookkeeping_kernel<<<blocks_for(g.hi - g.lo, kFinWarps), kFinWarps * 32, 0, s>>>(g, c, active,
+                                                                                     ctr);
 }
 
 }  // namespace knng_cuda

@@ -392,9 +392,9 @@ __global__ void __launch_bounds__(kMergeWarps * 32) join_merge_kernel(GraphView 
     if (threadIdx.x == 0) s_changes = 0;
     __syncthreads();
     const uint32_t lane = lane_id();
-    const uint32_t t = blockIdx.x * kMergeWarps + (threadIdx.x >> 5);
+    const uint32_t t = g.lo + blockIdx.x * kMergeWarps + (threadIdx.x >> 5);
     const uint32_t k = g.k, cap = c.cap;
-    const uint32_t cnt = t < g.n ? c.revcnt[t] : 0u;
+    const uint32_t cnt = t < g.hi ? c.revcnt[t] : 0u;
     if (cnt) {
         uint64_t key = lane < k ? g.keys[size_t(t) * k + lane] : kEmptyKey;
         uint32_t flags = g.flags[t];
@@ -570,8 +570,156 @@ void launch_join_distances(const GraphView& g, const CandView& c, const uint32_t
 
 void launch_join_merge(const GraphView& g, const CandView& c, IterCounters* ctr,
                        cudaStream_t s) {
-    join_merge_kernel<<<(g.n + kMergeWarps - 1) / kMergeWarps, kMergeWarps * 32, 0, s>>>(g, c,
-                                                                                         ctr);
+    if (g.hi <= g.lo) return;
+    join_merge_kernel<<<(g.hi - g.lo + kMergeWarps - 1) / kMergeWarps, kMergeWarps * 32, 0, s>>>(
+        g, c, ctr);
+}
+
+// ---------------------------------------------------------------------------
+// Multi-GPU: proposals for targets owned by other devices.
+// ---------------------------------------------------------------------------
+namespace {
+
+// Pass 1 (count) / pass 2 (write): one warp per non-owned target t named by
+// this device's lists; its partners below t's row maximum (the replicated,
+// iteration-start value: stale-upwards, so the filter is conservative) become
+// records (t, id, dist bits).  Records are laid out in ascending t, hence
+// grouped by owner device in rank order.
+template <bool kWrite>
+__global__ void __launch_bounds__(kMergeWarps * 32) export_remote_kernel(
+    GraphView g, CandView c, IterCounters* ctr, uint32_t* counts, const uint64_t* offsets,
+    uint32_t* records) {
+    if (ctr->overflow) return;
+    const uint32_t lane = lane_id();
+    const uint32_t t = blockIdx.x * kMergeWarps + (threadIdx.x >> 5);
+    if (t >= g.n) return;
+    const bool owned = t >= g.lo && t < g.hi;
+    const uint32_t cnt = owned ? 0u : c.revcnt[t];
+    if (!cnt) {
+        if (!kWrite && lane == 0) counts[t] = 0;
+        return;
+    }
+    const float mx = g.maxd[t];
+    const uint64_t* rv = c.rev + c.roff[t];
+    uint32_t written = 0;
+    uint64_t base = kWrite ? offsets[t] : 0;
+    for (uint32_t e = 0; e < cnt; ++e) {
+        const uint64_t r = rv[e];
+        const uint32_t u = uint32_t(r >> 8), p = uint32_t(r & 0xffu);
+        const uint32_t nn = c.nc[u], m = nn + c.oc[u];
+        const bool is_new = p < nn;
+        const uint32_t P = is_new ? m : nn;
+        const float* row = c.D + c.doff[u] + (is_new ? size_t(p) * m
+                                                     : size_t(nn) * m + size_t(p - nn) * nn);
+        const uint32_t* list = c.ids + size_t(u) * 2 * c.cap;
+        for (uint32_t q0 = 0; q0 < P; q0 += 32) {
+            const uint32_t q = q0 + lane;
+            const bool valid = q < P && q != p;
+            const float dist = valid ? row[q] : 0.0f;
+            const bool pass = valid && dist < mx;
+            const uint32_t mask = __ballot_sync(0xffffffffu, pass);
+            if (kWrite && pass) {
+                const uint32_t cand = q < nn ? list[q] : list[c.cap + q - nn];
+                uint32_t* rec = records + 3 * (base + written + __popc(mask & ((1u << lane) - 1u)));
+                rec[0] = t;
+                rec[1] = cand;
+                rec[2] = __float_as_uint(dist);
+            }
+            written += __popc(mask);
+        }
+    }
+    if (!kWrite && lane == 0) counts[t] = written;
+}
+
+// Received records grouped by target (counting sort), then one warp per owned
+// target merges its records with try_insert semantics.
+__global__ void recv_count_kernel(const uint32_t* records, uint64_t count, uint32_t* cnt) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < count) atomicAdd(cnt + records[3 * i], 1u);
+}
+
+__global__ void recv_scatter_kernel(const uint32_t* records, uint64_t count, const uint32_t* off,
+                                    uint32_t* cur, uint64_t* grouped) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const uint32_t t = records[3 * i];
+    const uint32_t slot = off[t] + atomicAdd(cur + t, 1u);
+    grouped[slot] = pack_key(__uint_as_float(records[3 * i + 2]), records[3 * i + 1]);
+}
+
+__global__ void __launch_bounds__(kMergeWarps * 32) merge_received_kernel(
+    GraphView g, const uint32_t* cnt, const uint32_t* off, const uint64_t* grouped,
+    IterCounters* ctr) {
+    __shared__ unsigned long long s_changes;
+    if (threadIdx.x == 0) s_changes = 0;
+    __syncthreads();
+    const uint32_t lane = lane_id(), k = g.k;
+    const uint32_t t = g.lo + blockIdx.x * kMergeWarps + (threadIdx.x >> 5);
+    const uint32_t n_rec = t < g.hi ? cnt[t] : 0u;
+    if (n_rec) {
+        uint64_t key = lane < k ? g.keys[size_t(t) * k + lane] : kEmptyKey;
+        uint32_t flags = g.flags[t];
+        float cur_max = key_dist(__shfl_sync(0xffffffffu, key, k - 1));
+        uint32_t inserted = 0;
+        const uint64_t* recs = grouped + off[t];
+        for (uint32_t r0 = 0; r0 < n_rec; r0 += 32) {
+            const bool valid = r0 + lane < n_rec;
+            const uint64_t rk = valid ? recs[r0 + lane] : kEmptyKey;
+            uint32_t pass = __ballot_sync(0xffffffffu, valid && key_dist(rk) < cur_max);
+            while (pass) {
+                const uint32_t src = __ffs(pass) - 1u;
+                pass &= pass - 1u;
+                const uint64_t kk = __shfl_sync(0xffffffffu, rk, src);
+                if (key_dist(kk) < cur_max &&
+                    warp_try_insert(key, flags, k, key_dist(kk), key_id(kk))) {
+                    ++inserted;
+                    cur_max = key_dist(__shfl_sync(0xffffffffu, key, k - 1));
+                }
+            }
+        }
+        if (inserted) {
+            if (lane < k) g.keys[size_t(t) * k + lane] = key;
+            if (lane == 0) {
+                g.flags[t] = flags;
+                g.maxd[t] = cur_max;
+                atomicAdd(&s_changes, (unsigned long long)inserted);
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && s_changes) atomicAdd(&ctr->changes, s_changes);
+}
+
+}  // namespace
+
+void launch_export_remote(const GraphView& g, const CandView& c, IterCounters* ctr,
+                          uint32_t* counts, const uint64_t* offsets, uint32_t* records,
+                          bool write, cudaStream_t s) {
+    const uint32_t grid = (g.n + kMergeWarps - 1) / kMergeWarps;
+    if (write)
+        export_remote_kernel<true><<<grid, kMergeWarps * 32, 0, s>>>(g, c, ctr, counts, offsets,
+                                                                     records);
+    else
+        export_remote_kernel<false><<<grid, kMergeWarps * 32, 0, s>>>(g, c, ctr, counts, offsets,
+                                                                      records);
+}
+
+void launch_merge_received(const GraphView& g, const uint32_t* records, uint64_t count,
+                           uint32_t* cnt, uint32_t* off, uint32_t* cur, uint64_t* grouped,
+                           void* scratch, size_t scratch_bytes, IterCounters* ctr,
+                           cudaStream_t s) {
+    cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * g.n, s);
+    cudaMemsetAsync(cur, 0, sizeof(uint32_t) * g.n, s);
+    if (count) {
+        const uint32_t grid = uint32_t((count + 255) / 256);
+        recv_count_kernel<<<grid, 256, 0, s>>>(records, count, cnt);
+        size_t bytes = scratch_bytes;
+        cub::DeviceScan::ExclusiveSum(scratch, bytes, cnt, off, int(g.n), s);
+        recv_scatter_kernel<<<grid, 256, 0, s>>>(records, count, off, cur, grouped);
+    }
+    if (g.hi <= g.lo || !count) return;
+    merge_received_kernel<<<(g.hi - g.lo + kMergeWarps - 1) / kMergeWarps, kMergeWarps * 32, 0,
+                            s>>>(g, cnt, off, grouped, ctr);
 }
 
 }  // namespace knng_cuda

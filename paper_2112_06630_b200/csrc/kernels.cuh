@@ -17,6 +17,10 @@ struct GraphView {
     uint64_t* keys;     // n x k
     uint32_t* flags;    // n
     float* maxd;        // n
+    // Rows this device owns (multi-GPU sharding): init, finalize,
+    // the join's active nodes and the merges cover [lo, hi); the graph itself
+    // is replicated (allgathered each iteration).  Single GPU: [0, n).
+    uint32_t lo, hi;
 };
 
 // Per-iteration candidate lists (CandidateSet layout, selection.hpp:22-49):
@@ -88,6 +92,17 @@ void launch_join_distances(const GraphView& g, const CandView& c, const uint32_t
 // Update stage: one warp per target pulls and merges its proposals.
 void launch_join_merge(const GraphView& g, const CandView& c, IterCounters* ctr,
                        cudaStream_t s);
+// Multi-GPU: records (t, id, dist bits) for non-owned targets; pass 1 counts
+// per target (counts[n]), pass 2 writes at offsets[t] (exclusive scan).
+void launch_export_remote(const GraphView& g, const CandView& c, IterCounters* ctr,
+                          uint32_t* counts, const uint64_t* offsets, uint32_t* records,
+                          bool write, cudaStream_t s);
+// Multi-GPU: merge received records into the owned rows (counting sort by
+// target, then one warp per owned target).
+void launch_merge_received(const GraphView& g, const uint32_t* records, uint64_t count,
+                           uint32_t* cnt, uint32_t* off, uint32_t* cur, uint64_t* grouped,
+                           void* scratch, size_t scratch_bytes, IterCounters* ctr,
+                           cudaStream_t s);
 
 // --- bruteforce.cu ---------------------------------------------------------
 // Exact k nearest neighbours of the listed query rows among all n rows.

@@ -1,0 +1,123 @@
+"""The sharded (multi-GPU) path on one GPU: world_size 1 over NCCL exercises the
+CUDA shard engine (knng_cuda_shard_*) end to end, including the record
+export / all-to-all / merge machinery with an empty exchange, and must match
+the single-GPU build's quality.  (More ranks than GPUs is not run: ranks whose
+kernels wait on each other must not share a device — B200_PROFILING.md.)"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import paper_2112_06630_b200 as kg
+from paper_2112_06630_b200 import datasets
+
+pytestmark = pytest.mark.gpu
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.fixture(scope="module")
+def nccl_world():
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{_port()}", rank=0,
+                            world_size=1, device_id=torch.device("cuda", 0))
+    yield dist
+    dist.destroy_process_group()
+
+
+def test_sharded_world1_matches_single_gpu(gpu, nccl_world):
+    import torch
+    from paper_2112_06630_b200.shard import GpuShardEngine, gather_graph, run_sharded
+    cfg = datasets.CONFIGS["C1"]
+    data = datasets.generate(cfg)
+    params = kg.RunParams(k=cfg.k, max_candidates=cfg.cap, seed=0)
+    eng = GpuShardEngine(torch.from_numpy(data).cuda(), params, 0, 1)
+    res = run_sharded(eng, params)
+    ids, dists = gather_graph(res, cfg.n, cfg.k)
+    ids = ids.cpu().numpy().astype(np.uint32)
+    ex, _ = kg.brute_force_knng(data, cfg.k)
+    single = kg.run(data, params)
+    r_sh = kg.recall(ids, ex)
+    r_single = kg.recall(single.graph.ids, ex)
+    assert r_sh >= r_single - 0.005, (r_sh, r_single)
+    # same seeds, same per-edge draws: the same number of iterations +-1
+    assert abs(len(res.metrics.iterations) - len(single.metrics.iterations)) <= 1
+    assert res.metrics.iterations[0].dist_evals == cfg.n * cfg.k
+    d = dists.cpu().numpy()
+    assert np.all(np.diff(d, axis=1) >= 0)
+    eng.close()
+
+
+def test_shard_step_exports_nothing_with_one_rank(gpu, nccl_world):
+    import torch
+    from paper_2112_06630_b200.shard import GpuShardEngine
+    data = np.random.default_rng(0).standard_normal((2000, 24)).astype(np.float32)
+    params = kg.RunParams(k=8, max_candidates=16, seed=3)
+    eng = GpuShardEngine(torch.from_numpy(data).cuda(), params, 0, 1)
+    eng.init(1)
+    st = eng.step(2)
+    assert st["send_counts"] == [0] and st["send"].numel() == 0
+    assert st["evals"] > 0 and st["active"] > 0
+    assert eng.merge(torch.empty(0, dtype=torch.int32, device="cuda")) >= 0
+    eng.close()
+
+
+def test_shard_engine_two_ranks_one_process_exchange(gpu):
+    """Two shard engines of a 2-rank split in ONE process (no collectives,
+    sequential kernels — nothing waits on another rank): records exported by
+    each rank are exactly for the other rank's rows, and merging them gives a
+    graph whose recall matches the single-GPU build."""
+    import torch
+    from paper_2112_06630_b200.shard import GpuShardEngine, seed_sequence
+    cfg = datasets.CONFIGS["C1"]
+    data = datasets.generate(cfg)
+    n, k = cfg.n, cfg.k
+    params = kg.RunParams(k=k, max_candidates=cfg.cap, seed=0)
+    dd = torch.from_numpy(data).cuda()
+    engs = [GpuShardEngine(dd, params, r, 2) for r in range(2)]
+    seeds = seed_sequence(0, 31)
+    for e in engs:
+        e.init(int(seeds[0]))
+    chunk = engs[0].chunk
+
+    def allgather():
+        for buf, w in (("keys", k), ("flags", 1), ("maxd", 1)):
+            for r in range(2):
+                src = getattr(engs[r], buf)[r * chunk * w:(r + 1) * chunk * w]
+                for q in range(2):
+                    if q != r:
+                        getattr(engs[q], buf)[r * chunk * w:(r + 1) * chunk * w].copy_(src)
+        torch.cuda.synchronize()
+
+    allgather()
+    for it in range(1, 31):
+        steps = [e.step(int(seeds[it])) for e in engs]
+        changes = 0
+        for r in range(2):
+            c = steps[r]["send_counts"]
+            assert c[r] == 0  # nothing addressed to itself
+            recs = steps[r]["send"].view(-1, 3)
+            t = recs[:, 0].cpu().numpy()
+            other = 1 - r
+            assert np.all((t >= engs[other].lo) & (t < engs[other].hi))
+        for r in range(2):
+            other = 1 - r
+            changes += engs[r].merge(steps[other]["send"].clone())
+        allgather()
+        if changes < params.termination_delta * n * k:
+            break
+    ids = torch.cat([e.export()[0] for e in engs]).cpu().numpy().astype(np.uint32)
+    ex, _ = kg.brute_force_knng(data, k)
+    single = kg.run(data, params)
+    assert kg.recall(ids, ex) >= kg.recall(single.graph.ids, ex) - 0.005
+    for e in engs:
+        e.close()
