@@ -68,17 +68,21 @@ constexpr uint32_t kInvalid = 0xffu;
 // segments of a row are XOR-swizzled by the row's 8-block index so that the
 // four 8-lane groups of a warp, reading the same element of rows from
 // different 8-blocks, hit four different bank octets.
+constexpr uint32_t kMaxBatch = 8;  // nodes per CTA batch
+
 struct DistShared {
     float slab[kStages][kMaxColSlots * kSlab];
-    uint32_t colrow[kMaxColSlots];   // col slot -> data row id (0xffffffff: padding)
-    uint8_t rowmap[kMaxRowSlots];    // row slot -> new index
-    uint8_t colmap[kMaxColSlots];    // col slot -> combined index
-    uint16_t tiles[kMaxTiles];       // (rb << 8) | cb, in (rb, cb) order
-    uint32_t n_tiles;
-    uint32_t node;
-    uint32_t blkmask;                // column-slot 8-blocks read by the current pass
+    uint32_t colrow[kMaxColSlots];            // batch col slot -> data row id (~0: padding)
+    uint8_t colmap[kMaxColSlots];             // batch col slot -> combined index in its node
+    uint8_t rowmap[kMaxBatch][kMaxRowSlots];  // row slot -> new index, per node
+    uint16_t tiles[kMaxTiles];                // (node << 13) | (rb << 8) | cb
+    uint32_t n_tiles, nv, pending;
+    uint32_t blkmask;                         // column-slot 8-blocks read by the current pass
     uint32_t nblk;
     uint8_t blklist[kMaxColSlots / 8];
+    uint32_t warp_cnt[kThreads / 32];
+    uint32_t node[kMaxBatch], vnn[kMaxBatch], vno[kMaxBatch], colbase[kMaxBatch];
+    unsigned long long doff[kMaxBatch];
 };
 
 __device__ __forceinline__ void cp_async16(float* smem_dst, const float* gmem_src) {
@@ -199,6 +203,41 @@ __device__ __forceinline__ void group_reduce64(const float2 (&acc)[32], uint32_t
     }
 }
 
+// Per-node slot geometry (see the file comment): fullN/fullO, the padded
+// fused/unfused row and column extents, and the slot -> index maps.
+struct NodeGeom {
+    uint32_t nn, no, fn, fo, rf, rs, cf, cs;
+    __device__ __forceinline__ void set(uint32_t nn_, uint32_t no_) {
+        nn = nn_;
+        no = no_;
+        fn = nn - nn % 5;
+        fo = no - no % 5;
+        rf = (fn + 7) & ~7u;
+        rs = (nn - fn + 7) & ~7u;
+        cf = (fn + fo + 7) & ~7u;
+        cs = (nn - fn + no - fo + 7) & ~7u;
+    }
+    __device__ __forceinline__ uint32_t rbs() const { return (rf + rs) / 8; }
+    __device__ __forceinline__ uint32_t cbs() const { return (cf + cs) / 8; }
+    __device__ __forceinline__ uint32_t row(uint32_t sl) const {  // row slot -> new index
+        if (sl < fn) return sl;
+        if (sl >= rf && sl - rf < nn - fn) return fn + (sl - rf);
+        return kInvalid;
+    }
+    __device__ __forceinline__ uint32_t col(uint32_t sl) const {  // col slot -> combined index
+        if (sl < fn) return sl;
+        if (sl < fn + fo) return nn + (sl - fn);
+        if (sl >= cf && sl - cf < nn - fn) return fn + (sl - cf);
+        if (sl >= cf + (nn - fn) && sl - cf - (nn - fn) < no - fo)
+            return nn + fo + (sl - cf - (nn - fn));
+        return kInvalid;
+    }
+};
+
+// A CTA takes a BATCH of active nodes whose column slots fit the staging
+// buffer together (up to kMaxBatch nodes), so short lists (late iterations,
+// small k) share one tile sweep, one set of barriers and one staging pass
+// instead of paying them per node.
 __global__ void __launch_bounds__(kThreads) join_distances_kernel(
     GraphView g, CandView c, const uint32_t* __restrict__ active, IterCounters* ctr) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -208,77 +247,106 @@ __global__ void __launch_bounds__(kThreads) join_distances_kernel(
     if (ctr->overflow) return;
     const uint32_t n_active = ctr->active;
     const uint32_t n_slabs = (stride + kSlab - 1) / kSlab;
+    if (tid == 0) sh.pending = 0xffffffffu;
 
     while (true) {
         __syncthreads();
         if (tid == 0) {
-            const uint32_t a = atomicAdd(&ctr->work, 1u);
-            sh.node = a < n_active ? active[a] : 0xffffffffu;
+            uint32_t nv = 0, slots = 0, tiles = 0;
+            while (nv < kMaxBatch) {
+                uint32_t u = sh.pending;
+                if (u == 0xffffffffu) {
+                    const uint32_t a = atomicAdd(&ctr->work, 1u);
+                    if (a >= n_active) break;
+                    u = active[a];
+                }
+                NodeGeom ng;
+                ng.set(c.nc[u], c.oc[u]);
+                const uint32_t s = ng.cf + ng.cs, t = ng.rbs() * ng.cbs();
+                if (nv > 0 && (slots + s > kMaxColSlots || tiles + t > kMaxTiles - 8)) {
+                    sh.pending = u;
+                    break;
+                }
+                sh.pending = 0xffffffffu;
+                sh.node[nv] = u;
+                sh.vnn[nv] = ng.nn;
+                sh.vno[nv] = ng.no;
+                sh.colbase[nv] = slots;
+                sh.doff[nv] = c.doff[u];
+                slots += s;
+                tiles += t;
+                ++nv;
+            }
+            sh.nv = nv;
+            sh.n_tiles = 0;
         }
         __syncthreads();
-        const uint32_t u = sh.node;
-        if (u == 0xffffffffu) break;
-        const uint32_t nn = c.nc[u], no = c.oc[u], m = nn + no;
-        const uint32_t fn = nn - nn % 5, fo = no - no % 5;
-        const uint32_t rf = (fn + 7) & ~7u, rs = (nn - fn + 7) & ~7u;
-        const uint32_t cf = (fn + fo + 7) & ~7u, cs = (nn - fn + no - fo + 7) & ~7u;
-        const uint32_t rbs = (rf + rs) / 8, cbs = (cf + cs) / 8;
-        const uint32_t* list = c.ids + size_t(u) * 2 * cap;
-        for (uint32_t sl = tid; sl < rf + rs; sl += kThreads) {
-            uint32_t v = kInvalid;
-            if (sl < fn) v = sl;
-            else if (sl >= rf && sl - rf < nn - fn) v = fn + (sl - rf);
-            sh.rowmap[sl] = uint8_t(v);
+        const uint32_t nv = sh.nv;
+        if (nv == 0) break;
+        // slot maps of every node of the batch
+        for (uint32_t v = 0; v < nv; ++v) {
+            NodeGeom ng;
+            ng.set(sh.vnn[v], sh.vno[v]);
+            const uint32_t* list = c.ids + size_t(sh.node[v]) * 2 * cap;
+            for (uint32_t sl = tid; sl < ng.rf + ng.rs; sl += kThreads)
+                sh.rowmap[v][sl] = uint8_t(ng.row(sl));
+            for (uint32_t sl = tid; sl < ng.cf + ng.cs; sl += kThreads) {
+                const uint32_t x = ng.col(sl);
+                sh.colmap[sh.colbase[v] + sl] = uint8_t(x);
+                sh.colrow[sh.colbase[v] + sl] =
+                    x == kInvalid ? 0xffffffffu : (x < ng.nn ? list[x] : list[cap + x - ng.nn]);
+            }
         }
-        for (uint32_t sl = tid; sl < cf + cs; sl += kThreads) {
-            uint32_t v = kInvalid;
-            if (sl < fn) v = sl;
-            else if (sl < fn + fo) v = nn + (sl - fn);
-            else if (sl >= cf && sl - cf < nn - fn) v = fn + (sl - cf);
-            else if (sl >= cf + (nn - fn) && sl - cf - (nn - fn) < no - fo)
-                v = nn + fo + (sl - cf - (nn - fn));
-            sh.colmap[sl] = uint8_t(v);
-            sh.colrow[sl] = v == kInvalid ? 0xffffffffu : (v < nn ? list[v] : list[cap + v - nn]);
-        }
-        if (tid == 0) sh.n_tiles = 0;
         __syncthreads();
-        // live tiles (any valid pair): fused tiles, padding to a whole warp
-        // (4 groups), then unfused tiles, so every warp runs one path; each
-        // phase in (rb, cb) order so a warp's groups mostly share the A block
-        __shared__ uint32_t warp_cnt[kThreads / 32];
+        // live tiles (any valid pair) of all nodes: fused tiles, padding to a
+        // whole warp (4 groups), then unfused tiles, so every warp runs one
+        // path; in (node, rb, cb) order so a warp's groups mostly share A
+        uint32_t total = 0;
+        for (uint32_t v = 0; v < nv; ++v) {
+            NodeGeom ng;
+            ng.set(sh.vnn[v], sh.vno[v]);
+            total += ng.rbs() * ng.cbs();
+        }
         for (uint32_t phase = 0; phase < 2; ++phase) {
-            for (uint32_t t0 = 0; t0 < rbs * cbs; t0 += kThreads) {
-                const uint32_t t = t0 + tid;
+            for (uint32_t t0 = 0; t0 < total; t0 += kThreads) {
+                uint32_t t = t0 + tid, v = 0;
                 bool live = false;
-                if (t < rbs * cbs) {
-                    const uint32_t rb = t / cbs, cb = t % cbs;
-                    const bool fused_tile = rb * 8 < rf && cb * 8 < cf;
+                NodeGeom ng;
+                ng.set(sh.vnn[0], sh.vno[0]);
+                if (t < total) {
+                    while (t >= ng.rbs() * ng.cbs()) {
+                        t -= ng.rbs() * ng.cbs();
+                        ++v;
+                        ng.set(sh.vnn[v], sh.vno[v]);
+                    }
+                    const uint32_t rb = t / ng.cbs(), cb = t % ng.cbs();
+                    const bool fused_tile = rb * 8 < ng.rf && cb * 8 < ng.cf;
                     if (fused_tile == (phase == 0)) {
                         uint32_t imin = kInvalid;
                         for (uint32_t x = 0; x < 8; ++x)
-                            imin = min(imin, uint32_t(sh.rowmap[rb * 8 + x]));
+                            imin = min(imin, uint32_t(sh.rowmap[v][rb * 8 + x]));
                         if (imin != kInvalid)
                             for (uint32_t y = 0; y < 8; ++y) {
-                                const uint32_t col = sh.colmap[cb * 8 + y];
-                                live |= col != kInvalid && (col >= nn || col > imin);
+                                const uint32_t col = sh.colmap[sh.colbase[v] + cb * 8 + y];
+                                live |= col != kInvalid && (col >= ng.nn || col > imin);
                             }
                     }
                 }
                 // order-preserving compaction: warp ballots + per-warp offsets
                 const uint32_t mask = __ballot_sync(0xffffffffu, live);
-                if ((tid & 31u) == 0) warp_cnt[tid >> 5] = __popc(mask);
+                if ((tid & 31u) == 0) sh.warp_cnt[tid >> 5] = __popc(mask);
                 __syncthreads();
                 uint32_t base = sh.n_tiles;
-                for (uint32_t w = 0; w < (tid >> 5); ++w) base += warp_cnt[w];
+                for (uint32_t w = 0; w < (tid >> 5); ++w) base += sh.warp_cnt[w];
                 if (live) {
-                    const uint32_t rb = t / cbs, cb = t % cbs;
+                    const uint32_t rb = t / ng.cbs(), cb = t % ng.cbs();
                     sh.tiles[base + __popc(mask & ((1u << (tid & 31u)) - 1u))] =
-                        uint16_t((rb << 8) | cb);
+                        uint16_t((v << 13) | (rb << 8) | cb);
                 }
                 __syncthreads();
                 if (tid == 0) {
                     uint32_t tot = 0;
-                    for (uint32_t w = 0; w < kThreads / 32; ++w) tot += warp_cnt[w];
+                    for (uint32_t w = 0; w < kThreads / 32; ++w) tot += sh.warp_cnt[w];
                     sh.n_tiles += tot;
                 }
                 __syncthreads();
@@ -292,22 +360,25 @@ __global__ void __launch_bounds__(kThreads) join_distances_kernel(
             }
         }
         const uint32_t n_tiles = sh.n_tiles;
-        float* const D = c.D + c.doff[u];
 
         for (uint32_t t0 = 0; t0 < n_tiles; t0 += kGroups) {
             const uint32_t t = t0 + group;
             const uint32_t tile0 = t < n_tiles ? sh.tiles[t] : kDeadTile;
             const bool live = tile0 != kDeadTile;
             const uint32_t tile = live ? tile0 : 0u;
-            const uint32_t rb = tile >> 8, cb = tile & 0xffu;
-            const bool fused = rb * 8 < rf && cb * 8 < cf;
-            // row slot block -> column slot block holding the same new candidates
-            const uint32_t a_blk = rb * 8 < rf ? rb : cf / 8 + (rb - rf / 8);
-            // stage only the 8-blocks this pass reads (a partial last pass
-            // needs a fraction of the rows)
+            const uint32_t v = tile >> 13, rb = (tile >> 8) & 31u, cb = tile & 0xffu;
+            NodeGeom ng;
+            ng.set(sh.vnn[v], sh.vno[v]);
+            const bool fused = rb * 8 < ng.rf && cb * 8 < ng.cf;
+            // row slot block -> column slot block holding the same new
+            // candidates, then into the batch's column-slot space
+            const uint32_t cb0 = sh.colbase[v] / 8;
+            const uint32_t a_blk = cb0 + (rb * 8 < ng.rf ? rb : ng.cf / 8 + (rb - ng.rf / 8));
+            const uint32_t b_blk = cb0 + cb;
+            // stage only the 8-blocks this pass reads
             if (tid == 0) sh.blkmask = 0;
             __syncthreads();
-            if (live && l8 == 0) atomicOr(&sh.blkmask, (1u << a_blk) | (1u << cb));
+            if (live && l8 == 0) atomicOr(&sh.blkmask, (1u << a_blk) | (1u << b_blk));
             __syncthreads();
             if (tid == 0) {
                 uint32_t msk = sh.blkmask, nb = 0;
@@ -338,9 +409,9 @@ __global__ void __launch_bounds__(kThreads) join_distances_kernel(
                 const float* slab = sh.slab[s % kStages];
                 if (live) {
                     if (fused)
-                        tile_slab<true>(slab, a_blk, cb, l8, acc);
+                        tile_slab<true>(slab, a_blk, b_blk, l8, acc);
                     else
-                        tile_slab<false>(slab, a_blk, cb, l8, acc);
+                        tile_slab<false>(slab, a_blk, b_blk, l8, acc);
                 }
             }
             cp_async_wait_0();
@@ -348,11 +419,13 @@ __global__ void __launch_bounds__(kThreads) join_distances_kernel(
             float row[8];
             group_reduce64(acc, l8, row);
             const uint32_t x = 4u * (l8 & 1u) + 2u * ((l8 >> 1) & 1u) + ((l8 >> 2) & 1u);
-            const uint32_t i = live ? sh.rowmap[rb * 8 + x] : kInvalid;
+            const uint32_t i = live ? sh.rowmap[v][rb * 8 + x] : kInvalid;
             if (i != kInvalid) {
+                const uint32_t nn = ng.nn, m = ng.nn + ng.no;
+                float* const D = c.D + sh.doff[v];
 #pragma unroll
                 for (uint32_t y = 0; y < 8; ++y) {
-                    const uint32_t col = sh.colmap[cb * 8 + y];
+                    const uint32_t col = sh.colmap[sh.colbase[v] + cb * 8 + y];
                     if (col == kInvalid || !(col >= nn || col > i)) continue;
                     D[size_t(i) * m + col] = row[y];
                     if (col < nn)
@@ -364,6 +437,7 @@ __global__ void __launch_bounds__(kThreads) join_distances_kernel(
         }
     }
 }
+
 
 // Warp-wide bounded insert into a sorted row held one key per lane (lanes
 // >= k hold kEmptyKey).  try_insert semantics (graph.hpp:116-129).
