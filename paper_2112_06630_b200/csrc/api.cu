@@ -215,12 +215,15 @@ struct Engine {
     DevBuf<uint64_t> keys;
     DevBuf<uint32_t> flags, indeg, cand, raw_new, raw_old, nc, oc, active;
     DevBuf<uint64_t> dsz, doff;
+    DevBuf<float> cmax;
+    DevBuf<uint4> arec;
     DevBuf<uint32_t> revcnt, roff, rcur;
     DevBuf<unsigned char> scan_tmp;
     size_t scan_bytes = 0;
     // grow-only per-iteration buffers: reverse index and distance blocks
     DevBuf<uint64_t> rev;
-    DevBuf<float> dblocks;
+    DevBuf<uint64_t> dblocks;
+    int filter = 1;  // join proposals prefiltered by the row maxima (0: keep all)
     size_t rev_cap = 0, d_cap = 0;
     DevBuf<IterCounters> ctr;
     IterCounters* h_ctr = nullptr;
@@ -251,6 +254,8 @@ struct Engine {
             active.alloc(n, pool, s);
             dsz.alloc(n, pool, s);
             doff.alloc(n, pool, s);
+            cmax.alloc(size_t(n) * 2 * cap, pool, s);
+            arec.alloc(n, pool, s);
             revcnt.alloc(n, pool, s);
             roff.alloc(n, pool, s);
             rcur.alloc(n, pool, s);
@@ -274,20 +279,21 @@ struct Engine {
     }
     CandView cv() const {
         return CandView{cap,   cand.p,   raw_new.p, raw_old.p, nc.p, oc.p, dsz.p,
-                        doff.p, revcnt.p, roff.p,   rcur.p,    rev.p, dblocks.p};
+                        doff.p, revcnt.p, roff.p,   rcur.p,    rev.p, dblocks.p, filter,
+                        cmax.p, arec.p};
     }
 
-    void reserve_join(uint64_t rev_entries, uint64_t dfloats) {
+    void reserve_join(uint64_t rev_entries, uint64_t dwords) {
         if (rev_entries > rev_cap) {
             rev.~DevBuf();
             new (&rev) DevBuf<uint64_t>();
             rev_cap = rev_entries + rev_entries / 4 + 1024;
             rev.alloc(rev_cap, pool, s);
         }
-        if (dfloats > d_cap) {
+        if (dwords > d_cap) {
             dblocks.~DevBuf();
-            new (&dblocks) DevBuf<float>();
-            d_cap = dfloats + dfloats / 4 + 4096;
+            new (&dblocks) DevBuf<uint64_t>();
+            d_cap = dwords + dwords / 4 + 4096;
             dblocks.alloc(d_cap, pool, s);
         }
     }
@@ -336,7 +342,7 @@ struct Engine {
         join_stages(timer, distances_only);
         read_counters();
         if (h_ctr->overflow) {
-            reserve_join(h_ctr->rev, h_ctr->dfloats);
+            reserve_join(h_ctr->rev, h_ctr->dwords);
             CK(cudaMemsetAsync(&ctr.p->overflow, 0, sizeof(uint32_t), s));
             join_stages(timer, distances_only);
             read_counters();
@@ -730,12 +736,14 @@ int knng_cuda_candidate_distances(const float* data, uint32_t n, uint32_t d, uin
                            cudaMemcpyHostToDevice, e.s));
         CK(cudaMemcpyAsync(e.nc.p, new_counts, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, e.s));
         CK(cudaMemcpyAsync(e.oc.p, old_counts, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, e.s));
+        e.filter = 0;
         launch_bookkeeping(e.gv(), e.cv(), e.active.p, e.ctr.p, e.s);
         KernelTimer timer(false, e.s, nullptr);
         e.join(timer, /*distances_only=*/true);
-        // the first nn*m floats of each distance block are the nn x m matrix
-        const uint64_t dtotal = e.h_ctr->dfloats;
-        std::vector<float> blocks(dtotal);
+        // unfiltered proposal blocks: row i (new candidate i) holds every
+        // partner as (distance, id); place each by its partner's position
+        const uint64_t dtotal = e.h_ctr->dwords;
+        std::vector<uint64_t> blocks(dtotal);
         std::vector<uint64_t> doff(n);
         if (dtotal) to_host(blocks.data(), e.dblocks.p, dtotal, e);
         to_host(doff.data(), e.doff.p, n, e);
@@ -743,9 +751,19 @@ int knng_cuda_candidate_distances(const float* data, uint32_t n, uint32_t d, uin
         for (uint32_t u = 0; u < n; ++u) {
             const uint64_t nn = new_counts[u], m = nn + old_counts[u];
             if (!nn) continue;
-            for (uint64_t i = 0; i < nn; ++i)
-                for (uint64_t j = 0; j < m; ++j)
-                    if (j != i) out_dists[offsets[u] + i * m + j] = blocks[doff[u] + i * m + j];
+            const uint32_t* list = cand_ids + size_t(u) * 2 * cap;
+            for (uint64_t i = 0; i < nn; ++i) {
+                const uint64_t* row = blocks.data() + doff[u] + i * m;
+                for (uint64_t q = 0; q < row[0]; ++q) {
+                    const uint32_t id = uint32_t(row[1 + q]);
+                    const uint32_t bits = uint32_t(row[1 + q] >> 32);
+                    float dist;
+                    std::memcpy(&dist, &bits, 4);
+                    for (uint64_t j = 0; j < m; ++j)
+                        if (j != i && (j < nn ? list[j] : list[cap + j - nn]) == id)
+                            out_dists[offsets[u] + i * m + j] = dist;
+                }
+            }
         }
     });
 }

@@ -201,28 +201,33 @@ constexpr uint32_t kFinWarps = 8;
 constexpr uint32_t kTomb = 0xffffffffu;
 
 struct BlockCounters {
-    unsigned long long evals, cands, dfloats, rev;
+    unsigned long long evals, cands, dwords, rev;
 };
 
 // The join's per-node accounting (one full warp): evaluation count
-// C(nn,2) + nn*no (acceptance.cpp:369-374), the size of the node's distance
-// block nn*(m + no) (join.cu), its entry in the active list, and one
-// reverse-index count for every candidate its lists name.
-__device__ __forceinline__ void join_bookkeeping(const CandView& c, uint32_t u, uint32_t nn,
-                                                 uint32_t no, uint32_t* active,
-                                                 IterCounters* ctr, BlockCounters& acc) {
+// C(nn,2) + nn*no (acceptance.cpp:369-374), the size of the node's proposal
+// block nn*(m + no) + m words (join.cu: one counted row per candidate), its
+// entry in the active list, and one reverse-index count for every candidate
+// its lists name.
+__device__ __forceinline__ void join_bookkeeping(const GraphView& g, const CandView& c,
+                                                 uint32_t u, uint32_t nn, uint32_t no,
+                                                 uint32_t* active, IterCounters* ctr,
+                                                 BlockCounters& acc) {
     const uint32_t lane = lane_id(), m = nn + no;
-    if (lane == 0) c.dsz[u] = nn ? uint64_t(nn) * (m + no) : 0ull;
+    if (lane == 0) c.dsz[u] = nn ? uint64_t(nn) * (m + no) + no : 0ull;
     if (nn == 0) return;
     const uint32_t* list = c.ids + size_t(u) * 2 * c.cap;
     for (uint32_t p = lane; p < m; p += 32) {
-        const uint32_t x = p < nn ? list[p] : list[c.cap + p - nn];
+        const uint32_t slot = p < nn ? p : c.cap + p - nn;
+        const uint32_t x = list[slot];
         atomicAdd(c.revcnt + x, 1u);
+        // the join's prefilter bound, gathered here once per listed candidate
+        c.cmax[size_t(u) * 2 * c.cap + slot] = g.maxd[x];
     }
     if (lane == 0) {
         atomicAdd(&acc.evals, (unsigned long long)nn * (nn - 1) / 2 + (unsigned long long)nn * no);
         atomicAdd(&acc.cands, (unsigned long long)m);
-        atomicAdd(&acc.dfloats, (unsigned long long)nn * (m + no));
+        atomicAdd(&acc.dwords, (unsigned long long)nn * (m + no) + no);
         atomicAdd(&acc.rev, (unsigned long long)m);
         active[atomicAdd(&ctr->active, 1u)] = u;
     }
@@ -233,7 +238,7 @@ __device__ __forceinline__ void flush_block_counters(const BlockCounters& acc,
     if (threadIdx.x == 0) {
         if (acc.evals) atomicAdd(&ctr->evals, acc.evals);
         if (acc.cands) atomicAdd(&ctr->cands, acc.cands);
-        if (acc.dfloats) atomicAdd(&ctr->dfloats, acc.dfloats);
+        if (acc.dwords) atomicAdd(&ctr->dwords, acc.dwords);
         if (acc.rev) atomicAdd(&ctr->rev, acc.rev);
     }
 }
@@ -329,7 +334,7 @@ __global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(GraphView g, C
             c.oc[u] = no;
             g.flags[u] = hflags & ~clear;
         }
-        join_bookkeeping(c, u, nn, no, active, ctr, acc);
+        join_bookkeeping(g, c, u, nn, no, active, ctr, acc);
     }
     __syncthreads();
     flush_block_counters(acc, ctr);
@@ -344,7 +349,7 @@ __global__ void __launch_bounds__(kFinWarps * 32) bookkeeping_kernel(GraphView g
     if (threadIdx.x == 0) acc = BlockCounters{0, 0, 0, 0};
     __syncthreads();
     const uint32_t u = g.lo + blockIdx.x * kFinWarps + (threadIdx.x >> 5);
-    if (u < g.hi) join_bookkeeping(c, u, c.nc[u], c.oc[u], active, ctr, acc);
+    if (u < g.hi) join_bookkeeping(g, c, u, c.nc[u], c.oc[u], active, ctr, acc);
     __syncthreads();
     flush_block_counters(acc, ctr);
 }

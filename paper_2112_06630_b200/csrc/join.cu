@@ -4,13 +4,13 @@
 // 1. join_distances_kernel — the FP32 hot loop.  One CTA (128 threads = 16
 //    groups of 8) evaluates, for one active node u at a time, every
 //    new x new unordered pair and every new x old pair of u's candidate lists
-//    (the same C(nn,2) + nn*no evaluations as compute_step) and writes them
-//    to u's distance block in HBM.  Candidate rows stream through shared
+//    (the same C(nn,2) + nn*no evaluations as compute_step) and writes the
+//    proposals that can matter to u's proposal block in HBM.  Candidate rows stream through shared
 //    memory in 32-float slabs (cp.async, double-buffered); each group owns an
 //    8x8 pair tile, thread l8 of the group being reference lane l8.
 // 2. join_merge_kernel — the bounded list updates.  One warp per target t
 //    walks the reverse index (every (u, position) whose lists name t), reads
-//    t's row of each distance block, and inserts the partners that beat t's
+//    t's row of each proposal block, and inserts the partners that beat t's
 //    current maximum into t's sorted row with try_insert's semantics
 //    (graph.hpp:116-129: strict improvement, id dedup, evict the max).  A
 //    target is owned by exactly one warp, so there are no locks and no
@@ -30,10 +30,14 @@
 // with fullN = nn - nn%5, fullO = no - no%5.  Zero padding of the last slab is
 // exact (0 - 0 contributes +0 to either form).
 //
-// Distance block of u (nn new, no old, m = nn + no candidates), nn*(m + no)
-// floats at doff[u]: row r < nn (new r) holds m entries indexed by combined
-// position (new j, then old at nn + j'); row r >= nn (old r - nn) holds nn
-// entries indexed by new position.  Every pair is written to both rows.
+// Proposal block of u (nn new, no old, m = nn + no candidates),
+// nn*(m + no) + no u64 words at doff[u], one row per candidate (prow below):
+// row r < nn (new r) has m words, row r >= nn (old r - nn) has nn + 1.  Word 0
+// is the row's count, then that many keys (distance bits << 32 | partner id):
+// every evaluated pair is a proposal to both endpoints, kept only when it
+// beats the endpoint's iteration-start row maximum (c.filter; rows maxima only
+// fall during an iteration, so the filter never drops an accepted update).
+#include <cstdlib>
 #include <cub/device/device_scan.cuh>
 
 #include "kernels.cuh"
@@ -71,16 +75,23 @@ constexpr uint32_t kInvalid = 0xffu;
 constexpr uint32_t kMaxBatch = 8;  // nodes per CTA batch
 
 struct DistShared {
-    float slab[kStages][kMaxColSlots * kSlab];
+    // the slab ring (kStages x max_slots x kSlab floats, sized by the cap at
+    // launch) follows this struct in dynamic shared memory
     uint32_t colrow[kMaxColSlots];            // batch col slot -> data row id (~0: padding)
     uint8_t colmap[kMaxColSlots];             // batch col slot -> combined index in its node
     uint8_t rowmap[kMaxBatch][kMaxRowSlots];  // row slot -> new index, per node
     uint16_t tiles[kMaxTiles];                // (node << 13) | (rb << 8) | cb
-    uint32_t n_tiles, nv, pending;
+    uint32_t n_tiles, nv, nslots;
+    // claimed-but-unbatched nodes (claims come in chunks of kMaxBatch)
+    uint32_t qn;
+    uint4 q[2 * kMaxBatch];  // active-node records (scatter_rev_kernel)
+    uint32_t max_slots;                       // column slots one slab stage holds
     uint32_t blkmask;                         // column-slot 8-blocks read by the current pass
     uint32_t nblk;
     uint8_t blklist[kMaxColSlots / 8];
     uint32_t warp_cnt[kThreads / 32];
+    float colmax[kMaxColSlots];               // batch col slot -> candidate's row maximum
+    uint32_t rowcnt[kMaxColSlots];            // proposals kept per candidate row, at colbase + r
     uint32_t node[kMaxBatch], vnn[kMaxBatch], vno[kMaxBatch], colbase[kMaxBatch];
     unsigned long long doff[kMaxBatch];
 };
@@ -96,6 +107,20 @@ __device__ __forceinline__ void cp_async_wait_pending() {
 }
 __device__ __forceinline__ void cp_async_wait_0() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
+constexpr size_t kSlabOffset = (sizeof(DistShared) + 127) / 128 * 128;
+
+__device__ __forceinline__ float* slab_buf(DistShared& sh, uint32_t buf) {
+    return reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(&sh) + kSlabOffset) +
+           size_t(buf) * sh.max_slots * kSlab;
+}
+
+// Offset of candidate r's row in its node's proposal block (nn new, m = nn + no
+// candidates): word 0 = count, then up to m - 1 (new r) or nn (old r) keys
+// (distance bits << 32 | partner id).
+__device__ __forceinline__ size_t prow(uint32_t r, uint32_t nn, uint32_t m) {
+    return r < nn ? size_t(r) * m : size_t(nn) * m + size_t(r - nn) * (nn + 1);
+}
+
 __device__ __forceinline__ uint32_t swz(uint32_t slot, uint32_t seg) {
     return slot * kSlab + ((seg ^ ((slot >> 3) & 3u)) << 3);
 }
@@ -109,13 +134,35 @@ __device__ __forceinline__ void stage_slab(DistShared& sh, const float* __restri
                                            uint32_t buf) {
     constexpr uint32_t kC4 = kSlab / 4;  // 16-byte chunks per row per slab
     const uint32_t e0 = s * kSlab;
-    float* dst = sh.slab[buf];
+    float* dst = slab_buf(sh, buf);
     for (uint32_t i = threadIdx.x; i < nblk * 8u * kC4; i += kThreads) {
         const uint32_t slot = sh.blklist[i / (8u * kC4)] * 8u + ((i / kC4) & 7u), j = i % kC4;
         const uint32_t row = sh.colrow[slot];
         if (row == 0xffffffffu) continue;
         float* p = dst + swz(slot, j >> 1) + (j & 1u) * 4;
         const uint32_t e = e0 + 4 * j;
+        if (e < stride)
+            cp_async16(p, data + size_t(row) * stride + e);
+        else
+            *reinterpret_cast<float4*>(p) = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+}
+
+// Resident mode (the whole padded row fits the slab ring, n_slabs <= kStages):
+// every column slot of the batch, all slabs, staged once per batch; slab s
+// goes to buffer s.  Consecutive threads take consecutive 16-byte chunks of a
+// row, so each row is one coalesced read.
+__device__ __forceinline__ void stage_batch(DistShared& sh, const float* __restrict__ data,
+                                            uint32_t stride, uint32_t nslots, uint32_t n_slabs) {
+    constexpr uint32_t kC4 = kSlab / 4;
+    const uint32_t per_slot = n_slabs * kC4;
+    for (uint32_t i = threadIdx.x; i < nslots * per_slot; i += kThreads) {
+        const uint32_t slot = i / per_slot, r = i - slot * per_slot;
+        const uint32_t s = r / kC4, j = r % kC4;
+        const uint32_t row = sh.colrow[slot];
+        if (row == 0xffffffffu) continue;
+        float* p = slab_buf(sh, s) + swz(slot, j >> 1) + (j & 1u) * 4;
+        const uint32_t e = s * kSlab + 4 * j;
         if (e < stride)
             cp_async16(p, data + size_t(row) * stride + e);
         else
@@ -239,46 +286,81 @@ struct NodeGeom {
 // small k) share one tile sweep, one set of barriers and one staging pass
 // instead of paying them per node.
 __global__ void __launch_bounds__(kThreads) join_distances_kernel(
-    GraphView g, CandView c, const uint32_t* __restrict__ active, IterCounters* ctr) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    GraphView g, CandView c, const uint32_t* __restrict__ active, IterCounters* ctr,
+    uint32_t max_slots) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     DistShared& sh = *reinterpret_cast<DistShared*>(smem_raw);
     const uint32_t tid = threadIdx.x, group = tid >> 3, l8 = tid & 7u;
     const uint32_t stride = g.stride, cap = c.cap;
     if (ctr->overflow) return;
     const uint32_t n_active = ctr->active;
     const uint32_t n_slabs = (stride + kSlab - 1) / kSlab;
-    if (tid == 0) sh.pending = 0xffffffffu;
+    const bool resident = n_slabs <= kStages;
+    if (tid == 0) {
+        sh.qn = 0;
+        sh.max_slots = max_slots;
+    }
+    // warp 0 claims chunks of kMaxBatch active indices one batch ahead, so
+    // the claim's atomic round trip overlaps the current batch
+    uint32_t a_next = 0;
+    if (tid == 0) a_next = atomicAdd(&ctr->work, kMaxBatch);
 
     while (true) {
         __syncthreads();
-        if (tid == 0) {
-            uint32_t nv = 0, slots = 0, tiles = 0;
-            while (nv < kMaxBatch) {
-                uint32_t u = sh.pending;
-                if (u == 0xffffffffu) {
-                    const uint32_t a = atomicAdd(&ctr->work, 1u);
-                    if (a >= n_active) break;
-                    u = active[a];
-                }
-                NodeGeom ng;
-                ng.set(c.nc[u], c.oc[u]);
-                const uint32_t s = ng.cf + ng.cs, t = ng.rbs() * ng.cbs();
-                if (nv > 0 && (slots + s > kMaxColSlots || tiles + t > kMaxTiles - 8)) {
-                    sh.pending = u;
-                    break;
-                }
-                sh.pending = 0xffffffffu;
-                sh.node[nv] = u;
-                sh.vnn[nv] = ng.nn;
-                sh.vno[nv] = ng.no;
-                sh.colbase[nv] = slots;
-                sh.doff[nv] = c.doff[u];
-                slots += s;
-                tiles += t;
-                ++nv;
+        if (tid < 32) {
+            // warp 0 forms the batch: top the queue up with the claimed chunk
+            // (one 16-byte record per node), claim the next, then take the
+            // longest queue prefix whose column slots and tiles fit
+            const uint32_t lane = tid;
+            uint32_t qn = sh.qn;
+            const uint32_t a = __shfl_sync(0xffffffffu, a_next, 0);
+            if (qn < kMaxBatch && a < n_active) {
+                if (lane < kMaxBatch && a + lane < n_active) sh.q[qn + lane] = c.arec[a + lane];
+                qn += min(kMaxBatch, n_active - a);
+                if (lane == 0) a_next = atomicAdd(&ctr->work, kMaxBatch);
+                __syncwarp();
             }
-            sh.nv = nv;
-            sh.n_tiles = 0;
+            uint32_t s_l = 0, t_l = 0, u = 0, nn = 0, no = 0;
+            uint4 rec = make_uint4(0, 0, 0, 0);
+            if (lane < qn) {
+                rec = sh.q[lane];
+                u = rec.x;
+                nn = rec.y & 0xffffu;
+                no = rec.y >> 16;
+                NodeGeom ng;
+                ng.set(nn, no);
+                s_l = ng.cf + ng.cs;
+                t_l = ng.rbs() * ng.cbs();
+            }
+            uint32_t si = s_l, ti = t_l;
+#pragma unroll
+            for (uint32_t o = 1; o < 32; o <<= 1) {
+                const uint32_t sp = __shfl_up_sync(0xffffffffu, si, o);
+                const uint32_t tp = __shfl_up_sync(0xffffffffu, ti, o);
+                if (lane >= o) {
+                    si += sp;
+                    ti += tp;
+                }
+            }
+            const bool fit = lane < qn && lane < kMaxBatch &&
+                             (lane == 0 || (si <= sh.max_slots && ti <= kMaxTiles - 8));
+            const uint32_t nv = __popc(__ballot_sync(0xffffffffu, fit));  // a prefix
+            __syncwarp();
+            if (lane < nv) {
+                sh.node[lane] = u;
+                sh.vnn[lane] = nn;
+                sh.vno[lane] = no;
+                sh.colbase[lane] = si - s_l;
+                sh.doff[lane] = uint64_t(rec.z) | (uint64_t(rec.w) << 32);
+            } else if (lane < qn) {
+                sh.q[lane - nv] = rec;
+            }
+            if (lane == nv - 1) sh.nslots = si;
+            if (lane == 0) {
+                sh.qn = qn - nv;
+                sh.nv = nv;
+                sh.n_tiles = 0;
+            }
         }
         __syncthreads();
         const uint32_t nv = sh.nv;
@@ -288,16 +370,28 @@ __global__ void __launch_bounds__(kThreads) join_distances_kernel(
             NodeGeom ng;
             ng.set(sh.vnn[v], sh.vno[v]);
             const uint32_t* list = c.ids + size_t(sh.node[v]) * 2 * cap;
+            const float* cmax = c.cmax + size_t(sh.node[v]) * 2 * cap;
             for (uint32_t sl = tid; sl < ng.rf + ng.rs; sl += kThreads)
                 sh.rowmap[v][sl] = uint8_t(ng.row(sl));
             for (uint32_t sl = tid; sl < ng.cf + ng.cs; sl += kThreads) {
                 const uint32_t x = ng.col(sl);
                 sh.colmap[sh.colbase[v] + sl] = uint8_t(x);
-                sh.colrow[sh.colbase[v] + sl] =
+                const uint32_t id =
                     x == kInvalid ? 0xffffffffu : (x < ng.nn ? list[x] : list[cap + x - ng.nn]);
+                sh.colrow[sh.colbase[v] + sl] = id;
+                sh.colmax[sh.colbase[v] + sl] =
+                    x == kInvalid ? 0.0f
+                    : c.filter    ? cmax[x < ng.nn ? x : cap + x - ng.nn]
+                                  : __int_as_float(0x7f800000);
             }
+            for (uint32_t r = tid; r < ng.nn + ng.no; r += kThreads) sh.rowcnt[sh.colbase[v] + r] = 0;
         }
         __syncthreads();
+        // resident mode: the batch's rows load while the tile list is built
+        if (resident) {
+            stage_batch(sh, g.data, stride, sh.nslots, n_slabs);
+            cp_async_commit();
+        }
         // live tiles (any valid pair) of all nodes: fused tiles, padding to a
         // whole warp (4 groups), then unfused tiles, so every warp runs one
         // path; in (node, rb, cb) order so a warp's groups mostly share A
@@ -360,6 +454,10 @@ __global__ void __launch_bounds__(kThreads) join_distances_kernel(
             }
         }
         const uint32_t n_tiles = sh.n_tiles;
+        if (resident) {
+            cp_async_wait_0();
+            __syncthreads();
+        }
 
         for (uint32_t t0 = 0; t0 < n_tiles; t0 += kGroups) {
             const uint32_t t = t0 + group;
@@ -375,65 +473,93 @@ __global__ void __launch_bounds__(kThreads) join_distances_kernel(
             const uint32_t cb0 = sh.colbase[v] / 8;
             const uint32_t a_blk = cb0 + (rb * 8 < ng.rf ? rb : ng.cf / 8 + (rb - ng.rf / 8));
             const uint32_t b_blk = cb0 + cb;
-            // stage only the 8-blocks this pass reads
-            if (tid == 0) sh.blkmask = 0;
-            __syncthreads();
-            if (live && l8 == 0) atomicOr(&sh.blkmask, (1u << a_blk) | (1u << b_blk));
-            __syncthreads();
-            if (tid == 0) {
-                uint32_t msk = sh.blkmask, nb = 0;
-                while (msk) {
-                    sh.blklist[nb++] = uint8_t(__ffs(msk) - 1);
-                    msk &= msk - 1u;
-                }
-                sh.nblk = nb;
-            }
-            __syncthreads();
-            const uint32_t nblk = sh.nblk;
             float2 acc[32];
 #pragma unroll
             for (uint32_t p = 0; p < 32; ++p) acc[p] = make_float2(0.0f, 0.0f);
-
-            // 3-stage cp.async pipeline, one barrier per slab
-            for (uint32_t p = 0; p < kStages - 1; ++p) {
-                if (p < n_slabs) stage_slab(sh, g.data, stride, nblk, p, p);
-                cp_async_commit();
-            }
-            for (uint32_t s = 0; s < n_slabs; ++s) {
-                cp_async_wait_pending<kStages - 2>();  // slab s has landed
+            if (resident) {
+                if (live)
+                    for (uint32_t s = 0; s < n_slabs; ++s) {
+                        if (fused)
+                            tile_slab<true>(slab_buf(sh, s), a_blk, b_blk, l8, acc);
+                        else
+                            tile_slab<false>(slab_buf(sh, s), a_blk, b_blk, l8, acc);
+                    }
+            } else {
+                // stage only the 8-blocks this pass reads
+                if (tid == 0) sh.blkmask = 0;
                 __syncthreads();
-                if (s + kStages - 1 < n_slabs)
-                    stage_slab(sh, g.data, stride, nblk, s + kStages - 1,
-                               (s + kStages - 1) % kStages);
-                cp_async_commit();
-                const float* slab = sh.slab[s % kStages];
-                if (live) {
-                    if (fused)
-                        tile_slab<true>(slab, a_blk, b_blk, l8, acc);
-                    else
-                        tile_slab<false>(slab, a_blk, b_blk, l8, acc);
+                if (live && l8 == 0) atomicOr(&sh.blkmask, (1u << a_blk) | (1u << b_blk));
+                __syncthreads();
+                if (tid == 0) {
+                    uint32_t msk = sh.blkmask, nb = 0;
+                    while (msk) {
+                        sh.blklist[nb++] = uint8_t(__ffs(msk) - 1);
+                        msk &= msk - 1u;
+                    }
+                    sh.nblk = nb;
                 }
+                __syncthreads();
+                const uint32_t nblk = sh.nblk;
+                // 3-stage cp.async pipeline, one barrier per slab
+                for (uint32_t p = 0; p < kStages - 1; ++p) {
+                    if (p < n_slabs) stage_slab(sh, g.data, stride, nblk, p, p);
+                    cp_async_commit();
+                }
+                for (uint32_t s = 0; s < n_slabs; ++s) {
+                    cp_async_wait_pending<kStages - 2>();  // slab s has landed
+                    __syncthreads();
+                    if (s + kStages - 1 < n_slabs)
+                        stage_slab(sh, g.data, stride, nblk, s + kStages - 1,
+                                   (s + kStages - 1) % kStages);
+                    cp_async_commit();
+                    const float* slab = slab_buf(sh, s % kStages);
+                    if (live) {
+                        if (fused)
+                            tile_slab<true>(slab, a_blk, b_blk, l8, acc);
+                        else
+                            tile_slab<false>(slab, a_blk, b_blk, l8, acc);
+                    }
+                }
+                cp_async_wait_0();
+                __syncthreads();
             }
-            cp_async_wait_0();
-            __syncthreads();
             float row[8];
             group_reduce64(acc, l8, row);
             const uint32_t x = 4u * (l8 & 1u) + 2u * ((l8 >> 1) & 1u) + ((l8 >> 2) & 1u);
             const uint32_t i = live ? sh.rowmap[v][rb * 8 + x] : kInvalid;
             if (i != kInvalid) {
+                // each pair is a proposal to both endpoints; kept (compacted
+                // into the endpoint's row) only if it beats that candidate's
+                // iteration-start row maximum — the stale-upwards prefilter of
+                // compute_step (descent.hpp:97-102,134-147)
                 const uint32_t nn = ng.nn, m = ng.nn + ng.no;
-                float* const D = c.D + sh.doff[v];
+                uint64_t* const D = c.D + sh.doff[v];
+                const uint32_t slot_i = sh.colbase[v] + (i < ng.fn ? i : ng.cf + (i - ng.fn));
+                const uint32_t id_i = sh.colrow[slot_i];
+                const float mx_i = sh.colmax[slot_i];
 #pragma unroll
                 for (uint32_t y = 0; y < 8; ++y) {
-                    const uint32_t col = sh.colmap[sh.colbase[v] + cb * 8 + y];
+                    const uint32_t slot_c = sh.colbase[v] + cb * 8 + y;
+                    const uint32_t col = sh.colmap[slot_c];
                     if (col == kInvalid || !(col >= nn || col > i)) continue;
-                    D[size_t(i) * m + col] = row[y];
-                    if (col < nn)
-                        D[size_t(col) * m + i] = row[y];
-                    else
-                        D[size_t(nn) * m + size_t(col - nn) * nn + i] = row[y];
+                    const float dist = row[y];
+                    if (dist < mx_i) {
+                        const uint32_t pos = atomicAdd(&sh.rowcnt[sh.colbase[v] + i], 1u);
+                        D[prow(i, nn, m) + 1 + pos] = pack_key(dist, sh.colrow[slot_c]);
+                    }
+                    if (dist < sh.colmax[slot_c]) {
+                        const uint32_t pos = atomicAdd(&sh.rowcnt[sh.colbase[v] + col], 1u);
+                        D[prow(col, nn, m) + 1 + pos] = pack_key(dist, id_i);
+                    }
                 }
             }
+        }
+        // row counts of the batch's proposal blocks
+        __syncthreads();
+        for (uint32_t v = 0; v < nv; ++v) {
+            const uint32_t nn = sh.vnn[v], m = nn + sh.vno[v];
+            for (uint32_t r = tid; r < m; r += kThreads)
+                c.D[sh.doff[v] + prow(r, nn, m)] = sh.rowcnt[sh.colbase[v] + r];
         }
     }
 }
@@ -467,7 +593,7 @@ __global__ void __launch_bounds__(kMergeWarps * 32) join_merge_kernel(GraphView 
     __syncthreads();
     const uint32_t lane = lane_id();
     const uint32_t t = g.lo + blockIdx.x * kMergeWarps + (threadIdx.x >> 5);
-    const uint32_t k = g.k, cap = c.cap;
+    const uint32_t k = g.k;
     const uint32_t cnt = t < g.hi ? c.revcnt[t] : 0u;
     if (cnt) {
         uint64_t key = lane < k ? g.keys[size_t(t) * k + lane] : kEmptyKey;
@@ -476,23 +602,20 @@ __global__ void __launch_bounds__(kMergeWarps * 32) join_merge_kernel(GraphView 
         uint32_t inserted = 0;
         const uint64_t* rv = c.rev + c.roff[t];
         for (uint32_t e0 = 0; e0 < cnt; e0 += 32) {
-            // metadata of 32 entries at once, one per lane
-            uint32_t mu = 0, mp = 0, mnn = 0, mm = 0;
-            uint64_t moff = 0;
+            // metadata of 32 entries at once, one per lane: where t's row of
+            // the node's proposal block starts and how many proposals it kept
+            uint64_t mrow = 0;
+            uint32_t pe = 0;
             if (e0 + lane < cnt) {
                 const uint64_t r = rv[e0 + lane];
-                mu = uint32_t(r >> 8);
-                mp = uint32_t(r & 0xffu);
-                mnn = c.nc[mu];
-                mm = mnn + c.oc[mu];
-                moff = c.doff[mu];
+                const uint32_t u = uint32_t(r >> 8), p = uint32_t(r & 0xffu);
+                const uint32_t nn = c.nc[u], m = nn + c.oc[u];
+                mrow = c.doff[u] + prow(p, nn, m);
+                pe = uint32_t(c.D[mrow]);
             }
-            // The batch's partners, flattened: entry e contributes P_e
-            // partners (new target: the other m - 1 candidates; old target:
-            // the nn new ones), so every lane of every step has work even
-            // when lists are short.  Each step's loads are issued one step
-            // ahead so the D-row / id fetch overlaps the inserts.
-            const uint32_t pe = e0 + lane < cnt ? (mp < mnn ? mm - 1 : mnn) : 0u;
+            // The batch's proposals, flattened across entries so every lane of
+            // every step has work even when rows are short.  Each step's loads
+            // are issued one step ahead so the fetch overlaps the inserts.
             uint32_t incl = pe;
 #pragma unroll
             for (uint32_t o = 1; o < 32; o <<= 1) {
@@ -515,21 +638,13 @@ __global__ void __launch_bounds__(kMergeWarps * 32) join_merge_kernel(GraphView 
                     const uint32_t probe = __shfl_sync(0xffffffffu, excl, (e + step) & 31u);
                     if (e + step < 32 && probe <= f) e += step;
                 }
-                const uint32_t u = __shfl_sync(0xffffffffu, mu, e);
-                const uint32_t p = __shfl_sync(0xffffffffu, mp, e);
-                const uint32_t nn = __shfl_sync(0xffffffffu, mnn, e);
-                const uint32_t m = __shfl_sync(0xffffffffu, mm, e);
-                const uint64_t off = __shfl_sync(0xffffffffu, moff, e);
+                const uint64_t row = __shfl_sync(0xffffffffu, mrow, e);
                 const uint32_t q = f - __shfl_sync(0xffffffffu, excl, e);
                 Step st{0.0f, 0u, f < total};
                 if (st.valid) {
-                    const bool is_new = p < nn;
-                    const uint32_t qq = is_new && q >= p ? q + 1 : q;  // skip self
-                    const float* row = c.D + off + (is_new ? size_t(p) * m
-                                                           : size_t(nn) * m + size_t(p - nn) * nn);
-                    const uint32_t* list = c.ids + size_t(u) * 2 * cap;
-                    st.dist = row[qq];
-                    st.cand = qq < nn ? list[qq] : list[cap + qq - nn];
+                    const uint64_t kk = c.D[row + 1 + q];
+                    st.dist = key_dist(kk);
+                    st.cand = key_id(kk);
                 }
                 return st;
             };
@@ -571,6 +686,10 @@ __global__ void scatter_rev_kernel(CandView c, const uint32_t* __restrict__ acti
     if (a >= ctr->active || ctr->overflow) return;
     const uint32_t u = active[a], lane = lane_id();
     const uint32_t nn = c.nc[u], no = c.oc[u], m = nn + no;
+    if (lane == 0) {  // the distance kernel's per-node record
+        const uint64_t off = c.doff[u];
+        c.arec[a] = make_uint4(u, nn | (no << 16), uint32_t(off), uint32_t(off >> 32));
+    }
     const uint32_t* list = c.ids + size_t(u) * 2 * c.cap;
     for (uint32_t p = lane; p < m; p += 32) {
         const uint32_t x = p < nn ? list[p] : list[c.cap + p - nn];
@@ -580,7 +699,7 @@ __global__ void scatter_rev_kernel(CandView c, const uint32_t* __restrict__ acti
 }
 
 __global__ void check_capacity_kernel(IterCounters* ctr, unsigned long long capacity) {
-    ctr->overflow = ctr->dfloats > capacity ? 1u : 0u;
+    ctr->overflow = ctr->dwords > capacity ? 1u : 0u;
 }
 
 uint32_t g_sm_count = 0;
@@ -627,19 +746,28 @@ void launch_scatter_rev(const CandView& c, const uint32_t* active, IterCounters*
 void launch_join_distances(const GraphView& g, const CandView& c, const uint32_t* active,
                            IterCounters* ctr, uint32_t max_active, cudaStream_t s) {
     if (!max_active) return;
-    const size_t smem = sizeof(DistShared);
-    static int per_sm = 0;  // occupancy is a property of the kernel: query once
-    if (!per_sm) {
+    // a node needs at most 2 cap column slots plus two 8-paddings
+    uint32_t max_slots = std::min<uint32_t>(kMaxColSlots, (2 * c.cap + 16 + 7) / 8 * 8);
+    static const int env_slots = [] {
+        const char* v = getenv("KNNG_JOIN_SLOTS");
+        return v ? atoi(v) : 0;
+    }();
+    if (env_slots > 0)
+        max_slots = std::max<uint32_t>(max_slots, std::min<uint32_t>(kMaxColSlots, (env_slots + 7) / 8 * 8));
+    const size_t smem = kSlabOffset + size_t(kStages) * max_slots * kSlab * sizeof(float);
+    static int per_sm[kMaxColSlots + 1] = {};  // occupancy per slab size: query once
+    if (!per_sm[max_slots]) {
         cudaFuncSetAttribute(join_distances_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(smem));
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, join_distances_kernel,
-                                                      int(kThreads), smem);
-        if (per_sm < 1) per_sm = 1;
+                             int(kSlabOffset + size_t(kStages) * kMaxColSlots * kSlab * 4));
+        int v = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, join_distances_kernel, int(kThreads),
+                                                      smem);
+        per_sm[max_slots] = v < 1 ? 1 : v;
     }
-    uint32_t grid = sm_count() * uint32_t(per_sm);
+    uint32_t grid = sm_count() * uint32_t(per_sm[max_slots]);
     if (grid > max_active) grid = max_active;
     cudaMemsetAsync(&ctr->work, 0, sizeof(uint32_t), s);
-    join_distances_kernel<<<grid, kThreads, smem, s>>>(g, c, active, ctr);
+    join_distances_kernel<<<grid, kThreads, smem, s>>>(g, c, active, ctr, max_slots);
 }
 
 void launch_join_merge(const GraphView& g, const CandView& c, IterCounters* ctr,
@@ -681,23 +809,18 @@ __global__ void __launch_bounds__(kMergeWarps * 32) export_remote_kernel(
         const uint64_t r = rv[e];
         const uint32_t u = uint32_t(r >> 8), p = uint32_t(r & 0xffu);
         const uint32_t nn = c.nc[u], m = nn + c.oc[u];
-        const bool is_new = p < nn;
-        const uint32_t P = is_new ? m : nn;
-        const float* row = c.D + c.doff[u] + (is_new ? size_t(p) * m
-                                                     : size_t(nn) * m + size_t(p - nn) * nn);
-        const uint32_t* list = c.ids + size_t(u) * 2 * c.cap;
+        const uint64_t* row = c.D + c.doff[u] + prow(p, nn, m);
+        const uint32_t P = uint32_t(row[0]);  // proposals kept for t in this join
         for (uint32_t q0 = 0; q0 < P; q0 += 32) {
             const uint32_t q = q0 + lane;
-            const bool valid = q < P && q != p;
-            const float dist = valid ? row[q] : 0.0f;
-            const bool pass = valid && dist < mx;
+            const uint64_t kk = q < P ? row[1 + q] : kEmptyKey;
+            const bool pass = q < P && key_dist(kk) < mx;
             const uint32_t mask = __ballot_sync(0xffffffffu, pass);
             if (kWrite && pass) {
-                const uint32_t cand = q < nn ? list[q] : list[c.cap + q - nn];
                 uint32_t* rec = records + 3 * (base + written + __popc(mask & ((1u << lane) - 1u)));
                 rec[0] = t;
-                rec[1] = cand;
-                rec[2] = __float_as_uint(dist);
+                rec[1] = key_id(kk);
+                rec[2] = uint32_t(kk >> 32);
             }
             written += __popc(mask);
         }

@@ -35,13 +35,17 @@ struct CandView {
     uint32_t* raw_old;   // n
     uint32_t* nc;        // n, final new counts
     uint32_t* oc;        // n, final old counts
-    uint64_t* dsz;       // n, floats in u's distance block (0 when nn == 0)
+    uint64_t* dsz;       // n, words in u's proposal block (0 when nn == 0)
     uint64_t* doff;      // n, exclusive prefix sum of dsz
     uint32_t* revcnt;    // n, how many active lists name t
     uint32_t* roff;      // n, exclusive prefix sum of revcnt
     uint32_t* rcur;      // n, scatter cursors
     uint64_t* rev;       // total entries: (u << 8) | position of t in u's list
-    float* D;            // distance blocks, see join.cu
+    uint64_t* D;         // proposal blocks, see join.cu
+    int filter;          // 1: keep only proposals below the target's row maximum
+    float* cmax;         // n x 2cap, the row maximum of each listed candidate
+                         // (iteration start), beside ids
+    uint4* arec;         // per active index: {u, nn | no << 16, doff lo, doff hi}
 };
 
 // Device counters for one iteration.
@@ -49,7 +53,7 @@ struct IterCounters {
     unsigned long long changes;
     unsigned long long evals;
     unsigned long long cands;    // sum of (nn + no) over active nodes
-    unsigned long long dfloats;  // total distance-block floats
+    unsigned long long dwords;   // total distance-block words (u64)
     unsigned long long rev;      // total reverse-index entries
     uint32_t active;             // number of nodes with nn > 0
     uint32_t work;               // dynamic work counter
