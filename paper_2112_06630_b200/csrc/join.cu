@@ -61,37 +61,57 @@ constexpr uint32_t kSlab = KNNG_JOIN_SLAB;      // floats per row per smem stage
 constexpr uint32_t kStages = KNNG_JOIN_STAGES;  // cp.async pipeline depth
 constexpr uint32_t kMaxM = 2 * kMaxCap;  // candidates per node
 constexpr uint32_t kMaxRowSlots = kMaxCap + 16;
-constexpr uint32_t kMaxColSlots = kMaxM + 16;
-constexpr uint32_t kMaxTiles = (kMaxRowSlots / 8) * (kMaxColSlots / 8) + 4;
+constexpr uint32_t kMaxColSlots = kMaxM + 16;  // column slots of one node
 constexpr uint16_t kDeadTile = 0xffffu;
 constexpr uint32_t kInvalid = 0xffu;
 
 // Candidate rows are staged in COLUMN-slot order (every candidate has a column
 // slot; a new candidate's row slot maps to a column slot of the same 8-block
-// offset, see a_block below), 32 floats per row per stage.  The four 8-float
+// offset, see a_blk below), 32 floats per row per stage.  The four 8-float
 // segments of a row are XOR-swizzled by the row's 8-block index so that the
 // four 8-lane groups of a warp, reading the same element of rows from
 // different 8-blocks, hit four different bank octets.
-constexpr uint32_t kMaxBatch = 8;  // nodes per CTA batch
+//
+// A CTA works on a BATCH of active nodes (up to kMaxBatch) whose column
+// slots share one slot table.  Two staging modes, chosen per launch:
+//  - pass mode (long rows): each pass of up to 16 tiles (one per 8-lane
+//    group) stages only the 8-blocks its tiles read — at most kPassBlk, packed
+//    into ring positions — slab by slab through a kStages-deep cp.async ring.
+//    The ring is sized by kPassBlk, not by the batch, so a batch can hold
+//    many nodes and passes stay full across node boundaries.
+//  - resident mode (short rows, all slabs fit): the batch's rows are staged
+//    once, slab s of slot r at ring row s * res_slots + r, and every pass
+//    reads them without further staging.
+constexpr uint32_t kMaxBatch = 8;              // nodes per CTA batch
+constexpr uint32_t kSlotTab = 320;             // batch column slots (pass mode budget)
+constexpr uint32_t kBlkTab = kSlotTab / 8;     // batch 8-blocks
+constexpr uint32_t kPassBlk = 15;              // 8-blocks one pass may stage
+constexpr uint32_t kRingRows = kPassBlk * 8;   // rows per ring stage
+// an 8-block of rows in a ring stage: 8 rows of kSlab floats plus 8 floats of
+// padding, so the four groups of a warp reading the same element of rows
+// from four consecutive blocks hit four different bank octets
+constexpr uint32_t kBlkPitch = 8 * kSlab + 8;
+constexpr uint32_t kMaxTiles = 512;            // tiles of one batch
+static_assert(kMaxColSlots <= kSlotTab, "one node must fit the slot table");
+static_assert(kBlkTab <= 64, "pass block masks are 64-bit");
 
 struct DistShared {
-    // the slab ring (kStages x max_slots x kSlab floats, sized by the cap at
-    // launch) follows this struct in dynamic shared memory
-    uint32_t colrow[kMaxColSlots];            // batch col slot -> data row id (~0: padding)
-    uint8_t colmap[kMaxColSlots];             // batch col slot -> combined index in its node
+    // the slab ring (kStages x kPassBlk x kBlkPitch floats) follows this
+    // struct in dynamic shared memory
+    uint32_t colrow[kSlotTab];                // batch col slot -> data row id (~0: padding)
+    float colmax[kSlotTab];                   // batch col slot -> candidate's row maximum
+    uint32_t rowcnt[kSlotTab];                // proposals kept per candidate row, at colbase + r
+    uint8_t colmap[kSlotTab];                 // batch col slot -> combined index in its node
     uint8_t rowmap[kMaxBatch][kMaxRowSlots];  // row slot -> new index, per node
     uint16_t tiles[kMaxTiles];                // (node << 13) | (rb << 8) | cb
-    uint32_t n_tiles, nv, nslots;
+    uint8_t blkpos[kBlkTab];                  // pass mode: batch 8-block -> ring position
+    uint8_t blklist[kPassBlk];                // pass mode: ring position -> batch 8-block
+    uint32_t ringrow[kRingRows];              // pass mode: ring row -> data row (~0: none)
+    uint32_t n_tiles, nv, nslots, pass_len, nblk, slot_budget;
     // claimed-but-unbatched nodes (claims come in chunks of kMaxBatch)
     uint32_t qn;
     uint4 q[2 * kMaxBatch];  // active-node records (scatter_rev_kernel)
-    uint32_t max_slots;                       // column slots one slab stage holds
-    uint32_t blkmask;                         // column-slot 8-blocks read by the current pass
-    uint32_t nblk;
-    uint8_t blklist[kMaxColSlots / 8];
     uint32_t warp_cnt[kThreads / 32];
-    float colmax[kMaxColSlots];               // batch col slot -> candidate's row maximum
-    uint32_t rowcnt[kMaxColSlots];            // proposals kept per candidate row, at colbase + r
     uint32_t node[kMaxBatch], vnn[kMaxBatch], vno[kMaxBatch], colbase[kMaxBatch];
     unsigned long long doff[kMaxBatch];
 };
@@ -108,10 +128,13 @@ __device__ __forceinline__ void cp_async_wait_pending() {
 __device__ __forceinline__ void cp_async_wait_0() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
 constexpr size_t kSlabOffset = (sizeof(DistShared) + 127) / 128 * 128;
+constexpr size_t kDistSmem = kSlabOffset + size_t(kStages) * kPassBlk * kBlkPitch * sizeof(float);
+// four CTAs per SM (the register limit at 128 threads): <= 55 KB each plus
+// the per-CTA reservation
+static_assert(kDistSmem <= 55 * 1024, "join distance kernel shared memory over budget");
 
-__device__ __forceinline__ float* slab_buf(DistShared& sh, uint32_t buf) {
-    return reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(&sh) + kSlabOffset) +
-           size_t(buf) * sh.max_slots * kSlab;
+__device__ __forceinline__ float* ring_base(DistShared& sh) {
+    return reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(&sh) + kSlabOffset);
 }
 
 // Offset of candidate r's row in its node's proposal block (nn new, m = nn + no
@@ -121,52 +144,30 @@ __device__ __forceinline__ size_t prow(uint32_t r, uint32_t nn, uint32_t m) {
     return r < nn ? size_t(r) * m : size_t(nn) * m + size_t(r - nn) * (nn + 1);
 }
 
-__device__ __forceinline__ uint32_t swz(uint32_t slot, uint32_t seg) {
-    return slot * kSlab + ((seg ^ ((slot >> 3) & 3u)) << 3);
+// Float offset of row x of 8-block blk within a ring stage.
+__device__ __forceinline__ uint32_t ring_row(uint32_t blk, uint32_t x) {
+    return blk * kBlkPitch + x * kSlab;
 }
 
-// Stage slab `s` (elements [32 s, 32 s + 32)) of the rows of the column-slot
-// 8-blocks the current pass reads (sh.blklist) into buffer `buf` with 16-byte
-// cp.async; chunks past the row stride are zero (exact: they contribute +0
-// under either accumulation).
-__device__ __forceinline__ void stage_slab(DistShared& sh, const float* __restrict__ data,
-                                           uint32_t stride, uint32_t nblk, uint32_t s,
-                                           uint32_t buf) {
-    constexpr uint32_t kC4 = kSlab / 4;  // 16-byte chunks per row per slab
-    const uint32_t e0 = s * kSlab;
-    float* dst = slab_buf(sh, buf);
-    for (uint32_t i = threadIdx.x; i < nblk * 8u * kC4; i += kThreads) {
-        const uint32_t slot = sh.blklist[i / (8u * kC4)] * 8u + ((i / kC4) & 7u), j = i % kC4;
-        const uint32_t row = sh.colrow[slot];
-        if (row == 0xffffffffu) continue;
-        float* p = dst + swz(slot, j >> 1) + (j & 1u) * 4;
-        const uint32_t e = e0 + 4 * j;
-        if (e < stride)
-            cp_async16(p, data + size_t(row) * stride + e);
-        else
-            *reinterpret_cast<float4*>(p) = make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-}
-
-// Resident mode (the whole padded row fits the slab ring, n_slabs <= kStages):
-// every column slot of the batch, all slabs, staged once per batch; slab s
-// goes to buffer s.  Consecutive threads take consecutive 16-byte chunks of a
-// row, so each row is one coalesced read.
+// Resident mode: every column slot of the batch, all slabs, staged once;
+// slab s of slot r at ring row s * res_slots + r (res_slots a multiple of 8).
+// Consecutive threads take consecutive 16-byte chunks of a row, so each row
+// is one coalesced read; chunks past the row stride are never read.
 __device__ __forceinline__ void stage_batch(DistShared& sh, const float* __restrict__ data,
-                                            uint32_t stride, uint32_t nslots, uint32_t n_slabs) {
+                                            uint32_t stride, uint32_t nslots, uint32_t n_slabs,
+                                            uint32_t res_slots) {
     constexpr uint32_t kC4 = kSlab / 4;
     const uint32_t per_slot = n_slabs * kC4;
+    float* ring = ring_base(sh);
     for (uint32_t i = threadIdx.x; i < nslots * per_slot; i += kThreads) {
         const uint32_t slot = i / per_slot, r = i - slot * per_slot;
         const uint32_t s = r / kC4, j = r % kC4;
         const uint32_t row = sh.colrow[slot];
-        if (row == 0xffffffffu) continue;
-        float* p = slab_buf(sh, s) + swz(slot, j >> 1) + (j & 1u) * 4;
         const uint32_t e = s * kSlab + 4 * j;
-        if (e < stride)
-            cp_async16(p, data + size_t(row) * stride + e);
-        else
-            *reinterpret_cast<float4*>(p) = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (row == 0xffffffffu || e >= stride) continue;
+        float* p = ring + size_t(s) * (res_slots / 8) * kBlkPitch + ring_row(slot >> 3, slot & 7u) +
+                   4 * j;
+        cp_async16(p, data + size_t(row) * stride + e);
     }
 }
 
@@ -179,12 +180,14 @@ __device__ __forceinline__ void stage_batch(DistShared& sh, const float* __restr
 // ones.  acc[4 x + j] holds pairs (x, 2j) and (x, 2j + 1).
 template <bool kFusedTile>
 __device__ __forceinline__ void tile_slab(const float* __restrict__ slab, uint32_t a_blk,
-                                          uint32_t b_blk, uint32_t l8, float2 (&acc)[32]) {
+                                          uint32_t b_blk, uint32_t l8, uint32_t nseg,
+                                          float2 minus_zero, float2 (&acc)[32]) {
     const float2 minus_one = make_float2(-1.0f, -1.0f);
 #pragma unroll
     for (uint32_t s = 0; s < kSlab / 8; ++s) {
-        const float* pa = slab + swz(a_blk * 8, s) + l8;
-        const float* pb = slab + swz(b_blk * 8, s) + l8;
+        if (s >= nseg) break;  // the row's last slab may be partial (stride % 32)
+        const float* pa = slab + ring_row(a_blk, 0) + 8 * s + l8;
+        const float* pb = slab + ring_row(b_blk, 0) + 8 * s + l8;
         float a[8];
         float2 b[4];
 #pragma unroll
@@ -204,13 +207,14 @@ __device__ __forceinline__ void tile_slab(const float* __restrict__ slab, uint32
                     acc[4 * x + j] = __ffma2_rn(diff, diff, acc[4 * x + j]);
                 else
                 {
-                    // unfused: scalar FMUL then packed FADD2.  ptxas (CUDA 12.9)
-                    // contracts a packed mul.rn.f32x2 + add.rn.f32x2 pair into
-                    // FFMA2 even under --fmad=false; a scalar product feeding
-                    // the packed add stays two roundings (checked in SASS).
-                    float2 sq;
-                    sq.x = __fmul_rn(diff.x, diff.x);
-                    sq.y = __fmul_rn(diff.y, diff.y);
+                    // unfused: the rounded square as fma(diff, diff, -0) (x + -0
+                    // == x exactly, +0 included), then a packed FADD2.  ptxas
+                    // (CUDA 12.9) contracts a packed mul.rn.f32x2 +
+                    // add.rn.f32x2 pair into FFMA2 even under --fmad=false, and
+                    // turns an fma with a literal -0 addend into that mul, so
+                    // the -0 arrives as a kernel argument it cannot see
+                    // through (checked in SASS and by the bit-exact tests).
+                    const float2 sq = __ffma2_rn(diff, diff, minus_zero);
                     acc[4 * x + j] = __fadd2_rn(acc[4 * x + j], sq);
                 }
             }
@@ -281,13 +285,15 @@ struct NodeGeom {
     }
 };
 
-// A CTA takes a BATCH of active nodes whose column slots fit the staging
-// buffer together (up to kMaxBatch nodes), so short lists (late iterations,
-// small k) share one tile sweep, one set of barriers and one staging pass
-// instead of paying them per node.
+// A CTA takes a BATCH of active nodes whose column slots fit the slot budget
+// together (up to kMaxBatch nodes), so short lists (late iterations, small k)
+// share one tile sweep, one set of barriers and one staging pass instead of
+// paying them per node.  res_slots > 0 selects resident mode with that slot
+// budget; 0 selects pass mode.
 __global__ void __launch_bounds__(kThreads) join_distances_kernel(
     GraphView g, CandView c, const uint32_t* __restrict__ active, IterCounters* ctr,
-    uint32_t max_slots) {
+    uint32_t res_slots, float minus_zero) {
+    const float2 mz2 = make_float2(minus_zero, minus_zero);  // -0.0f, opaque to ptxas
     extern __shared__ __align__(128) unsigned char smem_raw[];
     DistShared& sh = *reinterpret_cast<DistShared*>(smem_raw);
     const uint32_t tid = threadIdx.x, group = tid >> 3, l8 = tid & 7u;
@@ -295,11 +301,12 @@ __global__ void __launch_bounds__(kThreads) join_distances_kernel(
     if (ctr->overflow) return;
     const uint32_t n_active = ctr->active;
     const uint32_t n_slabs = (stride + kSlab - 1) / kSlab;
-    const bool resident = n_slabs <= kStages;
+    const bool resident = res_slots != 0;
     if (tid == 0) {
         sh.qn = 0;
-        sh.max_slots = max_slots;
+        sh.slot_budget = resident ? res_slots : kSlotTab;
     }
+    uint32_t gslab = 0;  // pass mode: slabs staged so far (ring stage = gslab % kStages)
     // warp 0 claims chunks of kMaxBatch active indices one batch ahead, so
     // the claim's atomic round trip overlaps the current batch
     uint32_t a_next = 0;
@@ -343,7 +350,7 @@ __global__ void __launch_bounds__(kThreads) join_distances_kernel(
                 }
             }
             const bool fit = lane < qn && lane < kMaxBatch &&
-                             (lane == 0 || (si <= sh.max_slots && ti <= kMaxTiles - 8));
+                             (lane == 0 || (si <= sh.slot_budget && ti <= kMaxTiles - 8));
             const uint32_t nv = __popc(__ballot_sync(0xffffffffu, fit));  // a prefix
             __syncwarp();
             if (lane < nv) {
@@ -389,7 +396,7 @@ __global__ void __launch_bounds__(kThreads) join_distances_kernel(
         __syncthreads();
         // resident mode: the batch's rows load while the tile list is built
         if (resident) {
-            stage_batch(sh, g.data, stride, sh.nslots, n_slabs);
+            stage_batch(sh, g.data, stride, sh.nslots, n_slabs, res_slots);
             cp_async_commit();
         }
         // live tiles (any valid pair) of all nodes: fused tiles, padding to a
@@ -459,9 +466,59 @@ __global__ void __launch_bounds__(kThreads) join_distances_kernel(
             __syncthreads();
         }
 
-        for (uint32_t t0 = 0; t0 < n_tiles; t0 += kGroups) {
+        uint32_t pass_len = kGroups;
+        for (uint32_t t0 = 0; t0 < n_tiles; t0 += pass_len) {
+            if (!resident) {
+                // warp 0 schedules the pass: the longest run of whole warps'
+                // tiles (<= 16) whose 8-blocks fit kPassBlk ring positions
+                if (tid < 32) {
+                    const uint32_t lane = tid, left = min(kGroups, n_tiles - t0);
+                    uint64_t m = 0;
+                    if (lane < left) {
+                        const uint32_t tile = sh.tiles[t0 + lane];
+                        if (tile != kDeadTile) {
+                            const uint32_t v = tile >> 13, rb = (tile >> 8) & 31u,
+                                           cb = tile & 0xffu;
+                            NodeGeom ng;
+                            ng.set(sh.vnn[v], sh.vno[v]);
+                            const uint32_t cb0 = sh.colbase[v] / 8;
+                            const uint32_t ab =
+                                cb0 + (rb * 8 < ng.rf ? rb : ng.cf / 8 + (rb - ng.rf / 8));
+                            m = (1ull << ab) | (1ull << (cb0 + cb));
+                        }
+                    }
+#pragma unroll
+                    for (uint32_t o = 1; o < 32; o <<= 1) {
+                        const uint64_t mp = __shfl_up_sync(0xffffffffu, m, o);
+                        if (lane >= o) m |= mp;
+                    }
+                    const bool ok = lane < left && __popcll(m) <= kPassBlk &&
+                                    ((lane & 3u) == 3u || lane + 1 == left);
+                    const uint32_t okm = __ballot_sync(0xffffffffu, ok);
+                    const uint32_t last = 31u - __clz(okm);  // 4 tiles need <= 8 blocks
+                    const uint64_t pm = __shfl_sync(0xffffffffu, m, last);
+                    for (uint32_t bit = lane; bit < kBlkTab; bit += 32)
+                        if ((pm >> bit) & 1ull) {
+                            const uint32_t pos = __popcll(pm & ((1ull << bit) - 1ull));
+                            sh.blkpos[bit] = uint8_t(pos);
+                            sh.blklist[pos] = uint8_t(bit);
+                        }
+                    __syncwarp();
+                    // ring row -> data row of the pass (~0: padding slot)
+                    const uint32_t nrows = __popcll(pm) * 8u;
+                    for (uint32_t r = lane; r < kRingRows; r += 32)
+                        sh.ringrow[r] =
+                            r < nrows ? sh.colrow[sh.blklist[r >> 3] * 8u + (r & 7u)] : 0xffffffffu;
+                    if (lane == 0) {
+                        sh.pass_len = last + 1;
+                        sh.nblk = __popcll(pm);
+                    }
+                }
+                __syncthreads();
+                pass_len = sh.pass_len;
+            }
             const uint32_t t = t0 + group;
-            const uint32_t tile0 = t < n_tiles ? sh.tiles[t] : kDeadTile;
+            const uint32_t tile0 = group < pass_len && t < n_tiles ? sh.tiles[t] : kDeadTile;
             const bool live = tile0 != kDeadTile;
             const uint32_t tile = live ? tile0 : 0u;
             const uint32_t v = tile >> 13, rb = (tile >> 8) & 31u, cb = tile & 0xffu;
@@ -479,49 +536,64 @@ __global__ void __launch_bounds__(kThreads) join_distances_kernel(
             if (resident) {
                 if (live)
                     for (uint32_t s = 0; s < n_slabs; ++s) {
+                        const float* slab = ring_base(sh) + size_t(s) * (res_slots / 8) * kBlkPitch;
+                        const uint32_t nseg = min(kSlab, stride - s * kSlab) / 8u;
                         if (fused)
-                            tile_slab<true>(slab_buf(sh, s), a_blk, b_blk, l8, acc);
+                            tile_slab<true>(slab, a_blk, b_blk, l8, nseg, mz2, acc);
                         else
-                            tile_slab<false>(slab_buf(sh, s), a_blk, b_blk, l8, acc);
+                            tile_slab<false>(slab, a_blk, b_blk, l8, nseg, mz2, acc);
                     }
             } else {
-                // stage only the 8-blocks this pass reads
-                if (tid == 0) sh.blkmask = 0;
-                __syncthreads();
-                if (live && l8 == 0) atomicOr(&sh.blkmask, (1u << a_blk) | (1u << b_blk));
-                __syncthreads();
-                if (tid == 0) {
-                    uint32_t msk = sh.blkmask, nb = 0;
-                    while (msk) {
-                        sh.blklist[nb++] = uint8_t(__ffs(msk) - 1);
-                        msk &= msk - 1u;
+                const uint32_t a_pos = live ? sh.blkpos[a_blk] : 0u;
+                const uint32_t b_pos = live ? sh.blkpos[b_blk] : 0u;
+                // kStages-deep cp.async ring, one barrier per slab.  Thread
+                // tid stages 16-byte chunk tid % 8 of ring rows tid / 8 + 16 q;
+                // its data rows are read from the ring table once per pass.
+                constexpr uint32_t kRowsPerThread = (kRingRows + 15) / 16;
+                const uint32_t j = tid & 7u;
+                uint32_t my_rows[kRowsPerThread];
+#pragma unroll
+                for (uint32_t q = 0; q < kRowsPerThread; ++q) {
+                    const uint32_t r = (tid >> 3) + 16 * q;
+                    my_rows[q] = r < kRingRows ? sh.ringrow[r] : 0xffffffffu;
+                }
+                float* const my_dst = ring_base(sh) + ring_row(tid >> 6, (tid >> 3) & 7u) + 4 * j;
+                auto issue = [&](uint32_t sl) {
+                    const uint32_t st = (gslab + sl) % kStages, e = sl * kSlab + 4 * j;
+                    if (e < stride) {
+                        float* const dst = my_dst + size_t(st) * kPassBlk * kBlkPitch;
+#pragma unroll
+                        for (uint32_t q = 0; q < kRowsPerThread; ++q)
+                            if (my_rows[q] != 0xffffffffu)
+                                cp_async16(dst + q * 2 * kBlkPitch,
+                                           g.data + size_t(my_rows[q]) * stride + e);
                     }
-                    sh.nblk = nb;
-                }
-                __syncthreads();
-                const uint32_t nblk = sh.nblk;
-                // 3-stage cp.async pipeline, one barrier per slab
+                    cp_async_commit();
+                };
                 for (uint32_t p = 0; p < kStages - 1; ++p) {
-                    if (p < n_slabs) stage_slab(sh, g.data, stride, nblk, p, p);
-                    cp_async_commit();
+                    if (p < n_slabs)
+                        issue(p);
+                    else
+                        cp_async_commit();
                 }
-                for (uint32_t s = 0; s < n_slabs; ++s) {
-                    cp_async_wait_pending<kStages - 2>();  // slab s has landed
-                    __syncthreads();
-                    if (s + kStages - 1 < n_slabs)
-                        stage_slab(sh, g.data, stride, nblk, s + kStages - 1,
-                                   (s + kStages - 1) % kStages);
-                    cp_async_commit();
-                    const float* slab = slab_buf(sh, s % kStages);
+                for (uint32_t sl = 0; sl < n_slabs; ++sl) {
+                    const uint32_t st = (gslab + sl) % kStages;
+                    cp_async_wait_pending<kStages - 2>();  // slab sl has landed
+                    __syncthreads();  // for every thread; and slab sl - 1's stage is free
+                    if (sl + kStages - 1 < n_slabs)
+                        issue(sl + kStages - 1);
+                    else
+                        cp_async_commit();
+                    const float* slab = ring_base(sh) + size_t(st) * kPassBlk * kBlkPitch;
+                    const uint32_t nseg = min(kSlab, stride - sl * kSlab) / 8u;
                     if (live) {
                         if (fused)
-                            tile_slab<true>(slab, a_blk, b_blk, l8, acc);
+                            tile_slab<true>(slab, a_pos, b_pos, l8, nseg, mz2, acc);
                         else
-                            tile_slab<false>(slab, a_blk, b_blk, l8, acc);
+                            tile_slab<false>(slab, a_pos, b_pos, l8, nseg, mz2, acc);
                     }
                 }
-                cp_async_wait_0();
-                __syncthreads();
+                gslab += n_slabs;
             }
             float row[8];
             group_reduce64(acc, l8, row);
@@ -746,28 +818,26 @@ void launch_scatter_rev(const CandView& c, const uint32_t* active, IterCounters*
 void launch_join_distances(const GraphView& g, const CandView& c, const uint32_t* active,
                            IterCounters* ctr, uint32_t max_active, cudaStream_t s) {
     if (!max_active) return;
-    // a node needs at most 2 cap column slots plus two 8-paddings
-    uint32_t max_slots = std::min<uint32_t>(kMaxColSlots, (2 * c.cap + 16 + 7) / 8 * 8);
-    static const int env_slots = [] {
-        const char* v = getenv("KNNG_JOIN_SLOTS");
-        return v ? atoi(v) : 0;
-    }();
-    if (env_slots > 0)
-        max_slots = std::max<uint32_t>(max_slots, std::min<uint32_t>(kMaxColSlots, (env_slots + 7) / 8 * 8));
-    const size_t smem = kSlabOffset + size_t(kStages) * max_slots * kSlab * sizeof(float);
-    static int per_sm[kMaxColSlots + 1] = {};  // occupancy per slab size: query once
-    if (!per_sm[max_slots]) {
+    // resident mode when every slab of the batch's rows fits the ring with a
+    // slot budget of at least one full node (2 cap column slots plus two
+    // 8-paddings); otherwise pass mode
+    const uint32_t n_slabs = (g.stride + kSlab - 1) / kSlab;
+    const uint32_t node_slots = (2 * c.cap + 16 + 7) / 8 * 8;
+    uint32_t res_slots = std::min<uint32_t>(kSlotTab, kStages * kRingRows / n_slabs / 8 * 8);
+    if (res_slots < node_slots) res_slots = 0;
+    static int per_sm = 0;  // occupancy is a property of the kernel: query once
+    if (!per_sm) {
         cudaFuncSetAttribute(join_distances_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(kSlabOffset + size_t(kStages) * kMaxColSlots * kSlab * 4));
+                             int(kDistSmem));
         int v = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, join_distances_kernel, int(kThreads),
-                                                      smem);
-        per_sm[max_slots] = v < 1 ? 1 : v;
+                                                      kDistSmem);
+        per_sm = v < 1 ? 1 : v;
     }
-    uint32_t grid = sm_count() * uint32_t(per_sm[max_slots]);
+    uint32_t grid = sm_count() * uint32_t(per_sm);
     if (grid > max_active) grid = max_active;
     cudaMemsetAsync(&ctr->work, 0, sizeof(uint32_t), s);
-    join_distances_kernel<<<grid, kThreads, smem, s>>>(g, c, active, ctr, max_slots);
+    join_distances_kernel<<<grid, kThreads, kDistSmem, s>>>(g, c, active, ctr, res_slots, -0.0f);
 }
 
 void launch_join_merge(const GraphView& g, const CandView& c, IterCounters* ctr,

@@ -26,7 +26,7 @@ for name in names:
     print(json.dumps(dict(cfg=name, gen_s=round(tg, 2), wall_s=round(wall, 3), build_s=round(m.total_wall_time_s, 3),
         iters=len(m.iterations) - 1, evals=m.total_dist_evals, evals_per_s=m.total_dist_evals / m.total_wall_time_s,
         kernel_ms={k: round(v, 2) for k, v in m.kernel_ms.items()},
-        per_iter=[(it.iteration, round(it.wall_time_s * 1e3, 2), it.dist_evals, it.changes) for it in m.iterations])), flush=True)
+        per_iter=[(it.iteration, round(it.wall_time_s * 1e3, 2), it.dist_evals, it.changes, it.join_candidates, round(it.join_ms, 2)) for it in m.iterations])), flush=True)
     if cfg.n <= 200000 and max_iter >= 30:
         q = np.random.default_rng(1).choice(cfg.n, size=min(cfg.n, 5000), replace=False).astype(np.uint32)
         t = time.time(); ex, _ = kg.brute_force_knng(data, cfg.k, queries=q); tb = time.time() - t
