@@ -85,7 +85,10 @@ constexpr uint32_t kInvalid = 0xffu;
 constexpr uint32_t kMaxBatch = 8;              // nodes per CTA batch
 constexpr uint32_t kSlotTab = 320;             // batch column slots (pass mode budget)
 constexpr uint32_t kBlkTab = kSlotTab / 8;     // batch 8-blocks
-constexpr uint32_t kPassBlk = 15;              // 8-blocks one pass may stage
+#ifndef KNNG_JOIN_PASSBLK
+#define KNNG_JOIN_PASSBLK 15
+#endif
+constexpr uint32_t kPassBlk = KNNG_JOIN_PASSBLK;  // 8-blocks one pass may stage
 constexpr uint32_t kRingRows = kPassBlk * 8;   // rows per ring stage
 // an 8-block of rows in a ring stage: 8 rows of kSlab floats plus 8 floats of
 // padding, so the four groups of a warp reading the same element of rows
@@ -679,10 +682,7 @@ __global__ void __launch_bounds__(kMergeWarps * 32) join_merge_kernel(GraphView 
             uint64_t mrow = 0;
             uint32_t pe = 0;
             if (e0 + lane < cnt) {
-                const uint64_t r = rv[e0 + lane];
-                const uint32_t u = uint32_t(r >> 8), p = uint32_t(r & 0xffu);
-                const uint32_t nn = c.nc[u], m = nn + c.oc[u];
-                mrow = c.doff[u] + prow(p, nn, m);
+                mrow = rv[e0 + lane];
                 pe = uint32_t(c.D[mrow]);
             }
             // The batch's proposals, flattened across entries so every lane of
@@ -758,15 +758,14 @@ __global__ void scatter_rev_kernel(CandView c, const uint32_t* __restrict__ acti
     if (a >= ctr->active || ctr->overflow) return;
     const uint32_t u = active[a], lane = lane_id();
     const uint32_t nn = c.nc[u], no = c.oc[u], m = nn + no;
-    if (lane == 0) {  // the distance kernel's per-node record
-        const uint64_t off = c.doff[u];
+    const uint64_t off = c.doff[u];
+    if (lane == 0)  // the distance kernel's per-node record
         c.arec[a] = make_uint4(u, nn | (no << 16), uint32_t(off), uint32_t(off >> 32));
-    }
     const uint32_t* list = c.ids + size_t(u) * 2 * c.cap;
     for (uint32_t p = lane; p < m; p += 32) {
         const uint32_t x = p < nn ? list[p] : list[c.cap + p - nn];
         const uint32_t slot = c.roff[x] + atomicAdd(c.rcur + x, 1u);
-        c.rev[slot] = (uint64_t(u) << 8) | p;
+        c.rev[slot] = off + prow(p, nn, m);  // t's row of u's proposal block
     }
 }
 
@@ -876,10 +875,7 @@ __global__ void __launch_bounds__(kMergeWarps * 32) export_remote_kernel(
     uint32_t written = 0;
     uint64_t base = kWrite ? offsets[t] : 0;
     for (uint32_t e = 0; e < cnt; ++e) {
-        const uint64_t r = rv[e];
-        const uint32_t u = uint32_t(r >> 8), p = uint32_t(r & 0xffu);
-        const uint32_t nn = c.nc[u], m = nn + c.oc[u];
-        const uint64_t* row = c.D + c.doff[u] + prow(p, nn, m);
+        const uint64_t* row = c.D + rv[e];
         const uint32_t P = uint32_t(row[0]);  // proposals kept for t in this join
         for (uint32_t q0 = 0; q0 < P; q0 += 32) {
             const uint32_t q = q0 + lane;

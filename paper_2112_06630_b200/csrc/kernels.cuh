@@ -25,9 +25,9 @@ struct GraphView {
 
 // Per-iteration candidate lists (CandidateSet layout, selection.hpp:22-49):
 // per node 2*cap ids, new list first, old list second; plus the join's
-// bookkeeping: the size and offset of each active node's distance block, and
-// the reverse index (for every candidate t, the (node, position) pairs whose
-// lists name t) that lets one warp per target pull its proposals.
+// bookkeeping: the size and offset of each active node's proposal block, and
+// the reverse index (for every candidate t, where t's row of each proposal
+// block naming t starts) that lets one warp per target pull its proposals.
 struct CandView {
     uint32_t cap;
     uint32_t* ids;       // n x 2cap
@@ -40,7 +40,7 @@ struct CandView {
     uint32_t* revcnt;    // n, how many active lists name t
     uint32_t* roff;      // n, exclusive prefix sum of revcnt
     uint32_t* rcur;      // n, scatter cursors
-    uint64_t* rev;       // total entries: (u << 8) | position of t in u's list
+    uint64_t* rev;       // total entries: word offset in D of t's row of u's proposal block
     uint64_t* D;         // proposal blocks, see join.cu
     int filter;          // 1: keep only proposals below the target's row maximum
     float* cmax;         // n x 2cap, the row maximum of each listed candidate
