@@ -198,11 +198,26 @@ __global__ void reset_raw_kernel(CandView c, uint32_t n) {
 // graph.hpp:133-143), count the join's evaluations and list the node as
 // active when nn > 0 (compute_step skips nn == 0, descent.hpp:94).
 constexpr uint32_t kFinWarps = 8;
+constexpr uint32_t kFinNodesPerWarp = 4;  // nodes per warp: block-level counters amortised
+constexpr uint32_t kFinNodes = kFinWarps * kFinNodesPerWarp;
 constexpr uint32_t kTomb = 0xffffffffu;
 
+// Per-block accumulation (shared atomics), flushed with one global atomic per
+// counter per block: the iteration counters and the active-list append are
+// single global addresses, so per-node global atomics would serialise.
 struct BlockCounters {
     unsigned long long evals, cands, dwords, rev;
+    uint32_t nact, base;
+    uint32_t act[kFinNodes];
 };
+
+__device__ __forceinline__ void init_block_counters(BlockCounters& acc) {
+    if (threadIdx.x == 0) {
+        acc.evals = acc.cands = acc.dwords = acc.rev = 0;
+        acc.nact = 0;
+    }
+    __syncthreads();
+}
 
 // The join's per-node accounting (one full warp): evaluation count
 // C(nn,2) + nn*no (acceptance.cpp:369-374), the size of the node's proposal
@@ -211,7 +226,6 @@ struct BlockCounters {
 // its lists name.
 __device__ __forceinline__ void join_bookkeeping(const GraphView& g, const CandView& c,
                                                  uint32_t u, uint32_t nn, uint32_t no,
-                                                 uint32_t* active, IterCounters* ctr,
                                                  BlockCounters& acc) {
     const uint32_t lane = lane_id(), m = nn + no;
     if (lane == 0) c.dsz[u] = nn ? uint64_t(nn) * (m + no) + no : 0ull;
@@ -229,18 +243,23 @@ __device__ __forceinline__ void join_bookkeeping(const GraphView& g, const CandV
         atomicAdd(&acc.cands, (unsigned long long)m);
         atomicAdd(&acc.dwords, (unsigned long long)nn * (m + no) + no);
         atomicAdd(&acc.rev, (unsigned long long)m);
-        active[atomicAdd(&ctr->active, 1u)] = u;
+        acc.act[atomicAdd(&acc.nact, 1u)] = u;
     }
 }
 
-__device__ __forceinline__ void flush_block_counters(const BlockCounters& acc,
+// Block-collective: every thread of the block calls it once, at the end.
+__device__ __forceinline__ void flush_block_counters(BlockCounters& acc, uint32_t* active,
                                                      IterCounters* ctr) {
+    __syncthreads();
     if (threadIdx.x == 0) {
         if (acc.evals) atomicAdd(&ctr->evals, acc.evals);
         if (acc.cands) atomicAdd(&ctr->cands, acc.cands);
         if (acc.dwords) atomicAdd(&ctr->dwords, acc.dwords);
         if (acc.rev) atomicAdd(&ctr->rev, acc.rev);
+        acc.base = acc.nact ? atomicAdd(&ctr->active, acc.nact) : 0u;
     }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < acc.nact; i += blockDim.x) active[acc.base + i] = acc.act[i];
 }
 
 __global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(GraphView g, CandView c,
@@ -250,12 +269,13 @@ __global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(GraphView g, C
     __shared__ uint32_t s_old[kFinWarps][kMaxCap];
     __shared__ uint32_t s_hid[kFinWarps][kMaxK];
     __shared__ BlockCounters acc;
-    if (threadIdx.x == 0) acc = BlockCounters{0, 0, 0, 0};
-    __syncthreads();
+    init_block_counters(acc);
     const uint32_t w = threadIdx.x >> 5, lane = lane_id();
-    const uint32_t u = g.lo + blockIdx.x * kFinWarps + w;
     const uint32_t cap = c.cap, k = g.k;
-    if (u < g.hi) {
+    for (uint32_t it = 0; it < kFinNodesPerWarp; ++it) {
+        const uint32_t u = g.lo + (blockIdx.x * kFinNodesPerWarp + it) * kFinWarps + w;
+        if (u >= g.hi) break;
+        __syncwarp();  // the previous node's shared lists are no longer read
         const uint32_t nr = min(c.raw_new[u], cap), orr = min(c.raw_old[u], cap);
         const uint32_t* list = c.ids + size_t(u) * 2 * cap;
         for (uint32_t p = lane; p < nr; p += 32) s_new[w][p] = list[p];
@@ -334,10 +354,9 @@ __global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(GraphView g, C
             c.oc[u] = no;
             g.flags[u] = hflags & ~clear;
         }
-        join_bookkeeping(g, c, u, nn, no, active, ctr, acc);
+        join_bookkeeping(g, c, u, nn, no, acc);
     }
-    __syncthreads();
-    flush_block_counters(acc, ctr);
+    flush_block_counters(acc, active, ctr);
 }
 
 // Bookkeeping only, for candidate lists supplied from outside (the
@@ -346,12 +365,12 @@ __global__ void __launch_bounds__(kFinWarps * 32) bookkeeping_kernel(GraphView g
                                                                      uint32_t* active,
                                                                      IterCounters* ctr) {
     __shared__ BlockCounters acc;
-    if (threadIdx.x == 0) acc = BlockCounters{0, 0, 0, 0};
-    __syncthreads();
-    const uint32_t u = g.lo + blockIdx.x * kFinWarps + (threadIdx.x >> 5);
-    if (u < g.hi) join_bookkeeping(g, c, u, c.nc[u], c.oc[u], active, ctr, acc);
-    __syncthreads();
-    flush_block_counters(acc, ctr);
+    init_block_counters(acc);
+    for (uint32_t it = 0; it < kFinNodesPerWarp; ++it) {
+        const uint32_t u = g.lo + (blockIdx.x * kFinNodesPerWarp + it) * kFinWarps + (threadIdx.x >> 5);
+        if (u < g.hi) join_bookkeeping(g, c, u, c.nc[u], c.oc[u], acc);
+    }
+    flush_block_counters(acc, active, ctr);
 }
 
 inline uint32_t blocks_for(size_t items, uint32_t per_block) {
@@ -395,7 +414,7 @@ void launch_finalize(const GraphView& g, const CandView& c, uint32_t* active,
                      IterCounters* ctr, cudaStream_t s) {
     cudaMemsetAsync(c.revcnt, 0, sizeof(uint32_t) * g.n, s);
     if (g.hi <= g.lo) return;
-    finalize_kernel<<<blocks_for(g.hi - g.lo, kFinWarps), kFinWarps * 32, 0, s>>>(g, c, active,
+    finalize_kernel<<<blocks_for(g.hi - g.lo, kFinNodes), kFinWarps * 32, 0, s>>>(g, c, active,
                                                                                   ctr);
 }
 
@@ -403,7 +422,7 @@ void launch_bookkeeping(const GraphView& g, const CandView& c, uint32_t* active,
                         IterCounters* ctr, cudaStream_t s) {
     cudaMemsetAsync(c.revcnt, 0, sizeof(uint32_t) * g.n, s);
     if (g.hi <= g.lo) return;
-    bookkeeping_kernel<<<blocks_for(g.hi - g.lo, kFinWarps), kFinWarps * 32, 0, s>>>(g, c, active,
+    bookkeeping_kernel<<<blocks_for(g.hi - g.lo, kFinNodes), kFinWarps * 32, 0, s>>>(g, c, active,
                                                                                      ctr);
 }
 

@@ -662,9 +662,15 @@ constexpr uint32_t kMergeWarps = 8;
 
 __global__ void __launch_bounds__(kMergeWarps * 32) join_merge_kernel(GraphView g, CandView c,
                                                                      IterCounters* ctr) {
+    // changes are summed per block without a block barrier (targets are
+    // uneven; finished warps leave at once): the last warp out flushes
     __shared__ unsigned long long s_changes;
+    __shared__ uint32_t s_done;
     if (ctr->overflow) return;
-    if (threadIdx.x == 0) s_changes = 0;
+    if (threadIdx.x == 0) {
+        s_changes = 0;
+        s_done = 0;
+    }
     __syncthreads();
     const uint32_t lane = lane_id();
     const uint32_t t = g.lo + blockIdx.x * kMergeWarps + (threadIdx.x >> 5);
@@ -747,8 +753,14 @@ __global__ void __launch_bounds__(kMergeWarps * 32) join_merge_kernel(GraphView 
             }
         }
     }
-    __syncthreads();
-    if (threadIdx.x == 0 && s_changes) atomicAdd(&ctr->changes, s_changes);
+    if (lane == 0) {
+        __threadfence_block();
+        if (atomicAdd(&s_done, 1u) == kMergeWarps - 1) {
+            __threadfence_block();
+            const unsigned long long ch = atomicAdd(&s_changes, 0ull);
+            if (ch) atomicAdd(&ctr->changes, ch);
+        }
+    }
 }
 
 // One warp per active node: (u, position) into each named candidate's bucket.
