@@ -154,23 +154,24 @@ __device__ __forceinline__ uint32_t ring_row(uint32_t blk, uint32_t x) {
 
 // Resident mode: every column slot of the batch, all slabs, staged once;
 // slab s of slot r at ring row s * res_slots + r (res_slots a multiple of 8).
-// Consecutive threads take consecutive 16-byte chunks of a row, so each row
-// is one coalesced read; chunks past the row stride are never read.
+// Eight consecutive threads take the 16-byte chunks of one row slab, so each
+// row slab is one coalesced 128-byte read; chunks past the row stride are
+// never read.
 __device__ __forceinline__ void stage_batch(DistShared& sh, const float* __restrict__ data,
                                             uint32_t stride, uint32_t nslots, uint32_t n_slabs,
                                             uint32_t res_slots) {
-    constexpr uint32_t kC4 = kSlab / 4;
-    const uint32_t per_slot = n_slabs * kC4;
+    static_assert(kSlab / 4 == 8, "eight 16-byte chunks per row slab");
+    const uint32_t j = threadIdx.x & 7u;
     float* ring = ring_base(sh);
-    for (uint32_t i = threadIdx.x; i < nslots * per_slot; i += kThreads) {
-        const uint32_t slot = i / per_slot, r = i - slot * per_slot;
-        const uint32_t s = r / kC4, j = r % kC4;
-        const uint32_t row = sh.colrow[slot];
+    for (uint32_t s = 0; s < n_slabs; ++s) {
         const uint32_t e = s * kSlab + 4 * j;
-        if (row == 0xffffffffu || e >= stride) continue;
-        float* p = ring + size_t(s) * (res_slots / 8) * kBlkPitch + ring_row(slot >> 3, slot & 7u) +
-                   4 * j;
-        cp_async16(p, data + size_t(row) * stride + e);
+        if (e >= stride) continue;
+        float* const slab = ring + size_t(s) * (res_slots / 8) * kBlkPitch + 4 * j;
+        for (uint32_t slot = threadIdx.x >> 3; slot < nslots; slot += kThreads / 8) {
+            const uint32_t row = sh.colrow[slot];
+            if (row != 0xffffffffu)
+                cp_async16(slab + ring_row(slot >> 3, slot & 7u), data + size_t(row) * stride + e);
+        }
     }
 }
 
@@ -835,7 +836,11 @@ void launch_join_distances(const GraphView& g, const CandView& c, const uint32_t
     const uint32_t n_slabs = (g.stride + kSlab - 1) / kSlab;
     const uint32_t node_slots = (2 * c.cap + 16 + 7) / 8 * 8;
     uint32_t res_slots = std::min<uint32_t>(kSlotTab, kStages * kRingRows / n_slabs / 8 * 8);
-    if (res_slots < node_slots) res_slots = 0;
+    static const bool allow_resident = [] {  // KNNG_JOIN_RESIDENT=0: pass mode always (A/B)
+        const char* v = getenv("KNNG_JOIN_RESIDENT");
+        return !(v && v[0] == '0');
+    }();
+    if (res_slots < node_slots || !allow_resident) res_slots = 0;
     static int per_sm = 0;  // occupancy is a property of the kernel: query once
     if (!per_sm) {
         cudaFuncSetAttribute(join_distances_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
