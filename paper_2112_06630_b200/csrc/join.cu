@@ -660,8 +660,12 @@ __device__ __forceinline__ bool warp_try_insert(uint64_t& key, uint32_t& flags, 
 }
 
 constexpr uint32_t kMergeWarps = 8;
+#ifndef KNNG_MERGE_META
+#define KNNG_MERGE_META 2
+#endif
+constexpr uint32_t kMergeMeta = KNNG_MERGE_META;  // reverse-index chunks per metadata round trip
 
-__global__ void __launch_bounds__(kMergeWarps * 32) join_merge_kernel(GraphView g, CandView c,
+__global__ void __launch_bounds__(kMergeWarps * 32, 6) join_merge_kernel(GraphView g, CandView c,
                                                                      IterCounters* ctr) {
     // changes are summed per block without a block barrier (targets are
     // uneven; finished warps leave at once): the last warp out flushes
@@ -683,66 +687,81 @@ __global__ void __launch_bounds__(kMergeWarps * 32) join_merge_kernel(GraphView 
         float cur_max = key_dist(__shfl_sync(0xffffffffu, key, k - 1));
         uint32_t inserted = 0;
         const uint64_t* rv = c.rev + c.roff[t];
-        for (uint32_t e0 = 0; e0 < cnt; e0 += 32) {
-            // metadata of 32 entries at once, one per lane: where t's row of
-            // the node's proposal block starts and how many proposals it kept
-            uint64_t mrow = 0;
-            uint32_t pe = 0;
-            if (e0 + lane < cnt) {
-                mrow = rv[e0 + lane];
-                pe = uint32_t(c.D[mrow]);
-            }
-            // The batch's proposals, flattened across entries so every lane of
-            // every step has work even when rows are short.  Each step's loads
-            // are issued one step ahead so the fetch overlaps the inserts.
-            uint32_t incl = pe;
+        // Metadata of kMergeMeta chunks of 32 entries at once, one entry per
+        // lane per chunk: where t's row of the node's proposal block starts
+        // and how many proposals it kept.  Loading several chunks per round
+        // trip matters for hub targets named by thousands of lists, most of
+        // whose rows the prefilter left empty.
+        for (uint32_t g0 = 0; g0 < cnt; g0 += 32 * kMergeMeta) {
+            uint64_t mrows[kMergeMeta];
+            uint32_t pes[kMergeMeta];
 #pragma unroll
-            for (uint32_t o = 1; o < 32; o <<= 1) {
-                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += v;
+            for (uint32_t q = 0; q < kMergeMeta; ++q) {
+                const uint32_t e = g0 + 32 * q + lane;
+                mrows[q] = e < cnt ? rv[e] : 0ull;
             }
-            const uint32_t excl = incl - pe;
-            const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-            struct Step {
-                float dist;
-                uint32_t cand;
-                bool valid;
-            };
-            auto fetch = [&](uint32_t f0) {
-                const uint32_t f = f0 + lane;
-                // entry holding flattened partner f: last e with excl[e] <= f
-                uint32_t e = 0;
 #pragma unroll
-                for (uint32_t step = 16; step > 0; step >>= 1) {
-                    const uint32_t probe = __shfl_sync(0xffffffffu, excl, (e + step) & 31u);
-                    if (e + step < 32 && probe <= f) e += step;
+            for (uint32_t q = 0; q < kMergeMeta; ++q) {
+                const uint32_t e = g0 + 32 * q + lane;
+                pes[q] = e < cnt ? uint32_t(c.D[mrows[q]]) : 0u;
+            }
+#pragma unroll
+            for (uint32_t q = 0; q < kMergeMeta; ++q) {
+                if (g0 + 32 * q >= cnt) break;
+                const uint64_t mrow = mrows[q];
+                const uint32_t pe = pes[q];
+                // The batch's proposals, flattened across entries so every lane of
+                // every step has work even when rows are short.  Each step's loads
+                // are issued one step ahead so the fetch overlaps the inserts.
+                uint32_t incl = pe;
+#pragma unroll
+                for (uint32_t o = 1; o < 32; o <<= 1) {
+                    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += v;
                 }
-                const uint64_t row = __shfl_sync(0xffffffffu, mrow, e);
-                const uint32_t q = f - __shfl_sync(0xffffffffu, excl, e);
-                Step st{0.0f, 0u, f < total};
-                if (st.valid) {
-                    const uint64_t kk = c.D[row + 1 + q];
-                    st.dist = key_dist(kk);
-                    st.cand = key_id(kk);
-                }
-                return st;
-            };
-            Step cur = fetch(0);
-            for (uint32_t f0 = 0; f0 < total; f0 += 32) {
-                Step nxt{0.0f, 0u, false};
-                if (f0 + 32 < total) nxt = fetch(f0 + 32);
-                uint32_t pass = __ballot_sync(0xffffffffu, cur.valid && cur.dist < cur_max);
-                while (pass) {
-                    const uint32_t src = __ffs(pass) - 1u;
-                    pass &= pass - 1u;
-                    const float dd = __shfl_sync(0xffffffffu, cur.dist, src);
-                    const uint32_t cc = __shfl_sync(0xffffffffu, cur.cand, src);
-                    if (dd < cur_max && warp_try_insert(key, flags, k, dd, cc)) {
-                        ++inserted;
-                        cur_max = key_dist(__shfl_sync(0xffffffffu, key, k - 1));
+                const uint32_t excl = incl - pe;
+                const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+                struct Step {
+                    float dist;
+                    uint32_t cand;
+                    bool valid;
+                };
+                auto fetch = [&](uint32_t f0) {
+                    const uint32_t f = f0 + lane;
+                    // entry holding flattened partner f: last e with excl[e] <= f
+                    uint32_t e = 0;
+#pragma unroll
+                    for (uint32_t step = 16; step > 0; step >>= 1) {
+                        const uint32_t probe = __shfl_sync(0xffffffffu, excl, (e + step) & 31u);
+                        if (e + step < 32 && probe <= f) e += step;
                     }
+                    const uint64_t row = __shfl_sync(0xffffffffu, mrow, e);
+                    const uint32_t q = f - __shfl_sync(0xffffffffu, excl, e);
+                    Step st{0.0f, 0u, f < total};
+                    if (st.valid) {
+                        const uint64_t kk = c.D[row + 1 + q];
+                        st.dist = key_dist(kk);
+                        st.cand = key_id(kk);
+                    }
+                    return st;
+                };
+                Step cur = fetch(0);
+                for (uint32_t f0 = 0; f0 < total; f0 += 32) {
+                    Step nxt{0.0f, 0u, false};
+                    if (f0 + 32 < total) nxt = fetch(f0 + 32);
+                    uint32_t pass = __ballot_sync(0xffffffffu, cur.valid && cur.dist < cur_max);
+                    while (pass) {
+                        const uint32_t src = __ffs(pass) - 1u;
+                        pass &= pass - 1u;
+                        const float dd = __shfl_sync(0xffffffffu, cur.dist, src);
+                        const uint32_t cc = __shfl_sync(0xffffffffu, cur.cand, src);
+                        if (dd < cur_max && warp_try_insert(key, flags, k, dd, cc)) {
+                            ++inserted;
+                            cur_max = key_dist(__shfl_sync(0xffffffffu, key, k - 1));
+                        }
+                    }
+                    cur = nxt;
                 }
-                cur = nxt;
             }
         }
         if (inserted) {
