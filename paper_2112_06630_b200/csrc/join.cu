@@ -97,6 +97,7 @@ constexpr uint32_t kBlkPitch = 8 * kSlab + 8;
 constexpr uint32_t kMaxTiles = 512;            // tiles of one batch
 static_assert(kMaxColSlots <= kSlotTab, "one node must fit the slot table");
 static_assert(kBlkTab <= 64, "pass block masks are 64-bit");
+static_assert(kPassBlk >= 8, "a warp's four tiles may read eight 8-blocks");
 
 struct DistShared {
     // the slab ring (kStages x kPassBlk x kBlkPitch floats) follows this
@@ -154,20 +155,20 @@ __device__ __forceinline__ uint32_t ring_row(uint32_t blk, uint32_t x) {
 
 // Resident mode: every column slot of the batch, all slabs, staged once;
 // slab s of slot r at ring row s * res_slots + r (res_slots a multiple of 8).
-// Eight consecutive threads take the 16-byte chunks of one row slab, so each
-// row slab is one coalesced 128-byte read; chunks past the row stride are
-// never read.
+// kSlab / 4 consecutive threads take the 16-byte chunks of one row slab, so
+// each row slab is one coalesced read; chunks past the row stride are never
+// read.
 __device__ __forceinline__ void stage_batch(DistShared& sh, const float* __restrict__ data,
                                             uint32_t stride, uint32_t nslots, uint32_t n_slabs,
                                             uint32_t res_slots) {
-    static_assert(kSlab / 4 == 8, "eight 16-byte chunks per row slab");
-    const uint32_t j = threadIdx.x & 7u;
+    constexpr uint32_t kC4 = kSlab / 4;  // 16-byte chunks per row slab
+    const uint32_t j = threadIdx.x % kC4;
     float* ring = ring_base(sh);
     for (uint32_t s = 0; s < n_slabs; ++s) {
         const uint32_t e = s * kSlab + 4 * j;
         if (e >= stride) continue;
         float* const slab = ring + size_t(s) * (res_slots / 8) * kBlkPitch + 4 * j;
-        for (uint32_t slot = threadIdx.x >> 3; slot < nslots; slot += kThreads / 8) {
+        for (uint32_t slot = threadIdx.x / kC4; slot < nslots; slot += kThreads / kC4) {
             const uint32_t row = sh.colrow[slot];
             if (row != 0xffffffffu)
                 cp_async16(slab + ring_row(slot >> 3, slot & 7u), data + size_t(row) * stride + e);
@@ -551,17 +552,20 @@ __global__ void __launch_bounds__(kThreads) join_distances_kernel(
                 const uint32_t a_pos = live ? sh.blkpos[a_blk] : 0u;
                 const uint32_t b_pos = live ? sh.blkpos[b_blk] : 0u;
                 // kStages-deep cp.async ring, one barrier per slab.  Thread
-                // tid stages 16-byte chunk tid % 8 of ring rows tid / 8 + 16 q;
-                // its data rows are read from the ring table once per pass.
-                constexpr uint32_t kRowsPerThread = (kRingRows + 15) / 16;
-                const uint32_t j = tid & 7u;
+                // tid stages 16-byte chunk tid % kC4 of ring rows
+                // tid / kC4 + kSweep q; its data rows are read from the ring
+                // table once per pass.
+                constexpr uint32_t kC4 = kSlab / 4, kSweep = kThreads / kC4;
+                constexpr uint32_t kRowsPerThread = (kRingRows + kSweep - 1) / kSweep;
+                static_assert(kSweep % 8 == 0, "a sweep covers whole 8-blocks");
+                const uint32_t j = tid % kC4, r0 = tid / kC4;
                 uint32_t my_rows[kRowsPerThread];
 #pragma unroll
                 for (uint32_t q = 0; q < kRowsPerThread; ++q) {
-                    const uint32_t r = (tid >> 3) + 16 * q;
+                    const uint32_t r = r0 + kSweep * q;
                     my_rows[q] = r < kRingRows ? sh.ringrow[r] : 0xffffffffu;
                 }
-                float* const my_dst = ring_base(sh) + ring_row(tid >> 6, (tid >> 3) & 7u) + 4 * j;
+                float* const my_dst = ring_base(sh) + ring_row(r0 >> 3, r0 & 7u) + 4 * j;
                 auto issue = [&](uint32_t sl) {
                     const uint32_t st = (gslab + sl) % kStages, e = sl * kSlab + 4 * j;
                     if (e < stride) {
@@ -569,7 +573,7 @@ __global__ void __launch_bounds__(kThreads) join_distances_kernel(
 #pragma unroll
                         for (uint32_t q = 0; q < kRowsPerThread; ++q)
                             if (my_rows[q] != 0xffffffffu)
-                                cp_async16(dst + q * 2 * kBlkPitch,
+                                cp_async16(dst + q * (kSweep / 8) * kBlkPitch,
                                            g.data + size_t(my_rows[q]) * stride + e);
                     }
                     cp_async_commit();
