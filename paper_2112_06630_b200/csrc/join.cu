@@ -133,9 +133,13 @@ __device__ __forceinline__ void cp_async_wait_0() { asm volatile("cp.async.wait_
 
 constexpr size_t kSlabOffset = (sizeof(DistShared) + 127) / 128 * 128;
 constexpr size_t kDistSmem = kSlabOffset + size_t(kStages) * kPassBlk * kBlkPitch * sizeof(float);
-// four CTAs per SM (the register limit at 128 threads): <= 55 KB each plus
-// the per-CTA reservation
-static_assert(kDistSmem <= 55 * 1024, "join distance kernel shared memory over budget");
+#ifndef KNNG_JOIN_MINBLOCKS
+#define KNNG_JOIN_MINBLOCKS 4
+#endif
+// KNNG_JOIN_MINBLOCKS CTAs per SM: shared memory within the SM's 228 KB
+// (1 KB reserved per CTA); registers capped by __launch_bounds__
+static_assert(kDistSmem + 1024 <= 228 * 1024 / KNNG_JOIN_MINBLOCKS,
+              "join distance kernel shared memory over budget");
 
 __device__ __forceinline__ float* ring_base(DistShared& sh) {
     return reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(&sh) + kSlabOffset);
@@ -295,7 +299,7 @@ struct NodeGeom {
 // share one tile sweep, one set of barriers and one staging pass instead of
 // paying them per node.  res_slots > 0 selects resident mode with that slot
 // budget; 0 selects pass mode.
-__global__ void __launch_bounds__(kThreads) join_distances_kernel(
+__global__ void __launch_bounds__(kThreads, KNNG_JOIN_MINBLOCKS) join_distances_kernel(
     GraphView g, CandView c, const uint32_t* __restrict__ active, IterCounters* ctr,
     uint32_t res_slots, float minus_zero) {
     const float2 mz2 = make_float2(minus_zero, minus_zero);  // -0.0f, opaque to ptxas
