@@ -294,6 +294,16 @@ struct NodeGeom {
     }
 };
 
+#ifndef KNNG_JOIN_STATS
+#define KNNG_JOIN_STATS 0  // 1: count batches / passes / tiles / staged blocks (diagnostics)
+#endif
+#if KNNG_JOIN_STATS
+__device__ unsigned long long g_join_stats[8];
+#define JOIN_STAT(i, v) atomicAdd(&g_join_stats[i], (unsigned long long)(v))
+#else
+#define JOIN_STAT(i, v) ((void)0)
+#endif
+
 // A CTA takes a BATCH of active nodes whose column slots fit the slot budget
 // together (up to kMaxBatch nodes), so short lists (late iterations, small k)
 // share one tile sweep, one set of barriers and one staging pass instead of
@@ -381,6 +391,10 @@ __global__ void __launch_bounds__(kThreads, KNNG_JOIN_MINBLOCKS) join_distances_
         __syncthreads();
         const uint32_t nv = sh.nv;
         if (nv == 0) break;
+        if (tid == 0) {
+            JOIN_STAT(0, 1);
+            JOIN_STAT(1, nv);
+        }
         // slot maps of every node of the batch
         for (uint32_t v = 0; v < nv; ++v) {
             NodeGeom ng;
@@ -470,6 +484,7 @@ __global__ void __launch_bounds__(kThreads, KNNG_JOIN_MINBLOCKS) join_distances_
             }
         }
         const uint32_t n_tiles = sh.n_tiles;
+        if (tid == 0) JOIN_STAT(6, n_tiles);
         if (resident) {
             cp_async_wait_0();
             __syncthreads();
@@ -525,6 +540,12 @@ __global__ void __launch_bounds__(kThreads, KNNG_JOIN_MINBLOCKS) join_distances_
                 }
                 __syncthreads();
                 pass_len = sh.pass_len;
+                if (tid == 0) {
+                    JOIN_STAT(2, 1);
+                    JOIN_STAT(3, pass_len);
+                    JOIN_STAT(4, sh.nblk);
+                    JOIN_STAT(5, n_slabs);
+                }
             }
             const uint32_t t = t0 + group;
             const uint32_t tile0 = group < pass_len && t < n_tiles ? sh.tiles[t] : kDeadTile;
@@ -1030,3 +1051,14 @@ void launch_merge_received(const GraphView& g, const uint32_t* records, uint64_t
 }
 
 }  // namespace knng_cuda
+
+#if KNNG_JOIN_STATS
+// Diagnostics build only: read and clear the join counters.
+extern "C" int knng_cuda_debug_join_stats(unsigned long long* out) {
+    if (cudaMemcpyFromSymbol(out, knng_cuda::g_join_stats, sizeof(unsigned long long) * 8) !=
+        cudaSuccess)
+        return 1;
+    const unsigned long long zero[8] = {};
+    return cudaMemcpyToSymbol(knng_cuda::g_join_stats, zero, sizeof(zero)) != cudaSuccess;
+}
+#endif
