@@ -26,8 +26,12 @@ def make_data(kind, n, seed=0):
         rng = np.random.default_rng(seed)
         c = rng.normal(0, 10, (20, 128)).astype(np.float32)
         return (c[rng.integers(0, 20, n)] + rng.standard_normal((n, 128), dtype=np.float32))
+    if kind in ("C4", "C5"):  # d = 96 (resident staging), d = 960 (30 slabs per row)
+        return datasets.generate(datasets.CONFIGS[kind], n)
     if kind == "G24":
         return np.random.default_rng(seed).standard_normal((n, 24), dtype=np.float32)
+    if kind == "D100":  # stride 104: a partial last slab (8 floats) in resident staging
+        return np.random.default_rng(seed).uniform(0, 1, (n, 100)).astype(np.float32)
     raise KeyError(kind)
 
 
@@ -36,6 +40,9 @@ CASES = [  # kind, n, k, cap, seed, step
     ("C2", 3000, 20, 50, 1, 1), ("C2", 3000, 20, 50, 1, 2), ("C2", 3000, 20, 50, 1, 6),
     ("C3", 4000, 30, 50, 2, 1), ("C3", 4000, 30, 50, 2, 2), ("C3", 4000, 30, 50, 2, 4),
     ("G24", 600, 8, 15, 11, 1),
+    ("C4", 4000, 10, 50, 3, 1), ("C4", 4000, 10, 50, 3, 3),
+    ("C5", 2000, 20, 50, 4, 1), ("C5", 2000, 20, 50, 4, 2),
+    ("D100", 1500, 12, 20, 5, 1), ("D100", 1500, 12, 20, 5, 2),
 ]
 
 
