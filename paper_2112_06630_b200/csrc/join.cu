@@ -425,73 +425,68 @@ __global__ void __launch_bounds__(kThreads, KNNG_JOIN_MINBLOCKS) join_distances_
         // live tiles (any valid pair) of all nodes: fused tiles, padding to a
         // whole warp (4 groups), then unfused tiles, so every warp runs one
         // path; in (node, rb, cb) order so a warp's groups mostly share A
-        uint32_t total = 0;
-        for (uint32_t v = 0; v < nv; ++v) {
-            NodeGeom ng;
-            ng.set(sh.vnn[v], sh.vno[v]);
-            total += ng.rbs() * ng.cbs();
-        }
-        for (uint32_t phase = 0; phase < 2; ++phase) {
-            for (uint32_t t0 = 0; t0 < total; t0 += kThreads) {
-                uint32_t t = t0 + tid, v = 0;
-                bool live = false;
+        // (built by warp 0 alone: ballot compaction in chunks of 32, no CTA
+        // barriers while the other warps' row copies are in flight)
+        if (tid < 32) {
+            const uint32_t lane = tid;
+            uint32_t total = 0;
+            for (uint32_t v = 0; v < nv; ++v) {
                 NodeGeom ng;
-                ng.set(sh.vnn[0], sh.vno[0]);
-                if (t < total) {
-                    while (t >= ng.rbs() * ng.cbs()) {
-                        t -= ng.rbs() * ng.cbs();
-                        ++v;
-                        ng.set(sh.vnn[v], sh.vno[v]);
-                    }
-                    const uint32_t rb = t / ng.cbs(), cb = t % ng.cbs();
-                    const bool fused_tile = rb * 8 < ng.rf && cb * 8 < ng.cf;
-                    if (fused_tile == (phase == 0)) {
-                        uint32_t imin = kInvalid;
-                        for (uint32_t x = 0; x < 8; ++x)
-                            imin = min(imin, uint32_t(sh.rowmap[v][rb * 8 + x]));
-                        if (imin != kInvalid)
-                            for (uint32_t y = 0; y < 8; ++y) {
-                                const uint32_t col = sh.colmap[sh.colbase[v] + cb * 8 + y];
-                                live |= col != kInvalid && (col >= ng.nn || col > imin);
-                            }
-                    }
-                }
-                // order-preserving compaction: warp ballots + per-warp offsets
-                const uint32_t mask = __ballot_sync(0xffffffffu, live);
-                if ((tid & 31u) == 0) sh.warp_cnt[tid >> 5] = __popc(mask);
-                __syncthreads();
-                uint32_t base = sh.n_tiles;
-                for (uint32_t w = 0; w < (tid >> 5); ++w) base += sh.warp_cnt[w];
-                if (live) {
-                    const uint32_t rb = t / ng.cbs(), cb = t % ng.cbs();
-                    sh.tiles[base + __popc(mask & ((1u << (tid & 31u)) - 1u))] =
-                        uint16_t((v << 13) | (rb << 8) | cb);
-                }
-                __syncthreads();
-                if (tid == 0) {
-                    uint32_t tot = 0;
-                    for (uint32_t w = 0; w < kThreads / 32; ++w) tot += sh.warp_cnt[w];
-                    sh.n_tiles += tot;
-                }
-                __syncthreads();
+                ng.set(sh.vnn[v], sh.vno[v]);
+                total += ng.rbs() * ng.cbs();
             }
-            if (phase == 0) {  // pad the fused run to whole warps with dead tiles
-                const uint32_t nt = sh.n_tiles, padded = (nt + 3u) & ~3u;
-                if (tid < padded - nt) sh.tiles[nt + tid] = kDeadTile;
-                __syncthreads();
-                if (tid == 0) sh.n_tiles = padded;
-                __syncthreads();
+            uint32_t nt = 0;
+            for (uint32_t phase = 0; phase < 2; ++phase) {
+                for (uint32_t t0 = 0; t0 < total; t0 += 32) {
+                    uint32_t t = t0 + lane, v = 0, rb = 0, cb = 0;
+                    bool live = false;
+                    if (t < total) {
+                        NodeGeom ng;
+                        ng.set(sh.vnn[0], sh.vno[0]);
+                        while (t >= ng.rbs() * ng.cbs()) {
+                            t -= ng.rbs() * ng.cbs();
+                            ++v;
+                            ng.set(sh.vnn[v], sh.vno[v]);
+                        }
+                        rb = t / ng.cbs();
+                        cb = t % ng.cbs();
+                        const bool fused_tile = rb * 8 < ng.rf && cb * 8 < ng.cf;
+                        if (fused_tile == (phase == 0)) {
+                            uint32_t imin = kInvalid;
+                            for (uint32_t x = 0; x < 8; ++x)
+                                imin = min(imin, uint32_t(sh.rowmap[v][rb * 8 + x]));
+                            if (imin != kInvalid)
+                                for (uint32_t y = 0; y < 8; ++y) {
+                                    const uint32_t col = sh.colmap[sh.colbase[v] + cb * 8 + y];
+                                    live |= col != kInvalid && (col >= ng.nn || col > imin);
+                                }
+                        }
+                    }
+                    const uint32_t mask = __ballot_sync(0xffffffffu, live);
+                    if (live)
+                        sh.tiles[nt + __popc(mask & ((1u << lane) - 1u))] =
+                            uint16_t((v << 13) | (rb << 8) | cb);
+                    nt += __popc(mask);
+                }
+                if (phase == 0) {  // pad the fused run to whole warps with dead tiles
+                    const uint32_t padded = (nt + 3u) & ~3u;
+                    if (lane < padded - nt) sh.tiles[nt + lane] = kDeadTile;
+                    nt = padded;
+                }
             }
+            if (lane == 0) sh.n_tiles = nt;
         }
+        if (resident) cp_async_wait_0();
+        __syncthreads();
         const uint32_t n_tiles = sh.n_tiles;
         if (tid == 0) JOIN_STAT(6, n_tiles);
-        if (resident) {
-            cp_async_wait_0();
-            __syncthreads();
-        }
 
         uint32_t pass_len = kGroups;
         for (uint32_t t0 = 0; t0 < n_tiles; t0 += pass_len) {
+            if (resident && tid == 0) {
+                JOIN_STAT(2, 1);
+                JOIN_STAT(3, min(kGroups, n_tiles - t0));
+            }
             if (!resident) {
                 // warp 0 schedules the pass: the longest run of whole warps'
                 // tiles (<= 16) whose 8-blocks fit kPassBlk ring positions

@@ -23,6 +23,7 @@ for it in range(1, 17):
     cur = np.array(buf[:], np.int64)
     d = cur - prev
     prev = cur
-    if d[2] == 0:
+    if d[0] == 0:
         continue
-    print(it, d[0], d[1], d[2], round(d[3] / d[2], 2), round(d[4] / d[2], 2), d[5], d[6], flush=True)
+    p = max(d[2], 1)
+    print(it, d[0], d[1], d[2], round(d[3] / p, 2), round(d[4] / p, 2), d[5], d[6], flush=True)
