@@ -246,6 +246,8 @@ def test_select_expectation(gpu, restated):
     ("C3", 20000, 30, 50, 3),
     ("C2", 8000, 20, 50, 0),
     ("G24", 4000, 10, 30, 4),
+    ("C4", 20000, 10, 50, 5),      # d = 96: resident staging
+    ("C5", 3000, 20, 50, 6),       # d = 960, normalised gamma: hub-heavy, low recall for both
 ])
 def test_recall_matches_reference(gpu, restated, kind, n, k, cap, seed):
     """End-to-end recall@k within 0.5 pp of the reference's from the same seed
