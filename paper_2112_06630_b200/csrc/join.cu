@@ -912,10 +912,14 @@ void launch_join_merge(const GraphView& g, const CandView& c, IterCounters* ctr,
 namespace {
 
 // Pass 1 (count) / pass 2 (write): one warp per non-owned target t named by
-// this device's lists; its partners below t's row maximum (the replicated,
-// iteration-start value: stale-upwards, so the filter is conservative) become
-// records (t, id, dist bits).  Records are laid out in ascending t, hence
-// grouped by owner device in rank order.
+// this device's lists.  The warp replays its merge on the replica of t's row
+// (iteration-start keys) and exports only the proposals that entered it, at
+// most k per target: a proposal outside the k best distinct ids of (t's row,
+// this device's proposals) cannot enter t's final row (SURVEY §8e
+// pre-reduction; ties aside, as everywhere in the merge).  Both passes replay
+// the same entries in the same order, so they agree.  Records (t, id, dist
+// bits) are laid out in ascending t, hence grouped by owner device in rank
+// order.
 template <bool kWrite>
 __global__ void __launch_bounds__(kMergeWarps * 32) export_remote_kernel(
     GraphView g, CandView c, IterCounters* ctr, uint32_t* counts, const uint64_t* offsets,
@@ -930,28 +934,37 @@ __global__ void __launch_bounds__(kMergeWarps * 32) export_remote_kernel(
         if (!kWrite && lane == 0) counts[t] = 0;
         return;
     }
-    const float mx = g.maxd[t];
+    const uint32_t k = g.k;
+    uint64_t key = lane < k ? g.keys[size_t(t) * k + lane] : kEmptyKey;
+    uint32_t fresh = 0;  // bit i: entry i entered from this device's proposals
+    float cur_max = key_dist(__shfl_sync(0xffffffffu, key, k - 1));
     const uint64_t* rv = c.rev + c.roff[t];
-    uint32_t written = 0;
-    uint64_t base = kWrite ? offsets[t] : 0;
     for (uint32_t e = 0; e < cnt; ++e) {
         const uint64_t* row = c.D + rv[e];
         const uint32_t P = uint32_t(row[0]);  // proposals kept for t in this join
         for (uint32_t q0 = 0; q0 < P; q0 += 32) {
             const uint32_t q = q0 + lane;
             const uint64_t kk = q < P ? row[1 + q] : kEmptyKey;
-            const bool pass = q < P && key_dist(kk) < mx;
-            const uint32_t mask = __ballot_sync(0xffffffffu, pass);
-            if (kWrite && pass) {
-                uint32_t* rec = records + 3 * (base + written + __popc(mask & ((1u << lane) - 1u)));
-                rec[0] = t;
-                rec[1] = key_id(kk);
-                rec[2] = uint32_t(kk >> 32);
+            uint32_t pass = __ballot_sync(0xffffffffu, q < P && key_dist(kk) < cur_max);
+            while (pass) {
+                const uint32_t src = __ffs(pass) - 1u;
+                pass &= pass - 1u;
+                const uint64_t pk = __shfl_sync(0xffffffffu, kk, src);
+                const float dd = key_dist(pk);
+                if (dd < cur_max && warp_try_insert(key, fresh, k, dd, key_id(pk)))
+                    cur_max = key_dist(__shfl_sync(0xffffffffu, key, k - 1));
             }
-            written += __popc(mask);
         }
     }
-    if (!kWrite && lane == 0) counts[t] = written;
+    const uint32_t kmask = k >= 32 ? 0xffffffffu : ((1u << k) - 1u);
+    fresh &= kmask;
+    if (kWrite && ((fresh >> lane) & 1u)) {
+        uint32_t* rec = records + 3 * (offsets[t] + __popc(fresh & ((1u << lane) - 1u)));
+        rec[0] = t;
+        rec[1] = key_id(key);
+        rec[2] = uint32_t(key >> 32);
+    }
+    if (!kWrite && lane == 0) counts[t] = __popc(fresh);
 }
 
 // Received records grouped by target (counting sort), then one warp per owned

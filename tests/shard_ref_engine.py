@@ -138,9 +138,20 @@ class NumpyShardEngine:
             if self.lo <= t < self.hi:
                 changes += self._insert(t, plist)
             else:
+                # pre-reduced export: only the proposals that enter
+                # the k best distinct ids of (t's replicated row, these proposals)
+                row = self._row(t)
+                best = {int(i): float(dd) for i, dd in zip(_ids(row), _dist(row))}
+                entered = {}
                 for pid, pd in plist:
-                    if pd < maxd0[t]:
-                        records.append((t, pid, int(np.float32(pd).view(np.uint32))))
+                    if pd >= maxd0[t] or pid == t or pid in best or pid in entered:
+                        continue
+                    entered[pid] = pd
+                pool = sorted([(d_, i, 0) for i, d_ in best.items()] +
+                              [(d_, i, 1) for i, d_ in entered.items()])[:k]
+                for d_, pid, fresh in pool:
+                    if fresh:
+                        records.append((t, pid, int(np.float32(d_).view(np.uint32))))
         self._local_changes = changes
         owner = [min(self.nranks - 1, t // self.chunk) for t, _, _ in records]
         order = np.argsort(owner, kind="stable") if records else []

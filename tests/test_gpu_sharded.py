@@ -109,6 +109,9 @@ def test_shard_engine_two_ranks_one_process_exchange(gpu):
             t = recs[:, 0].cpu().numpy()
             other = 1 - r
             assert np.all((t >= engs[other].lo) & (t < engs[other].hi))
+            # pre-reduced export: at most k records per remote target
+            if len(t):
+                assert np.bincount(t).max() <= k
         for r in range(2):
             other = 1 - r
             changes += engs[r].merge(steps[other]["send"].clone())
