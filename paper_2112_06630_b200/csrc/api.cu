@@ -217,6 +217,7 @@ struct Engine {
     DevBuf<uint64_t> dsz, doff;
     DevBuf<float> cmax;
     DevBuf<uint4> arec;
+    DevBuf<uint32_t> hubs;
     DevBuf<uint32_t> revcnt, roff, rcur;
     DevBuf<unsigned char> scan_tmp;
     size_t scan_bytes = 0;
@@ -256,6 +257,7 @@ struct Engine {
             doff.alloc(n, pool, s);
             cmax.alloc(size_t(n) * 2 * cap, pool, s);
             arec.alloc(n, pool, s);
+            hubs.alloc(n, pool, s);
             revcnt.alloc(n, pool, s);
             roff.alloc(n, pool, s);
             rcur.alloc(n, pool, s);
@@ -280,7 +282,7 @@ struct Engine {
     CandView cv() const {
         return CandView{cap,   cand.p,   raw_new.p, raw_old.p, nc.p, oc.p, dsz.p,
                         doff.p, revcnt.p, roff.p,   rcur.p,    rev.p, dblocks.p, filter,
-                        cmax.p, arec.p};
+                        cmax.p, arec.p, hubs.p};
     }
 
     void reserve_join(uint64_t rev_entries, uint64_t dwords) {

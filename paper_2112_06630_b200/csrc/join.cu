@@ -642,6 +642,10 @@ __global__ void __launch_bounds__(kThreads, KNNG_JOIN_MINBLOCKS) join_distances_
                     const uint32_t slot_c = sh.colbase[v] + cb * 8 + y;
                     const uint32_t col = sh.colmap[slot_c];
                     if (col == kInvalid || !(col >= nn || col > i)) continue;
+                    // an id listed twice pairs with itself: try_insert ignores
+                    // self (graph.hpp:116-129), so neither endpoint gets it
+                    // (the unfiltered distances-only entry keeps every pair)
+                    if (c.filter && sh.colrow[slot_c] == id_i) continue;
                     const float dist = row[y];
                     if (dist < mx_i) {
                         const uint32_t pos = atomicAdd(&sh.rowcnt[sh.colbase[v] + i], 1u);
@@ -668,7 +672,8 @@ __global__ void __launch_bounds__(kThreads, KNNG_JOIN_MINBLOCKS) join_distances_
 // Warp-wide bounded insert into a sorted row held one key per lane (lanes
 // >= k hold kEmptyKey).  try_insert semantics (graph.hpp:116-129).
 __device__ __forceinline__ bool warp_try_insert(uint64_t& key, uint32_t& flags, uint32_t k,
-                                                float dist, uint32_t cand) {
+                                                float dist, uint32_t cand,
+                                                uint32_t* fresh = nullptr) {
     const uint32_t lane = lane_id();
     const uint64_t max_key = __shfl_sync(0xffffffffu, key, k - 1);
     if (!(dist < key_dist(max_key))) return false;
@@ -680,6 +685,7 @@ __device__ __forceinline__ bool warp_try_insert(uint64_t& key, uint32_t& flags, 
     const uint32_t low = (1u << pos) - 1u;
     const uint32_t kmask = k >= 32 ? 0xffffffffu : ((1u << k) - 1u);
     flags = ((flags & low) | (1u << pos) | ((flags & ~low) << 1)) & kmask;
+    if (fresh) *fresh = ((*fresh & low) | (1u << pos) | ((*fresh & ~low) << 1)) & kmask;
     return true;
 }
 
@@ -689,8 +695,103 @@ constexpr uint32_t kMergeWarps = 8;
 #endif
 constexpr uint32_t kMergeMeta = KNNG_MERGE_META;  // reverse-index chunks per metadata round trip
 
+// Merges the proposals of t's reverse-index entries rv[0, cnt) into the row
+// held by the calling warp (lane i = entry i).  `fresh` tracks which entries
+// came in (shifted like the flags).
+__device__ __forceinline__ void merge_entries(const CandView& c, const uint64_t* rv, uint32_t cnt,
+                                              uint32_t k, uint64_t& key, uint32_t& flags,
+                                              uint32_t& fresh, float& cur_max,
+                                              uint32_t& inserted) {
+    const uint32_t lane = lane_id();
+    // Metadata of kMergeMeta chunks of 32 entries at once, one entry per lane
+    // per chunk: where t's row of the node's proposal block starts and how
+    // many proposals it kept.  Loading several chunks per round trip matters
+    // for hub targets named by thousands of lists, most of whose rows the
+    // prefilter left empty.
+    for (uint32_t g0 = 0; g0 < cnt; g0 += 32 * kMergeMeta) {
+        uint64_t mrows[kMergeMeta];
+        uint32_t pes[kMergeMeta];
+#pragma unroll
+        for (uint32_t q = 0; q < kMergeMeta; ++q) {
+            const uint32_t e = g0 + 32 * q + lane;
+            mrows[q] = e < cnt ? rv[e] : 0ull;
+        }
+#pragma unroll
+        for (uint32_t q = 0; q < kMergeMeta; ++q) {
+            const uint32_t e = g0 + 32 * q + lane;
+            pes[q] = e < cnt ? uint32_t(c.D[mrows[q]]) : 0u;
+        }
+#pragma unroll
+        for (uint32_t q = 0; q < kMergeMeta; ++q) {
+            if (g0 + 32 * q >= cnt) break;
+            const uint64_t mrow = mrows[q];
+            const uint32_t pe = pes[q];
+            // The chunk's proposals, flattened across entries so every lane of
+            // every step has work even when rows are short.  Each step's loads
+            // are issued one step ahead so the fetch overlaps the inserts.
+            uint32_t incl = pe;
+#pragma unroll
+            for (uint32_t o = 1; o < 32; o <<= 1) {
+                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            const uint32_t excl = incl - pe;
+            const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+            struct Step {
+                float dist;
+                uint32_t cand;
+                bool valid;
+            };
+            auto fetch = [&](uint32_t f0) {
+                const uint32_t f = f0 + lane;
+                // entry holding flattened partner f: last e with excl[e] <= f
+                uint32_t e = 0;
+#pragma unroll
+                for (uint32_t step = 16; step > 0; step >>= 1) {
+                    const uint32_t probe = __shfl_sync(0xffffffffu, excl, (e + step) & 31u);
+                    if (e + step < 32 && probe <= f) e += step;
+                }
+                const uint64_t row = __shfl_sync(0xffffffffu, mrow, e);
+                const uint32_t qq = f - __shfl_sync(0xffffffffu, excl, e);
+                Step st{0.0f, 0u, f < total};
+                if (st.valid) {
+                    const uint64_t kk = c.D[row + 1 + qq];
+                    st.dist = key_dist(kk);
+                    st.cand = key_id(kk);
+                }
+                return st;
+            };
+            Step cur = fetch(0);
+            for (uint32_t f0 = 0; f0 < total; f0 += 32) {
+                Step nxt{0.0f, 0u, false};
+                if (f0 + 32 < total) nxt = fetch(f0 + 32);
+                uint32_t pass = __ballot_sync(0xffffffffu, cur.valid && cur.dist < cur_max);
+                while (pass) {
+                    const uint32_t src = __ffs(pass) - 1u;
+                    pass &= pass - 1u;
+                    const float dd = __shfl_sync(0xffffffffu, cur.dist, src);
+                    const uint32_t cc = __shfl_sync(0xffffffffu, cur.cand, src);
+                    if (dd < cur_max && warp_try_insert(key, flags, k, dd, cc, &fresh)) {
+                        ++inserted;
+                        cur_max = key_dist(__shfl_sync(0xffffffffu, key, k - 1));
+                    }
+                }
+                cur = nxt;
+            }
+        }
+    }
+}
+
+// Targets named by more than kHubEntries reverse-index entries are left to
+// hub_merge_kernel (a whole CTA per target).
+#ifndef KNNG_HUB_ENTRIES
+#define KNNG_HUB_ENTRIES 512
+#endif
+constexpr uint32_t kHubEntries = KNNG_HUB_ENTRIES;
+
 __global__ void __launch_bounds__(kMergeWarps * 32, 6) join_merge_kernel(GraphView g, CandView c,
-                                                                     IterCounters* ctr) {
+                                                                     IterCounters* ctr,
+                                                                     uint32_t* hubs) {
     // changes are summed per block without a block barrier (targets are
     // uneven; finished warps leave at once): the last warp out flushes
     __shared__ unsigned long long s_changes;
@@ -705,89 +806,14 @@ __global__ void __launch_bounds__(kMergeWarps * 32, 6) join_merge_kernel(GraphVi
     const uint32_t t = g.lo + blockIdx.x * kMergeWarps + (threadIdx.x >> 5);
     const uint32_t k = g.k;
     const uint32_t cnt = t < g.hi ? c.revcnt[t] : 0u;
-    if (cnt) {
+    if (cnt > kHubEntries && hubs) {
+        if (lane == 0) hubs[atomicAdd(&ctr->hubs, 1u)] = t;
+    } else if (cnt) {
         uint64_t key = lane < k ? g.keys[size_t(t) * k + lane] : kEmptyKey;
-        uint32_t flags = g.flags[t];
+        uint32_t flags = g.flags[t], fresh = 0;
         float cur_max = key_dist(__shfl_sync(0xffffffffu, key, k - 1));
         uint32_t inserted = 0;
-        const uint64_t* rv = c.rev + c.roff[t];
-        // Metadata of kMergeMeta chunks of 32 entries at once, one entry per
-        // lane per chunk: where t's row of the node's proposal block starts
-        // and how many proposals it kept.  Loading several chunks per round
-        // trip matters for hub targets named by thousands of lists, most of
-        // whose rows the prefilter left empty.
-        for (uint32_t g0 = 0; g0 < cnt; g0 += 32 * kMergeMeta) {
-            uint64_t mrows[kMergeMeta];
-            uint32_t pes[kMergeMeta];
-#pragma unroll
-            for (uint32_t q = 0; q < kMergeMeta; ++q) {
-                const uint32_t e = g0 + 32 * q + lane;
-                mrows[q] = e < cnt ? rv[e] : 0ull;
-            }
-#pragma unroll
-            for (uint32_t q = 0; q < kMergeMeta; ++q) {
-                const uint32_t e = g0 + 32 * q + lane;
-                pes[q] = e < cnt ? uint32_t(c.D[mrows[q]]) : 0u;
-            }
-#pragma unroll
-            for (uint32_t q = 0; q < kMergeMeta; ++q) {
-                if (g0 + 32 * q >= cnt) break;
-                const uint64_t mrow = mrows[q];
-                const uint32_t pe = pes[q];
-                // The batch's proposals, flattened across entries so every lane of
-                // every step has work even when rows are short.  Each step's loads
-                // are issued one step ahead so the fetch overlaps the inserts.
-                uint32_t incl = pe;
-#pragma unroll
-                for (uint32_t o = 1; o < 32; o <<= 1) {
-                    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-                    if (lane >= o) incl += v;
-                }
-                const uint32_t excl = incl - pe;
-                const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-                struct Step {
-                    float dist;
-                    uint32_t cand;
-                    bool valid;
-                };
-                auto fetch = [&](uint32_t f0) {
-                    const uint32_t f = f0 + lane;
-                    // entry holding flattened partner f: last e with excl[e] <= f
-                    uint32_t e = 0;
-#pragma unroll
-                    for (uint32_t step = 16; step > 0; step >>= 1) {
-                        const uint32_t probe = __shfl_sync(0xffffffffu, excl, (e + step) & 31u);
-                        if (e + step < 32 && probe <= f) e += step;
-                    }
-                    const uint64_t row = __shfl_sync(0xffffffffu, mrow, e);
-                    const uint32_t q = f - __shfl_sync(0xffffffffu, excl, e);
-                    Step st{0.0f, 0u, f < total};
-                    if (st.valid) {
-                        const uint64_t kk = c.D[row + 1 + q];
-                        st.dist = key_dist(kk);
-                        st.cand = key_id(kk);
-                    }
-                    return st;
-                };
-                Step cur = fetch(0);
-                for (uint32_t f0 = 0; f0 < total; f0 += 32) {
-                    Step nxt{0.0f, 0u, false};
-                    if (f0 + 32 < total) nxt = fetch(f0 + 32);
-                    uint32_t pass = __ballot_sync(0xffffffffu, cur.valid && cur.dist < cur_max);
-                    while (pass) {
-                        const uint32_t src = __ffs(pass) - 1u;
-                        pass &= pass - 1u;
-                        const float dd = __shfl_sync(0xffffffffu, cur.dist, src);
-                        const uint32_t cc = __shfl_sync(0xffffffffu, cur.cand, src);
-                        if (dd < cur_max && warp_try_insert(key, flags, k, dd, cc)) {
-                            ++inserted;
-                            cur_max = key_dist(__shfl_sync(0xffffffffu, key, k - 1));
-                        }
-                    }
-                    cur = nxt;
-                }
-            }
-        }
+        merge_entries(c, c.rev + c.roff[t], cnt, k, key, flags, fresh, cur_max, inserted);
         if (inserted) {
             if (lane < k) g.keys[size_t(t) * k + lane] = key;
             if (lane == 0) {
@@ -804,6 +830,57 @@ __global__ void __launch_bounds__(kMergeWarps * 32, 6) join_merge_kernel(GraphVi
             const unsigned long long ch = atomicAdd(&s_changes, 0ull);
             if (ch) atomicAdd(&ctr->changes, ch);
         }
+    }
+}
+
+// A hub target per CTA: warp w merges a contiguous slice of the target's
+// entries into its own copy of the row; warp 0 then inserts the other warps'
+// incoming entries.  The result is the k smallest distinct candidates of the
+// row and all proposals, as in one warp (ties aside); the change count is the
+// number of entries that came in (the order-free count).
+__global__ void __launch_bounds__(kMergeWarps * 32) hub_merge_kernel(GraphView g, CandView c,
+                                                                    IterCounters* ctr,
+                                                                    const uint32_t* hubs) {
+    __shared__ unsigned long long s_keys[kMergeWarps][32];
+    __shared__ uint32_t s_fresh[kMergeWarps];
+    if (ctr->overflow) return;
+    const uint32_t lane = lane_id(), w = threadIdx.x >> 5, k = g.k;
+    const uint32_t nh = ctr->hubs;
+    for (uint32_t h = blockIdx.x; h < nh; h += gridDim.x) {
+        const uint32_t t = hubs[h];
+        const uint32_t cnt = c.revcnt[t];
+        const uint32_t b = uint32_t(uint64_t(cnt) * w / kMergeWarps);
+        const uint32_t e = uint32_t(uint64_t(cnt) * (w + 1) / kMergeWarps);
+        uint64_t key = lane < k ? g.keys[size_t(t) * k + lane] : kEmptyKey;
+        uint32_t flags = g.flags[t], fresh = 0, inserted = 0;
+        float cur_max = key_dist(__shfl_sync(0xffffffffu, key, k - 1));
+        merge_entries(c, c.rev + c.roff[t] + b, e - b, k, key, flags, fresh, cur_max, inserted);
+        s_keys[w][lane] = key;
+        if (lane == 0) s_fresh[w] = fresh;
+        __syncthreads();
+        if (w == 0) {
+            for (uint32_t o = 1; o < kMergeWarps; ++o) {
+                const uint32_t fr = s_fresh[o];
+                for (uint32_t i = 0; i < k; ++i) {
+                    if (!((fr >> i) & 1u)) continue;
+                    const uint64_t pk = s_keys[o][i];
+                    const float dd = key_dist(pk);
+                    if (dd < cur_max && warp_try_insert(key, flags, k, dd, key_id(pk), &fresh))
+                        cur_max = key_dist(__shfl_sync(0xffffffffu, key, k - 1));
+                }
+            }
+            const uint32_t kmask = k >= 32 ? 0xffffffffu : ((1u << k) - 1u);
+            const uint32_t came = __popc(fresh & kmask);
+            if (came) {
+                if (lane < k) g.keys[size_t(t) * k + lane] = key;
+                if (lane == 0) {
+                    g.flags[t] = flags;
+                    g.maxd[t] = cur_max;
+                    atomicAdd(&ctr->changes, (unsigned long long)came);
+                }
+            }
+        }
+        __syncthreads();
     }
 }
 
@@ -903,7 +980,10 @@ void launch_join_merge(const GraphView& g, const CandView& c, IterCounters* ctr,
                        cudaStream_t s) {
     if (g.hi <= g.lo) return;
     join_merge_kernel<<<(g.hi - g.lo + kMergeWarps - 1) / kMergeWarps, kMergeWarps * 32, 0, s>>>(
-        g, c, ctr);
+        g, c, ctr, c.hubs);
+    // the hubs it left: a CTA each, blocks looping over the device-side count
+    hub_merge_kernel<<<std::min<uint32_t>(2 * sm_count(), (g.hi - g.lo + 1) / 2 + 1),
+                       kMergeWarps * 32, 0, s>>>(g, c, ctr, c.hubs);
 }
 
 // ---------------------------------------------------------------------------

@@ -46,6 +46,7 @@ struct CandView {
     float* cmax;         // n x 2cap, the row maximum of each listed candidate
                          // (iteration start), beside ids
     uint4* arec;         // per active index: {u, nn | no << 16, doff lo, doff hi}
+    uint32_t* hubs;      // n: targets with more than kHubEntries reverse entries
 };
 
 // Device counters for one iteration.
@@ -58,7 +59,7 @@ struct IterCounters {
     uint32_t active;             // number of nodes with nn > 0
     uint32_t work;               // dynamic work counter
     uint32_t overflow;           // distance blocks exceed the buffer: join skipped
-    uint32_t pad;
+    uint32_t hubs;               // merge: targets left to the per-CTA hub merge
 };
 
 // --- graph_kernels.cu ------------------------------------------------------

@@ -354,3 +354,36 @@ def test_reordered_run_returns_original_ids_and_recall(gpu):
     want = ((data[u].astype(np.float64) - data[v]) ** 2).sum(1)
     assert np.allclose(reo.graph.dists.ravel(), want, rtol=1e-5)
     assert not np.any(reo.graph.ids == np.arange(6000)[:, None])
+
+
+def test_hub_target_merge_matches_oracle(gpu, restated):
+    """A target named by every node's new list (2400 reverse entries, above the
+    per-warp limit) goes through the per-CTA hub merge: the step's accepted
+    updates still equal the reference's.  The hub's own lists name one id
+    twice (new and old): the pair of that id with itself is ignored, as
+    try_insert ignores self (graph.hpp:116-129)."""
+    import oracle
+    n, d, k, cap, hub = 2400, 32, 10, 12, 7
+    rng = np.random.default_rng(21)
+    data = rng.standard_normal((n, d), dtype=np.float32)
+    data[hub] = data.mean(axis=0)  # a central point: close to everyone
+    g0, _ = restated.init_random(data, k, 5)
+    ids = np.zeros((n, 2 * cap), np.uint32)
+    nc = np.zeros(n, np.uint32)
+    oc = np.zeros(n, np.uint32)
+    for u in range(n):
+        pool = rng.choice(np.delete(np.arange(n), [u, hub]), size=cap - 1 + 4, replace=False)
+        new = [hub] + pool[: cap - 1].tolist() if u != hub else pool[:cap].tolist()
+        ids[u, : len(new)] = new
+        nc[u] = len(new)
+        old = pool[cap - 1:cap + 3].tolist()
+        ids[u, cap: cap + len(old)] = old
+        oc[u] = len(old)
+    c = oracle.Cands(ids, nc, oc)
+    go, ch_ref, ev_ref = restated.compute_step(data, g0, c)
+    g, rev, ch, ev = kg.compute_step(data, g0.ids, g0.dists, g0.flags,
+                                     kg.CandidateSet(ids, nc, oc))
+    assert ev == ev_ref
+    st = compare_step(g0, go, g, restated=restated, data=data)
+    assert st["mismatch"] == 0 and st["flag_mismatch"] == 0, st
+    assert st["bit_exact"] + st["other_path"] == st["common"], st
