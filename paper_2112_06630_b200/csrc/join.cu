@@ -784,12 +784,15 @@ __device__ __forceinline__ void merge_entries(const CandView& c, const uint64_t*
 
 // Targets named by more than kHubEntries reverse-index entries are left to
 // hub_merge_kernel (a whole CTA per target).
+#ifndef KNNG_MERGE_MINBLOCKS
+#define KNNG_MERGE_MINBLOCKS 8
+#endif
 #ifndef KNNG_HUB_ENTRIES
 #define KNNG_HUB_ENTRIES 512
 #endif
 constexpr uint32_t kHubEntries = KNNG_HUB_ENTRIES;
 
-__global__ void __launch_bounds__(kMergeWarps * 32, 6) join_merge_kernel(GraphView g, CandView c,
+__global__ void __launch_bounds__(kMergeWarps * 32, KNNG_MERGE_MINBLOCKS) join_merge_kernel(GraphView g, CandView c,
                                                                      IterCounters* ctr,
                                                                      uint32_t* hubs) {
     // changes are summed per block without a block barrier (targets are
@@ -805,15 +808,20 @@ __global__ void __launch_bounds__(kMergeWarps * 32, 6) join_merge_kernel(GraphVi
     const uint32_t lane = lane_id();
     const uint32_t t = g.lo + blockIdx.x * kMergeWarps + (threadIdx.x >> 5);
     const uint32_t k = g.k;
-    const uint32_t cnt = t < g.hi ? c.revcnt[t] : 0u;
+    // the row, its flags and the reverse-index range load together (one
+    // round trip), speculatively for targets nothing names
+    const bool in_range = t < g.hi;
+    const uint32_t cnt = in_range ? c.revcnt[t] : 0u;
+    const uint32_t roff = in_range ? c.roff[t] : 0u;
+    uint64_t key = in_range && lane < k ? g.keys[size_t(t) * k + lane] : kEmptyKey;
+    uint32_t flags = in_range ? g.flags[t] : 0u;
     if (cnt > kHubEntries && hubs) {
         if (lane == 0) hubs[atomicAdd(&ctr->hubs, 1u)] = t;
     } else if (cnt) {
-        uint64_t key = lane < k ? g.keys[size_t(t) * k + lane] : kEmptyKey;
-        uint32_t flags = g.flags[t], fresh = 0;
+        uint32_t fresh = 0;
         float cur_max = key_dist(__shfl_sync(0xffffffffu, key, k - 1));
         uint32_t inserted = 0;
-        merge_entries(c, c.rev + c.roff[t], cnt, k, key, flags, fresh, cur_max, inserted);
+        merge_entries(c, c.rev + roff, cnt, k, key, flags, fresh, cur_max, inserted);
         if (inserted) {
             if (lane < k) g.keys[size_t(t) * k + lane] = key;
             if (lane == 0) {
