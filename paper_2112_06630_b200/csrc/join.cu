@@ -37,6 +37,7 @@
 // every evaluated pair is a proposal to both endpoints, kept only when it
 // beats the endpoint's iteration-start row maximum (c.filter; rows maxima only
 // fall during an iteration, so the filter never drops an accepted update).
+#include <cstdio>
 #include <cstdlib>
 #include <cub/device/device_scan.cuh>
 
@@ -111,13 +112,18 @@ struct DistShared {
     uint8_t blkpos[kBlkTab];                  // pass mode: batch 8-block -> ring position
     uint8_t blklist[kPassBlk];                // pass mode: ring position -> batch 8-block
     uint32_t ringrow[kRingRows];              // pass mode: ring row -> data row (~0: none)
-    uint32_t n_tiles, nv, nslots, pass_len, nblk, slot_budget;
+    uint32_t n_tiles, pass_len, nblk, slot_budget;
     // claimed-but-unbatched nodes (claims come in chunks of kMaxBatch)
     uint32_t qn;
     uint4 q[2 * kMaxBatch];  // active-node records (scatter_rev_kernel)
     uint32_t warp_cnt[kThreads / 32];
-    uint32_t node[kMaxBatch], vnn[kMaxBatch], vno[kMaxBatch], colbase[kMaxBatch];
-    unsigned long long doff[kMaxBatch];
+    // batch descriptors, double-buffered: warp 0 forms the next batch while
+    // the current one is processed
+    struct Batch {
+        uint32_t node[kMaxBatch], vnn[kMaxBatch], vno[kMaxBatch], colbase[kMaxBatch];
+        unsigned long long doff[kMaxBatch];
+        uint32_t nv, nslots;
+    } bd[2];
 };
 
 __device__ __forceinline__ void cp_async16(float* smem_dst, const float* gmem_src) {
@@ -294,6 +300,24 @@ struct NodeGeom {
     }
 };
 
+#ifndef KNNG_JOIN_PREFETCH
+#define KNNG_JOIN_PREFETCH 1
+#endif
+#ifndef KNNG_JOIN_CHECKS
+#define KNNG_JOIN_CHECKS 0  // 1: device-side bounds checks with a message (diagnostics)
+#endif
+#if KNNG_JOIN_CHECKS
+#define JCHECK(cond, what, a, b)                                                        \
+    do {                                                                                \
+        if (!(cond)) {                                                                  \
+            printf("join check failed: %s (%u, %u) block %d thread %d\n", what,        \
+                   unsigned(a), unsigned(b), int(blockIdx.x), int(threadIdx.x));      \
+            __trap();                                                                   \
+        }                                                                               \
+    } while (0)
+#else
+#define JCHECK(cond, what, a, b) ((void)0)
+#endif
 #ifndef KNNG_JOIN_STATS
 #define KNNG_JOIN_STATS 0  // 1: count batches / passes / tiles / staged blocks (diagnostics)
 #endif
@@ -331,95 +355,140 @@ __global__ void __launch_bounds__(kThreads, KNNG_JOIN_MINBLOCKS) join_distances_
     uint32_t a_next = 0;
     if (tid == 0) a_next = atomicAdd(&ctr->work, kMaxBatch);
 
-    while (true) {
-        __syncthreads();
-        if (tid < 32) {
-            // warp 0 forms the batch: top the queue up with the claimed chunk
-            // (one 16-byte record per node), claim the next, then take the
-            // longest queue prefix whose column slots and tiles fit
-            const uint32_t lane = tid;
-            uint32_t qn = sh.qn;
-            const uint32_t a = __shfl_sync(0xffffffffu, a_next, 0);
-            if (qn < kMaxBatch && a < n_active) {
-                if (lane < kMaxBatch && a + lane < n_active) sh.q[qn + lane] = c.arec[a + lane];
-                qn += min(kMaxBatch, n_active - a);
-                if (lane == 0) a_next = atomicAdd(&ctr->work, kMaxBatch);
-                __syncwarp();
-            }
-            uint32_t s_l = 0, t_l = 0, u = 0, nn = 0, no = 0;
-            uint4 rec = make_uint4(0, 0, 0, 0);
-            if (lane < qn) {
-                rec = sh.q[lane];
-                u = rec.x;
-                nn = rec.y & 0xffffu;
-                no = rec.y >> 16;
-                NodeGeom ng;
-                ng.set(nn, no);
-                s_l = ng.cf + ng.cs;
-                t_l = ng.rbs() * ng.cbs();
-            }
-            uint32_t si = s_l, ti = t_l;
-#pragma unroll
-            for (uint32_t o = 1; o < 32; o <<= 1) {
-                const uint32_t sp = __shfl_up_sync(0xffffffffu, si, o);
-                const uint32_t tp = __shfl_up_sync(0xffffffffu, ti, o);
-                if (lane >= o) {
-                    si += sp;
-                    ti += tp;
-                }
-            }
-            const bool fit = lane < qn && lane < kMaxBatch &&
-                             (lane == 0 || (si <= sh.slot_budget && ti <= kMaxTiles - 8));
-            const uint32_t nv = __popc(__ballot_sync(0xffffffffu, fit));  // a prefix
+    // warp 0 forms a batch into D: top the queue up with the claimed chunk
+    // (one 16-byte record per node), claim the next, then take the longest
+    // queue prefix whose column slots and tiles fit
+    auto form_batch = [&](DistShared::Batch& D) {
+        const uint32_t lane = tid;
+        uint32_t qn = sh.qn;
+        const uint32_t a = __shfl_sync(0xffffffffu, a_next, 0);
+        if (qn < kMaxBatch && a < n_active) {
+            if (lane < kMaxBatch && a + lane < n_active) sh.q[qn + lane] = c.arec[a + lane];
+            qn += min(kMaxBatch, n_active - a);
+            if (lane == 0) a_next = atomicAdd(&ctr->work, kMaxBatch);
             __syncwarp();
-            if (lane < nv) {
-                sh.node[lane] = u;
-                sh.vnn[lane] = nn;
-                sh.vno[lane] = no;
-                sh.colbase[lane] = si - s_l;
-                sh.doff[lane] = uint64_t(rec.z) | (uint64_t(rec.w) << 32);
-            } else if (lane < qn) {
-                sh.q[lane - nv] = rec;
-            }
-            if (lane == nv - 1) sh.nslots = si;
-            if (lane == 0) {
-                sh.qn = qn - nv;
-                sh.nv = nv;
-                sh.n_tiles = 0;
+        }
+        uint32_t s_l = 0, t_l = 0, u = 0, nn = 0, no = 0;
+        uint4 rec = make_uint4(0, 0, 0, 0);
+        if (lane < qn) {
+            rec = sh.q[lane];
+            u = rec.x;
+            nn = rec.y & 0xffffu;
+            no = rec.y >> 16;
+            NodeGeom ng;
+            ng.set(nn, no);
+            s_l = ng.cf + ng.cs;
+            t_l = ng.rbs() * ng.cbs();
+        }
+        uint32_t si = s_l, ti = t_l;
+#pragma unroll
+        for (uint32_t o = 1; o < 32; o <<= 1) {
+            const uint32_t sp = __shfl_up_sync(0xffffffffu, si, o);
+            const uint32_t tp = __shfl_up_sync(0xffffffffu, ti, o);
+            if (lane >= o) {
+                si += sp;
+                ti += tp;
             }
         }
-        __syncthreads();
-        const uint32_t nv = sh.nv;
+        const bool fit = lane < qn && lane < kMaxBatch &&
+                         (lane == 0 || (si <= sh.slot_budget && ti <= kMaxTiles - 8));
+        const uint32_t nv = __popc(__ballot_sync(0xffffffffu, fit));  // a prefix
+        __syncwarp();
+        if (lane < nv) {
+            D.node[lane] = u;
+            D.vnn[lane] = nn;
+            D.vno[lane] = no;
+            D.colbase[lane] = si - s_l;
+            D.doff[lane] = uint64_t(rec.z) | (uint64_t(rec.w) << 32);
+        } else if (lane < qn) {
+            sh.q[lane - nv] = rec;
+        }
+        if (nv > 0 && lane == nv - 1) D.nslots = si;
+        if (lane == 0) {
+            sh.qn = qn - nv;
+            D.nv = nv;
+            if (nv == 0) D.nslots = 0;  // no stale slots for the prefetch
+        }
+    };
+    // Column-slot contents of batch D, kSlotsPerThread slots per thread
+    // (slot s = tid + kThreads j): the candidate's data-row id and row
+    // maximum.  Loaded into registers one batch ahead, so the loads are in
+    // flight while the current batch computes.
+    constexpr uint32_t kSlotsPerThread = (kSlotTab + kThreads - 1) / kThreads;
+    uint32_t pf_id[kSlotsPerThread];
+    float pf_max[kSlotsPerThread];
+    auto load_slots = [&](const DistShared::Batch& D) {
+#pragma unroll
+        for (uint32_t j = 0; j < kSlotsPerThread; ++j) {
+            const uint32_t sidx = tid + kThreads * j;
+            pf_id[j] = 0xffffffffu;
+            pf_max[j] = 0.0f;
+            if (D.nv > 0 && sidx < D.nslots) {
+                uint32_t v = 0;
+                while (v + 1 < D.nv && D.colbase[v + 1] <= sidx) ++v;
+                NodeGeom ng;
+                ng.set(D.vnn[v], D.vno[v]);
+                const uint32_t x = ng.col(sidx - D.colbase[v]);
+                if (x != kInvalid) {
+                    const uint32_t pos = x < ng.nn ? x : cap + x - ng.nn;
+                    const size_t base = size_t(D.node[v]) * 2 * cap;
+                    pf_id[j] = c.ids[base + pos];
+                    pf_max[j] = c.filter ? c.cmax[base + pos] : __int_as_float(0x7f800000);
+                }
+            }
+        }
+    };
+
+    uint32_t cur = 0;
+    __syncthreads();  // the queue state tid 0 initialised
+    if (tid < 32) form_batch(sh.bd[0]);
+    __syncthreads();
+#if KNNG_JOIN_PREFETCH
+    load_slots(sh.bd[0]);
+#endif
+    while (true) {
+        const DistShared::Batch& B = sh.bd[cur];
+        const uint32_t nv = B.nv;
         if (nv == 0) break;
         if (tid == 0) {
             JOIN_STAT(0, 1);
             JOIN_STAT(1, nv);
+            sh.n_tiles = 0;
         }
-        // slot maps of every node of the batch
+        // slot maps of the batch (contents prefetched one batch ahead)
+#if !KNNG_JOIN_PREFETCH
+        load_slots(B);
+#endif
+#pragma unroll
+        for (uint32_t j = 0; j < kSlotsPerThread; ++j) {
+            const uint32_t sidx = tid + kThreads * j;
+            if (sidx < B.nslots) {
+                uint32_t v = 0;
+                while (v + 1 < nv && B.colbase[v + 1] <= sidx) ++v;
+                NodeGeom ng;
+                ng.set(B.vnn[v], B.vno[v]);
+                JCHECK(sidx < kSlotTab && v < nv, "slot map", sidx, v);
+                sh.colmap[sidx] = uint8_t(ng.col(sidx - B.colbase[v]));
+                sh.colrow[sidx] = pf_id[j];
+                sh.colmax[sidx] = pf_max[j];
+            }
+        }
         for (uint32_t v = 0; v < nv; ++v) {
             NodeGeom ng;
-            ng.set(sh.vnn[v], sh.vno[v]);
-            const uint32_t* list = c.ids + size_t(sh.node[v]) * 2 * cap;
-            const float* cmax = c.cmax + size_t(sh.node[v]) * 2 * cap;
+            ng.set(B.vnn[v], B.vno[v]);
             for (uint32_t sl = tid; sl < ng.rf + ng.rs; sl += kThreads)
                 sh.rowmap[v][sl] = uint8_t(ng.row(sl));
-            for (uint32_t sl = tid; sl < ng.cf + ng.cs; sl += kThreads) {
-                const uint32_t x = ng.col(sl);
-                sh.colmap[sh.colbase[v] + sl] = uint8_t(x);
-                const uint32_t id =
-                    x == kInvalid ? 0xffffffffu : (x < ng.nn ? list[x] : list[cap + x - ng.nn]);
-                sh.colrow[sh.colbase[v] + sl] = id;
-                sh.colmax[sh.colbase[v] + sl] =
-                    x == kInvalid ? 0.0f
-                    : c.filter    ? cmax[x < ng.nn ? x : cap + x - ng.nn]
-                                  : __int_as_float(0x7f800000);
-            }
-            for (uint32_t r = tid; r < ng.nn + ng.no; r += kThreads) sh.rowcnt[sh.colbase[v] + r] = 0;
+            for (uint32_t r = tid; r < ng.nn + ng.no; r += kThreads) sh.rowcnt[B.colbase[v] + r] = 0;
         }
+        // warp 0 forms the next batch meanwhile
+        if (tid < 32) form_batch(sh.bd[cur ^ 1u]);
         __syncthreads();
+#if KNNG_JOIN_PREFETCH
+        load_slots(sh.bd[cur ^ 1u]);  // consumed by the next iteration
+#endif
         // resident mode: the batch's rows load while the tile list is built
         if (resident) {
-            stage_batch(sh, g.data, stride, sh.nslots, n_slabs, res_slots);
+            stage_batch(sh, g.data, stride, B.nslots, n_slabs, res_slots);
             cp_async_commit();
         }
         // live tiles (any valid pair) of all nodes: fused tiles, padding to a
@@ -432,7 +501,7 @@ __global__ void __launch_bounds__(kThreads, KNNG_JOIN_MINBLOCKS) join_distances_
             uint32_t total = 0;
             for (uint32_t v = 0; v < nv; ++v) {
                 NodeGeom ng;
-                ng.set(sh.vnn[v], sh.vno[v]);
+                ng.set(B.vnn[v], B.vno[v]);
                 total += ng.rbs() * ng.cbs();
             }
             uint32_t nt = 0;
@@ -442,11 +511,11 @@ __global__ void __launch_bounds__(kThreads, KNNG_JOIN_MINBLOCKS) join_distances_
                     bool live = false;
                     if (t < total) {
                         NodeGeom ng;
-                        ng.set(sh.vnn[0], sh.vno[0]);
+                        ng.set(B.vnn[0], B.vno[0]);
                         while (t >= ng.rbs() * ng.cbs()) {
                             t -= ng.rbs() * ng.cbs();
                             ++v;
-                            ng.set(sh.vnn[v], sh.vno[v]);
+                            ng.set(B.vnn[v], B.vno[v]);
                         }
                         rb = t / ng.cbs();
                         cb = t % ng.cbs();
@@ -457,7 +526,7 @@ __global__ void __launch_bounds__(kThreads, KNNG_JOIN_MINBLOCKS) join_distances_
                                 imin = min(imin, uint32_t(sh.rowmap[v][rb * 8 + x]));
                             if (imin != kInvalid)
                                 for (uint32_t y = 0; y < 8; ++y) {
-                                    const uint32_t col = sh.colmap[sh.colbase[v] + cb * 8 + y];
+                                    const uint32_t col = sh.colmap[B.colbase[v] + cb * 8 + y];
                                     live |= col != kInvalid && (col >= ng.nn || col > imin);
                                 }
                         }
@@ -499,8 +568,8 @@ __global__ void __launch_bounds__(kThreads, KNNG_JOIN_MINBLOCKS) join_distances_
                             const uint32_t v = tile >> 13, rb = (tile >> 8) & 31u,
                                            cb = tile & 0xffu;
                             NodeGeom ng;
-                            ng.set(sh.vnn[v], sh.vno[v]);
-                            const uint32_t cb0 = sh.colbase[v] / 8;
+                            ng.set(B.vnn[v], B.vno[v]);
+                            const uint32_t cb0 = B.colbase[v] / 8;
                             const uint32_t ab =
                                 cb0 + (rb * 8 < ng.rf ? rb : ng.cf / 8 + (rb - ng.rf / 8));
                             m = (1ull << ab) | (1ull << (cb0 + cb));
@@ -548,11 +617,11 @@ __global__ void __launch_bounds__(kThreads, KNNG_JOIN_MINBLOCKS) join_distances_
             const uint32_t tile = live ? tile0 : 0u;
             const uint32_t v = tile >> 13, rb = (tile >> 8) & 31u, cb = tile & 0xffu;
             NodeGeom ng;
-            ng.set(sh.vnn[v], sh.vno[v]);
+            ng.set(B.vnn[v], B.vno[v]);
             const bool fused = rb * 8 < ng.rf && cb * 8 < ng.cf;
             // row slot block -> column slot block holding the same new
             // candidates, then into the batch's column-slot space
-            const uint32_t cb0 = sh.colbase[v] / 8;
+            const uint32_t cb0 = B.colbase[v] / 8;
             const uint32_t a_blk = cb0 + (rb * 8 < ng.rf ? rb : ng.cf / 8 + (rb - ng.rf / 8));
             const uint32_t b_blk = cb0 + cb;
             float2 acc[32];
@@ -633,13 +702,13 @@ __global__ void __launch_bounds__(kThreads, KNNG_JOIN_MINBLOCKS) join_distances_
                 // iteration-start row maximum — the stale-upwards prefilter of
                 // compute_step (descent.hpp:97-102,134-147)
                 const uint32_t nn = ng.nn, m = ng.nn + ng.no;
-                uint64_t* const D = c.D + sh.doff[v];
-                const uint32_t slot_i = sh.colbase[v] + (i < ng.fn ? i : ng.cf + (i - ng.fn));
+                uint64_t* const D = c.D + B.doff[v];
+                const uint32_t slot_i = B.colbase[v] + (i < ng.fn ? i : ng.cf + (i - ng.fn));
                 const uint32_t id_i = sh.colrow[slot_i];
                 const float mx_i = sh.colmax[slot_i];
 #pragma unroll
                 for (uint32_t y = 0; y < 8; ++y) {
-                    const uint32_t slot_c = sh.colbase[v] + cb * 8 + y;
+                    const uint32_t slot_c = B.colbase[v] + cb * 8 + y;
                     const uint32_t col = sh.colmap[slot_c];
                     if (col == kInvalid || !(col >= nn || col > i)) continue;
                     // an id listed twice pairs with itself: try_insert ignores
@@ -648,11 +717,15 @@ __global__ void __launch_bounds__(kThreads, KNNG_JOIN_MINBLOCKS) join_distances_
                     if (c.filter && sh.colrow[slot_c] == id_i) continue;
                     const float dist = row[y];
                     if (dist < mx_i) {
-                        const uint32_t pos = atomicAdd(&sh.rowcnt[sh.colbase[v] + i], 1u);
+                        JCHECK(B.colbase[v] + i < kSlotTab, "rowcnt i", B.colbase[v], i);
+                    const uint32_t pos = atomicAdd(&sh.rowcnt[B.colbase[v] + i], 1u);
+                    JCHECK(pos + 1 < (i < nn ? m : nn + 1), "row overflow i", pos, m);
                         D[prow(i, nn, m) + 1 + pos] = pack_key(dist, sh.colrow[slot_c]);
                     }
                     if (dist < sh.colmax[slot_c]) {
-                        const uint32_t pos = atomicAdd(&sh.rowcnt[sh.colbase[v] + col], 1u);
+                        JCHECK(B.colbase[v] + col < kSlotTab, "rowcnt col", B.colbase[v], col);
+                    const uint32_t pos = atomicAdd(&sh.rowcnt[B.colbase[v] + col], 1u);
+                    JCHECK(pos + 1 < (col < nn ? m : nn + 1), "row overflow col", pos, m);
                         D[prow(col, nn, m) + 1 + pos] = pack_key(dist, id_i);
                     }
                 }
@@ -661,10 +734,12 @@ __global__ void __launch_bounds__(kThreads, KNNG_JOIN_MINBLOCKS) join_distances_
         // row counts of the batch's proposal blocks
         __syncthreads();
         for (uint32_t v = 0; v < nv; ++v) {
-            const uint32_t nn = sh.vnn[v], m = nn + sh.vno[v];
+            const uint32_t nn = B.vnn[v], m = nn + B.vno[v];
             for (uint32_t r = tid; r < m; r += kThreads)
-                c.D[sh.doff[v] + prow(r, nn, m)] = sh.rowcnt[sh.colbase[v] + r];
+                c.D[B.doff[v] + prow(r, nn, m)] = sh.rowcnt[B.colbase[v] + r];
         }
+        __syncthreads();  // the next batch rewrites the slot tables
+        cur ^= 1u;
     }
 }
 
