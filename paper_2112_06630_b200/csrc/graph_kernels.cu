@@ -262,7 +262,7 @@ __device__ __forceinline__ void flush_block_counters(BlockCounters& acc, uint32_
     for (uint32_t i = threadIdx.x; i < acc.nact; i += blockDim.x) active[acc.base + i] = acc.act[i];
 }
 
-__global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(GraphView g, CandView c,
+__global__ void __launch_bounds__(kFinWarps * 32, 8) finalize_kernel(GraphView g, CandView c,
                                                                   uint32_t* active,
                                                                   IterCounters* ctr) {
     __shared__ uint32_t s_new[kFinWarps][kMaxCap];
@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(GraphView g, C
 
 // Bookkeeping only, for candidate lists supplied from outside (the
 // fixed-state local-join entry): same accounting as finalize.
-__global__ void __launch_bounds__(kFinWarps * 32) bookkeeping_kernel(GraphView g, CandView c,
+__global__ void __launch_bounds__(kFinWarps * 32, 8) bookkeeping_kernel(GraphView g, CandView c,
                                                                      uint32_t* active,
                                                                      IterCounters* ctr) {
     __shared__ BlockCounters acc;
