@@ -18,7 +18,8 @@ names = args or ["C1", "C2", "C3"]
 for name in names:
     cfg = datasets.CONFIGS[name]
     t = time.time(); data = datasets.generate(cfg); tg = time.time() - t
-    p = kg.RunParams(k=cfg.k, max_candidates=cfg.cap, seed=cfg.seed, profile=True, max_iterations=max_iter)
+    p = kg.RunParams(k=cfg.k, max_candidates=cfg.cap, seed=cfg.seed, profile=True, max_iterations=max_iter,
+                     reorder="--reorder" in sys.argv)
     if warm:
         kg.run(data[: min(len(data), 20000)], kg.RunParams(k=cfg.k, max_candidates=cfg.cap))
     t = time.time(); res = kg.run(data, p); wall = time.time() - t
