@@ -20,12 +20,12 @@ CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(PKG, "build")
 LIB = os.path.join(PKG, "lib", "libknng_cuda.so")
 DIAG = os.path.join(PKG, "lib", "libknng_diag.so")  # FFMA peak probe (bench only)
-SOURCES = ["graph_kernels.cu", "join.cu", "bruteforce.cu", "reorder.cu", "api.cu"]
+SOURCES = ["graph_kernels.cu", "join.cu", "join_tc.cu", "bruteforce.cu", "reorder.cu", "api.cu"]
 HEADERS = ["common.cuh", "kernels.cuh"]
 # join.cu: no FMA contraction anywhere, so the unfused (multiply, then add)
 # distance path stays unfused at the SASS level; explicit fma intrinsics are
 # unaffected (SURVEY.md §8a-6 bit-exactness)
-PER_FILE = {"join.cu": ["--fmad=false"]}
+PER_FILE = {"join.cu": ["--fmad=false"], "join_tc.cu": ["--fmad=false"]}
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
          "-I", os.path.join(ROOT, "include")]

@@ -12,6 +12,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -228,6 +229,13 @@ struct Engine {
     size_t rev_cap = 0, d_cap = 0;
     DevBuf<IterCounters> ctr;
     IterCounters* h_ctr = nullptr;
+    // tensor-core screened join (join_tc.cu): per-row norms for its bound,
+    // computed on first use and after the data is permuted
+    DevBuf<float> nrm2, nrmu;
+    DevBuf<uint4> ovf;           // its overflow list (nodes too large for its arena)
+    DevBuf<IterCounters> octr;   // and that list's counters
+    bool norms_valid = false;
+    uint32_t iteration = 0;  // the running iteration (1-based; 0 = fixed-state entry)
     uint64_t h2d = 0, d2h = 0;
 
     uint32_t lo = 0, hi = 0;  // owned rows (multi-GPU); [0, n) otherwise
@@ -343,6 +351,10 @@ struct Engine {
         timer.end(h);
         join_stages(timer, distances_only);
         read_counters();
+        if (h_ctr->screened && getenv("KNNG_TC_STATS"))
+            fprintf(stderr, "[knng] iteration %u screened join: %llu pairs, %llu exact (%.4f)\n",
+                    iteration, h_ctr->screened, h_ctr->survivors,
+                    double(h_ctr->survivors) / double(h_ctr->screened));
         if (h_ctr->overflow) {
             reserve_join(h_ctr->rev, h_ctr->dwords);
             CK(cudaMemsetAsync(&ctr.p->overflow, 0, sizeof(uint32_t), s));
@@ -357,7 +369,21 @@ struct Engine {
         launch_scatter_rev(cv(), active.p, ctr.p, n, n, s);
         timer.end(h);
         h = timer.begin(KNNG_CUDA_KERNEL_JOIN);
-        launch_join_distances(gv(), cv(), active.p, ctr.p, n, s);
+        if (use_screened_join(distances_only)) {
+            if (!norms_valid) {
+                if (!nrm2.p) {
+                    nrm2.alloc(n, pool, s);
+                    nrmu.alloc(n, pool, s);
+                    ovf.alloc(n, pool, s);
+                    octr.alloc(1, pool, s);
+                }
+                launch_row_norms(data.p, n, stride, nrm2.p, nrmu.p, s);
+                norms_valid = true;
+            }
+            launch_join_tc(gv(), cv(), ctr.p, n, nrm2.p, nrmu.p, ovf.p, octr.p, s);
+        } else {
+            launch_join_distances(gv(), cv(), active.p, ctr.p, n, s);
+        }
         timer.end(h);
         CK(cudaGetLastError());
         if (distances_only) return;
@@ -365,6 +391,19 @@ struct Engine {
         launch_join_merge(gv(), cv(), ctr.p, s);
         timer.end(h);
         CK(cudaGetLastError());
+    }
+
+    // The tensor-core screened join (join_tc.cu) is opt-in: KNNG_JOIN_TC=1
+    // runs it for every prefiltered join, =auto from iteration 2 on rows of
+    // >= 256 floats.  It needs the prefilter (it drops pairs that cannot beat
+    // an endpoint's row maximum).  Measured slower than the FP32 tile kernel
+    // on B200, so the default is off.
+    bool use_screened_join(bool distances_only) const {
+        if (distances_only || !filter) return false;
+        const char* v = getenv("KNNG_JOIN_TC");
+        if (!v || v[0] == '0') return false;
+        if (v[0] == '1') return true;
+        return iteration >= 2 && stride >= 256;  // "auto"
     }
 
     // ---- locality reorder (reorder.hpp:22-50, dataset.hpp:237-245,
@@ -403,6 +442,7 @@ struct Engine {
         data2.alloc(size_t(n) * stride, pool, s);
         launch_permute_rows(data.p, data2.p, sigma.p, n, stride, s);
         std::swap(data.p, data2.p);
+        norms_valid = false;
         remap_graph(sigma.p);
     }
 
@@ -480,6 +520,7 @@ void run_engine(Engine& e, const float* data, bool data_on_device, const knng_cu
     for (uint32_t iter = 1; iter <= p.max_iterations; ++iter) {
         t0 = now_s();
         const uint64_t iter_seed = master();
+        e.iteration = iter;
         CK(cudaMemsetAsync(e.ctr.p, 0, sizeof(IterCounters), e.s));
         e.select(iter_seed, timer);
         e.join(timer);  // ends with the iteration's counter read
@@ -1061,6 +1102,7 @@ int knng_cuda_shard_step(knng_cuda_shard* sh, uint64_t seed, uint64_t* out_count
         DeviceGuard dg(sh->device);
         Engine& e = *sh->e;
         KernelTimer timer(false, e.s, nullptr);
+        ++e.iteration;
         CK(cudaMemsetAsync(e.ctr.p, 0, sizeof(IterCounters), e.s));
         e.select(seed, timer);
         e.join(timer);  // local merges of the owned targets; ends with a counter read

@@ -60,6 +60,8 @@ struct IterCounters {
     uint32_t work;               // dynamic work counter
     uint32_t overflow;           // distance blocks exceed the buffer: join skipped
     uint32_t hubs;               // merge: targets left to the per-CTA hub merge
+    unsigned long long screened;   // screened join: pairs bounded
+    unsigned long long survivors;  // screened join: pairs evaluated exactly
 };
 
 // --- graph_kernels.cu ------------------------------------------------------
@@ -94,6 +96,17 @@ void launch_scatter_rev(const CandView& c, const uint32_t* active, IterCounters*
 // Distance stage of the local join: every active node's distance block.
 void launch_join_distances(const GraphView& g, const CandView& c, const uint32_t* active,
                            IterCounters* ctr, uint32_t max_active, cudaStream_t s);
+// --- join_tc.cu --------------------------------------------------------------
+// ||x||^2 (rounded down) and ||x|| (rounded up) of every data row.
+void launch_row_norms(const float* data, uint32_t n, uint32_t stride, float* nrm2, float* nrmu,
+                      cudaStream_t s);
+// Distance stage screened on the tensor cores: same proposal blocks as
+// launch_join_distances with the prefilter on (see join_tc.cu).  Nodes too
+// large for its shared-memory arena are listed in ovf (count in octr->active)
+// and run through launch_join_distances.
+void launch_join_tc(const GraphView& g, const CandView& c, IterCounters* ctr, uint32_t max_active,
+                    const float* nrm2, const float* nrmu, uint4* ovf, IterCounters* octr,
+                    cudaStream_t s);
 // Update stage: one warp per target pulls and merges its proposals.
 void launch_join_merge(const GraphView& g, const CandView& c, IterCounters* ctr,
                        cudaStream_t s);
