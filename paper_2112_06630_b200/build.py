@@ -20,7 +20,7 @@ CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(PKG, "build")
 LIB = os.path.join(PKG, "lib", "libknng_cuda.so")
 DIAG = os.path.join(PKG, "lib", "libknng_diag.so")  # FFMA peak probe (bench only)
-SOURCES = ["graph_kernels.cu", "join.cu", "join_tc.cu", "bruteforce.cu", "reorder.cu", "api.cu"]
+SOURCES = ["graph_kernels.cu", "join.cu", "join_tc.cu", "join_u8.cu", "bruteforce.cu", "reorder.cu", "api.cu"]
 HEADERS = ["common.cuh", "kernels.cuh"]
 # join.cu: no FMA contraction anywhere, so the unfused (multiply, then add)
 # distance path stays unfused at the SASS level; explicit fma intrinsics are

@@ -235,6 +235,12 @@ struct Engine {
     DevBuf<uint4> ovf;           // its overflow list (nodes too large for its arena)
     DevBuf<IterCounters> octr;   // and that list's counters
     bool norms_valid = false;
+    // byte-valued data (join_u8.cu): lane-major byte copy and lane norms,
+    // decided on first use and after the data is permuted
+    DevBuf<uint8_t> packed;
+    DevBuf<int32_t> lnorm;
+    DevBuf<uint32_t> u8_flag;
+    int u8_state = -1;  // -1 unknown, 0 not eligible, 1 packed
     uint32_t iteration = 0;  // the running iteration (1-based; 0 = fixed-state entry)
     uint64_t h2d = 0, d2h = 0;
 
@@ -369,7 +375,9 @@ struct Engine {
         launch_scatter_rev(cv(), active.p, ctr.p, n, n, s);
         timer.end(h);
         h = timer.begin(KNNG_CUDA_KERNEL_JOIN);
-        if (use_screened_join(distances_only)) {
+        if (use_u8_join()) {
+            launch_join_u8(gv(), cv(), ctr.p, n, packed.p, lnorm.p, s);
+        } else if (use_screened_join(distances_only)) {
             if (!norms_valid) {
                 if (!nrm2.p) {
                     nrm2.alloc(n, pool, s);
@@ -391,6 +399,25 @@ struct Engine {
         launch_join_merge(gv(), cv(), ctr.p, s);
         timer.end(h);
         CK(cudaGetLastError());
+    }
+
+    // Byte-valued data takes the integer tensor-core join (join_u8.cu,
+    // bit-identical); KNNG_JOIN_U8=0 forces the FP32 kernel (A/B).
+    bool use_u8_join() {
+        const char* v = getenv("KNNG_JOIN_U8");
+        if (v && v[0] == '0') return false;
+        if (u8_state < 0) {
+            if (!u8_flag.p) u8_flag.alloc(1, pool, s);
+            u8_state = u8_eligible(data.p, n, stride, u8_flag.p, s) ? 1 : 0;
+            if (u8_state == 1) {
+                if (!packed.p) {
+                    packed.alloc(size_t(n) * 8 * u8_lane_bytes(stride), pool, s);
+                    lnorm.alloc(size_t(n) * 8, pool, s);
+                }
+                launch_u8_pack(data.p, n, stride, packed.p, lnorm.p, s);
+            }
+        }
+        return u8_state == 1;
     }
 
     // The tensor-core screened join (join_tc.cu) is opt-in: KNNG_JOIN_TC=1
@@ -443,6 +470,7 @@ struct Engine {
         launch_permute_rows(data.p, data2.p, sigma.p, n, stride, s);
         std::swap(data.p, data2.p);
         norms_valid = false;
+        if (u8_state == 1) u8_state = -1;  // repack in the new row order
         remap_graph(sigma.p);
     }
 

@@ -107,6 +107,17 @@ void launch_row_norms(const float* data, uint32_t n, uint32_t stride, float* nrm
 void launch_join_tc(const GraphView& g, const CandView& c, IterCounters* ctr, uint32_t max_active,
                     const float* nrm2, const float* nrmu, uint4* ovf, IterCounters* octr,
                     cudaStream_t s);
+// --- join_u8.cu --------------------------------------------------------------
+// Byte-valued data (every coordinate an integer in [0, 255], stride / 8 <= 258):
+// the distance stage on the integer tensor cores, bit-identical to the FP32
+// tile kernel.  u8_eligible checks the data on the device (one host sync).
+uint32_t u8_lane_bytes(uint32_t stride);  // Kl: bytes per reference lane per row
+bool u8_eligible(const float* data, uint32_t n, uint32_t stride, uint32_t* d_flag,
+                 cudaStream_t s);
+void launch_u8_pack(const float* data, uint32_t n, uint32_t stride, uint8_t* packed,
+                    int32_t* lnorm, cudaStream_t s);
+void launch_join_u8(const GraphView& g, const CandView& c, IterCounters* ctr, uint32_t max_active,
+                    const uint8_t* packed, const int32_t* lnorm, cudaStream_t s);
 // Update stage: one warp per target pulls and merges its proposals.
 void launch_join_merge(const GraphView& g, const CandView& c, IterCounters* ctr,
                        cudaStream_t s);
