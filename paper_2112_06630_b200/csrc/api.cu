@@ -536,6 +536,7 @@ void run_engine(Engine& e, const float* data, bool data_on_device, const knng_cu
     e.upload(data, data_on_device);
     const uint64_t init_seed = master();
     int h = timer.begin(KNNG_CUDA_KERNEL_INIT);
+    e.use_u8_join();  // per-build data preparation (byte-valued data check + packing)
     launch_init_random(e.gv(), init_seed, e.s);
     timer.end(h);
     CK(cudaGetLastError());

@@ -12,7 +12,7 @@
 // and the reference's distance is the FP32 tree ((0+1)+(2+3))+((4+5)+(6+7))
 // of those lane sums.  This kernel forms the eight per-lane dot products with
 // mma.sync m16n8k32 u8 x u8 -> s32 on a lane-major byte copy of the data
-// (8 x Kl bytes per row, Kl = stride / 8 rounded up to 32), adds the per-lane
+// (8 x Kl bytes per row, Kl = stride / 8 rounded up to 64), adds the per-lane
 // squared norms, and applies the tree with __fadd_rn — every distance
 // bit-identical to the reference (tests/test_gpu_parity.py runs C2 through
 // this path; tests/test_gpu_u8.py compares it with the FP32 tile kernel).
@@ -34,6 +34,7 @@ constexpr uint32_t kUWarps = 8;                 // warps per CTA, one node each
 constexpr uint32_t kUMaxM = 2 * kMaxCap;
 
 struct U8Warp {
+    int32_t nrm[kUMaxM][8];   // per-lane squared norms of the node's candidates
     uint32_t rid[kUMaxM];     // combined index -> data row
     float rmx[kUMaxM];        // prefilter bound (row maximum), +inf when unfiltered
     uint32_t rowcnt[kUMaxM];  // proposals kept per candidate row
@@ -52,14 +53,16 @@ __device__ __forceinline__ size_t u8_prow(uint32_t r, uint32_t nn, uint32_t m) {
     return r < nn ? size_t(r) * m : size_t(nn) * m + size_t(r - nn) * (nn + 1);
 }
 
-// Byte-layout of one row: lane l occupies bytes [l Kl, (l + 1) Kl); inside a
-// lane, each 32-byte k-chunk is permuted so that MMA thread t's eight bytes
-// (k = 4t..4t+3 and 16+4t..16+4t+3 of the chunk) are contiguous at 8t: one
-// 8-byte load per fragment pair.  The permutation is the same for both MMA
-// operands, and integer dot products do not depend on the order of terms.
-__device__ __forceinline__ uint32_t u8_pos(uint32_t kk) {  // kk in [0, 32)
-    const uint32_t t = (kk & 15u) >> 2, h = kk >> 4, b = kk & 3u;
-    return 8 * t + 4 * h + b;
+// Byte-layout of one row: lane l occupies bytes [l Kl, (l + 1) Kl), Kl a
+// multiple of 64; inside a lane, each 64-byte pair of k-chunks is permuted so
+// that MMA thread t's sixteen bytes (k = 4t..4t+3 and 16+4t..16+4t+3 of both
+// chunks) are contiguous at 16t: one 16-byte load per row per chunk pair.  The
+// permutation is the same for both MMA operands, and integer dot products do
+// not depend on the order of terms.
+__device__ __forceinline__ uint32_t u8_pos(uint32_t kk) {  // kk in [0, 64)
+    const uint32_t ch = kk >> 5, k = kk & 31u;
+    const uint32_t t = (k & 15u) >> 2, h = k >> 4, b = k & 3u;
+    return 16 * t + 8 * ch + 4 * h + b;
 }
 
 // All coordinates integral in [0, 255]?  flag starts at 1; any miss clears it.
@@ -83,21 +86,29 @@ __global__ void u8_pack_kernel(const float* __restrict__ data, uint32_t n, uint3
     if (row >= n) return;
     const float* x = data + size_t(row) * stride;
     uint8_t* out = packed + size_t(row) * 8 * kl;
-    const uint32_t chunks = kl / 32;  // k-chunks per lane
+    const uint32_t groups = kl / 64;  // 64-byte chunk pairs per lane
     int32_t nrm = 0;                  // lane (lane & 7)'s partial norm
-    for (uint32_t w = lane; w < 8 * chunks; w += 32) {
-        const uint32_t l = w % 8, ch = w / 8;
-        uint8_t buf[32];
+    for (uint32_t w = lane; w < 8 * groups; w += 32) {
+        const uint32_t l = w % 8, gi = w / 8;
+        // byte p = 16 t + 8 ch + 4 h + b of the block holds k = 32 ch + 16 h + 4 t + b
+        uint32_t words[16];
 #pragma unroll
-        for (uint32_t kk = 0; kk < 32; ++kk) {
-            const uint32_t c = ch * 32 + kk, e = 8 * c + l;
-            const uint32_t v = e < stride ? uint32_t(x[e]) : 0u;
-            buf[u8_pos(kk)] = uint8_t(v);
-            nrm += int32_t(v * v);
+        for (uint32_t wi = 0; wi < 16; ++wi) {
+            const uint32_t t = wi / 4, ch = (wi % 4) / 2, h = wi % 2;
+            uint32_t v = 0;
+#pragma unroll
+            for (uint32_t b = 0; b < 4; ++b) {
+                const uint32_t e = 8 * (gi * 64 + 32 * ch + 16 * h + 4 * t + b) + l;
+                const uint32_t xv = e < stride ? uint32_t(x[e]) : 0u;
+                v |= xv << (8 * b);
+                nrm += int32_t(xv * xv);
+            }
+            words[wi] = v;
         }
-        uint4* dst = reinterpret_cast<uint4*>(out + l * kl + ch * 32);
-        dst[0] = *reinterpret_cast<const uint4*>(buf);
-        dst[1] = *reinterpret_cast<const uint4*>(buf + 16);
+        uint4* dst = reinterpret_cast<uint4*>(out + l * kl + gi * 64);
+#pragma unroll
+        for (uint32_t q = 0; q < 4; ++q)
+            dst[q] = make_uint4(words[4 * q], words[4 * q + 1], words[4 * q + 2], words[4 * q + 3]);
     }
     // lanes congruent mod 8 hold the same reference lane
     nrm += __shfl_xor_sync(0xffffffffu, nrm, 8);
@@ -105,19 +116,124 @@ __global__ void u8_pack_kernel(const float* __restrict__ data, uint32_t n, uint3
     if (lane < 8) lnorm[size_t(row) * 8 + lane] = nrm;
 }
 
-__global__ void __launch_bounds__(kUWarps * 32, 2) join_u8_kernel(GraphView g, CandView c,
+constexpr uint32_t kUNB = 2;  // column blocks per pass
+#ifndef KNNG_U8_MINB
+#define KNNG_U8_MINB 2  // CTAs per SM the register budget is sized for
+#endif
+
+// One 16-row block (mi) of new candidates against kUNB 8-column blocks from
+// njb: per reference lane l, the C k-chunks' fragments are all loaded before
+// the MMAs (the byte rows come from L2: latency, not bandwidth, bounds a
+// dependent load -> MMA chain), then the lane sums enter the FP32 tree; the
+// pairs' proposals are written at the end.
+template <uint32_t C2>
+__device__ __forceinline__ void tile_pairs(U8Warp& W, const uint8_t* __restrict__ packed,
+                                           uint32_t kl, uint32_t mi, uint32_t njb, uint32_t nn,
+                                           uint32_t m, uint32_t nnj, int filter, uint64_t* D) {
+    // C2 = 64-byte chunk pairs per lane (Kl / 64)
+    const uint32_t lane = threadIdx.x & 31u, gq = lane >> 2, t = lane & 3u;
+    const size_t row_bytes = size_t(8) * kl;
+    const uint32_t ra0 = 16 * mi + gq, ra1 = ra0 + 8;
+    const uint8_t* pa0 = packed + size_t(W.rid[ra0]) * row_bytes + 16 * t;
+    const uint8_t* pa1 = packed + size_t(W.rid[ra1]) * row_bytes + 16 * t;
+    const uint8_t* pb[kUNB];
+    uint32_t cb[kUNB];
+    bool live[kUNB];
+#pragma unroll
+    for (uint32_t q = 0; q < kUNB; ++q) {
+        live[q] = njb + q < nnj;
+        const uint32_t col = min(8 * (njb + q) + gq, kUMaxM - 1);
+        cb[q] = min(8 * (njb + q) + 2 * t, kUMaxM - 2);
+        pb[q] = packed + size_t(W.rid[live[q] ? col : 0]) * row_bytes + 16 * t;
+    }
+    // tree partials of the kUNB x 4 C elements (see the lane schedule below)
+    float part[kUNB][4][3];
+#pragma unroll
+    for (uint32_t l = 0; l < 8; ++l) {
+        uint4 A0[C2], A1[C2], B[kUNB][C2];
+#pragma unroll
+        for (uint32_t g2 = 0; g2 < C2; ++g2) {
+            const size_t o = size_t(l) * kl + 64 * g2;
+            A0[g2] = __ldg(reinterpret_cast<const uint4*>(pa0 + o));
+            A1[g2] = __ldg(reinterpret_cast<const uint4*>(pa1 + o));
+#pragma unroll
+            for (uint32_t q = 0; q < kUNB; ++q)
+                B[q][g2] = __ldg(reinterpret_cast<const uint4*>(pb[q] + o));
+        }
+        int acc[kUNB][4];
+#pragma unroll
+        for (uint32_t q = 0; q < kUNB; ++q)
+#pragma unroll
+            for (uint32_t r = 0; r < 4; ++r) acc[q][r] = 0;
+#pragma unroll
+        for (uint32_t g2 = 0; g2 < C2; ++g2)
+#pragma unroll
+            for (uint32_t q = 0; q < kUNB; ++q) {
+                mma_u8(acc[q], A0[g2].x, A1[g2].x, A0[g2].y, A1[g2].y, B[q][g2].x, B[q][g2].y);
+                mma_u8(acc[q], A0[g2].z, A1[g2].z, A0[g2].w, A1[g2].w, B[q][g2].z, B[q][g2].w);
+            }
+        // lane sums (exact integers < 2^24) into the reference's tree
+        // ((0+1)+(2+3))+((4+5)+(6+7)): p0 holds s0 / s01 / s4 / s45, p1 s2 / s6,
+        // p2 s0123; after lane 7 p0 is the distance
+        const int32_t a_n0 = W.nrm[ra0][l], a_n1 = W.nrm[ra1][l];
+#pragma unroll
+        for (uint32_t q = 0; q < kUNB; ++q) {
+            const int32_t b_n0 = W.nrm[cb[q]][l], b_n1 = W.nrm[cb[q] + 1][l];
+#pragma unroll
+            for (uint32_t r = 0; r < 4; ++r) {
+                const int32_t an = r < 2 ? a_n0 : a_n1;
+                const int32_t bn = (r & 1u) ? b_n1 : b_n0;
+                const float sl = float(an + bn - 2 * acc[q][r]);
+                float* p = part[q][r];
+                if (l == 0 || l == 4)
+                    p[0] = sl;
+                else if (l == 2 || l == 6)
+                    p[1] = sl;
+                else if (l == 1 || l == 5)
+                    p[0] = __fadd_rn(p[0], sl);
+                else if (l == 3)
+                    p[2] = __fadd_rn(p[0], __fadd_rn(p[1], sl));
+                else
+                    p[0] = __fadd_rn(p[2], __fadd_rn(p[0], __fadd_rn(p[1], sl)));
+            }
+        }
+    }
+#pragma unroll
+    for (uint32_t q = 0; q < kUNB; ++q) {
+        if (!live[q]) continue;
+#pragma unroll
+        for (uint32_t r = 0; r < 4; ++r) {
+            const uint32_t i = 16 * mi + gq + 8 * (r >> 1);
+            const uint32_t j = 8 * (njb + q) + 2 * t + (r & 1u);
+            if (i >= nn || j >= m || (j < nn && j <= i)) continue;
+            const uint32_t id_i = W.rid[i], id_j = W.rid[j];
+            // an id listed twice pairs with itself: try_insert ignores self
+            // (graph.hpp:116-129)
+            if (filter && id_i == id_j) continue;
+            const float dist = part[q][r][0];
+            if (dist < W.rmx[i]) {
+                const uint32_t pos = atomicAdd(&W.rowcnt[i], 1u);
+                D[u8_prow(i, nn, m) + 1 + pos] = pack_key(dist, id_j);
+            }
+            if (dist < W.rmx[j]) {
+                const uint32_t pos = atomicAdd(&W.rowcnt[j], 1u);
+                D[u8_prow(j, nn, m) + 1 + pos] = pack_key(dist, id_i);
+            }
+        }
+    }
+}
+
+template <uint32_t C>
+__global__ void __launch_bounds__(kUWarps * 32, KNNG_U8_MINB) join_u8_kernel(GraphView g, CandView c,
                                                                IterCounters* ctr,
                                                                const uint8_t* __restrict__ packed,
                                                                const int32_t* __restrict__ lnorm,
                                                                uint32_t kl) {
     __shared__ U8Warp shw[kUWarps];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
-    const uint32_t gq = lane >> 2, t = lane & 3u;
     U8Warp& W = shw[warp];
     if (ctr->overflow) return;
     const uint32_t n_active = ctr->active, cap = c.cap;
-    const size_t row_bytes = size_t(8) * kl;
-    const uint32_t chunks = kl / 32;
     for (;;) {
         uint32_t a = 0;
         if (lane == 0) a = atomicAdd(&ctr->work, 1u);
@@ -136,99 +252,19 @@ __global__ void __launch_bounds__(kUWarps * 32, 2) join_u8_kernel(GraphView g, C
         // padding rows of the last 16 / 8 blocks: any valid row (read, unused)
         for (uint32_t x = m + lane; x < kUMaxM; x += 32) W.rid[x] = W.rid[0];
         __syncwarp();
-        const uint32_t nmi = (nn + 15) / 16, nnj = (m + 7) / 8;
-        for (uint32_t mi = 0; mi < nmi; ++mi) {
-            const uint8_t* pa0 = packed + size_t(W.rid[16 * mi + gq]) * row_bytes + 8 * t;
-            const uint8_t* pa1 = packed + size_t(W.rid[16 * mi + gq + 8]) * row_bytes + 8 * t;
-            const int32_t* na0 = lnorm + size_t(W.rid[16 * mi + gq]) * 8;
-            const int32_t* na1 = lnorm + size_t(W.rid[16 * mi + gq + 8]) * 8;
-            // column blocks whose pairs all lie on or below the diagonal of
-            // the new x new triangle are skipped
-            for (uint32_t njb = 2 * mi; njb < nnj; njb += 4) {
-                const uint8_t* pb[4];
-                const int32_t* nb0[4];
-                const int32_t* nb1[4];
-#pragma unroll
-                for (uint32_t q = 0; q < 4; ++q) {
-                    const uint32_t col = min(8 * (njb + q) + gq, kUMaxM - 1);
-                    const uint32_t cn = min(8 * (njb + q) + 2 * t, kUMaxM - 2);
-                    pb[q] = packed + size_t(W.rid[col]) * row_bytes + 8 * t;
-                    nb0[q] = lnorm + size_t(W.rid[cn]) * 8;
-                    nb1[q] = lnorm + size_t(W.rid[cn + 1]) * 8;
-                }
-                // tree partials of the 4 x 4 C elements: s01/s45 after odd
-                // lanes, s0123 after lane 3
-                float part[4][4][3];
-#pragma unroll
-                for (uint32_t l = 0; l < 8; ++l) {
-                    int acc[4][4];
-#pragma unroll
-                    for (uint32_t q = 0; q < 4; ++q)
-#pragma unroll
-                        for (uint32_t r = 0; r < 4; ++r) acc[q][r] = 0;
-                    for (uint32_t ch = 0; ch < chunks; ++ch) {
-                        const size_t o = size_t(l) * kl + 32 * ch;
-                        const uint2 A0 = __ldg(reinterpret_cast<const uint2*>(pa0 + o));
-                        const uint2 A1 = __ldg(reinterpret_cast<const uint2*>(pa1 + o));
-#pragma unroll
-                        for (uint32_t q = 0; q < 4; ++q) {
-                            if (njb + q < nnj) {
-                                const uint2 B = __ldg(reinterpret_cast<const uint2*>(pb[q] + o));
-                                mma_u8(acc[q], A0.x, A1.x, A0.y, A1.y, B.x, B.y);
-                            }
-                        }
-                    }
-                    // lane sums (exact integers < 2^24) into the tree
-                    const int32_t a_n0 = __ldg(na0 + l), a_n1 = __ldg(na1 + l);
-#pragma unroll
-                    for (uint32_t q = 0; q < 4; ++q) {
-                        if (njb + q >= nnj) continue;
-                        const int32_t b_n0 = __ldg(nb0[q] + l);  // column 2t
-                        const int32_t b_n1 = __ldg(nb1[q] + l);  // column 2t + 1
-#pragma unroll
-                        for (uint32_t r = 0; r < 4; ++r) {
-                            const int32_t an = r < 2 ? a_n0 : a_n1;
-                            const int32_t bn = (r & 1u) ? b_n1 : b_n0;
-                            const float s = float(an + bn - 2 * acc[q][r]);
-                            float* p = part[q][r];
-                            if (l == 0 || l == 2 || l == 4 || l == 6) {
-                                p[l == 2 || l == 6 ? 1 : 0] = s;
-                            } else if (l == 1 || l == 5) {
-                                p[0] = __fadd_rn(p[0], s);  // (0+1) / (4+5)
-                            } else if (l == 3) {
-                                p[2] = __fadd_rn(p[0], __fadd_rn(p[1], s));  // (0+1)+(2+3)
-                            } else {  // l == 7
-                                p[0] = __fadd_rn(p[2], __fadd_rn(p[0], __fadd_rn(p[1], s)));
-                            }
-                        }
-                    }
-                }
-                // proposals of the 4 x 4 C elements
-#pragma unroll
-                for (uint32_t q = 0; q < 4; ++q) {
-                    if (njb + q >= nnj) continue;
-#pragma unroll
-                    for (uint32_t r = 0; r < 4; ++r) {
-                        const uint32_t i = 16 * mi + gq + 8 * (r >> 1);
-                        const uint32_t j = 8 * (njb + q) + 2 * t + (r & 1u);
-                        if (i >= nn || j >= m || (j < nn && j <= i)) continue;
-                        const uint32_t id_i = W.rid[i], id_j = W.rid[j];
-                        // an id listed twice pairs with itself: try_insert
-                        // ignores self (graph.hpp:116-129)
-                        if (c.filter && id_i == id_j) continue;
-                        const float dist = part[q][r][0];
-                        if (dist < W.rmx[i]) {
-                            const uint32_t pos = atomicAdd(&W.rowcnt[i], 1u);
-                            D[u8_prow(i, nn, m) + 1 + pos] = pack_key(dist, id_j);
-                        }
-                        if (dist < W.rmx[j]) {
-                            const uint32_t pos = atomicAdd(&W.rowcnt[j], 1u);
-                            D[u8_prow(j, nn, m) + 1 + pos] = pack_key(dist, id_i);
-                        }
-                    }
-                }
-            }
+        // the candidates' lane norms (32 bytes each), 4 threads per row
+        for (uint32_t q = lane; q < 4 * kUMaxM; q += 32) {
+            const uint2 v = __ldg(reinterpret_cast<const uint2*>(lnorm + size_t(W.rid[q >> 2]) * 8) +
+                                  (q & 3u));
+            W.nrm[q >> 2][2 * (q & 3u)] = int32_t(v.x);
+            W.nrm[q >> 2][2 * (q & 3u) + 1] = int32_t(v.y);
         }
+        __syncwarp();
+        const uint32_t nmi = (nn + 15) / 16, nnj = (m + 7) / 8;
+        for (uint32_t mi = 0; mi < nmi; ++mi)
+            // column blocks left of the diagonal block hold only pairs j <= i
+            for (uint32_t njb = 2 * mi; njb < nnj; njb += kUNB)
+                tile_pairs<C>(W, packed, kl, mi, njb, nn, m, nnj, c.filter, D);
         __syncwarp();
         for (uint32_t x = lane; x < m; x += 32) D[u8_prow(x, nn, m)] = W.rowcnt[x];
         __syncwarp();
@@ -248,7 +284,7 @@ uint32_t u8_sm_count() {
 
 }  // namespace
 
-uint32_t u8_lane_bytes(uint32_t stride) { return (stride / 8 + 31) / 32 * 32; }
+uint32_t u8_lane_bytes(uint32_t stride) { return (stride / 8 + 63) / 64 * 64; }
 
 bool u8_eligible(const float* data, uint32_t n, uint32_t stride, uint32_t* d_flag,
                  cudaStream_t s) {
@@ -272,18 +308,29 @@ void launch_u8_pack(const float* data, uint32_t n, uint32_t stride, uint8_t* pac
 void launch_join_u8(const GraphView& g, const CandView& c, IterCounters* ctr, uint32_t max_active,
                     const uint8_t* packed, const int32_t* lnorm, cudaStream_t s) {
     if (!max_active) return;
+    const uint32_t kl = u8_lane_bytes(g.stride);
     static int per_sm = 0;
     if (!per_sm) {
         int v = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, join_u8_kernel, int(kUWarps * 32), 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, join_u8_kernel<2>, int(kUWarps * 32), 0);
         per_sm = v < 1 ? 1 : v;
     }
     uint32_t grid = u8_sm_count() * uint32_t(per_sm);
     const uint32_t need = (max_active + kUWarps - 1) / kUWarps;
     if (grid > need) grid = need;
     cudaMemsetAsync(&ctr->work, 0, sizeof(uint32_t), s);
-    join_u8_kernel<<<grid, kUWarps * 32, 0, s>>>(g, c, ctr, packed, lnorm,
-                                                 u8_lane_bytes(g.stride));
+#define KNNG_U8_CASE(CH)                                                                   \
+    case CH:                                                                               \
+        join_u8_kernel<CH><<<grid, kUWarps * 32, 0, s>>>(g, c, ctr, packed, lnorm, kl);  \
+        break;
+    switch (kl / 64) {
+        KNNG_U8_CASE(1)
+        KNNG_U8_CASE(2)
+        KNNG_U8_CASE(3)
+        KNNG_U8_CASE(4)
+        default: join_u8_kernel<5><<<grid, kUWarps * 32, 0, s>>>(g, c, ctr, packed, lnorm, kl);
+    }
+#undef KNNG_U8_CASE
 }
 
 }  // namespace knng_cuda
