@@ -113,6 +113,109 @@ def ffma_peak_tflops(device: int):
     return max(t.value, t2.value)
 
 
+def imma_peak_tops(device: int):
+    """Measured legacy integer MMA peak (mma.sync m16n8k32 u8, TOPS)."""
+    import ctypes as C
+    path = os.path.join(ROOT, "paper_2112_06630_b200", "lib", "libknng_diag.so")
+    if not os.path.exists(path):
+        return None
+    lib = C.CDLL(path)
+    t = C.c_double(0)
+    if not hasattr(lib, "knng_diag_imma_peak") or lib.knng_diag_imma_peak(device, C.byref(t)) != 0:
+        return None
+    return t.value
+
+
+def byte_valued(data) -> bool:
+    """Does the build take the byte-valued join (csrc/join_u8.cu)?  Same rule
+    as the library: every coordinate an integer in [0, 255], stride / 8 <= 258,
+    and KNNG_JOIN_U8 not set to 0."""
+    if os.environ.get("KNNG_JOIN_U8", "1").startswith("0"):
+        return False
+    stride = (data.shape[1] + 7) // 8 * 8
+    return bool(stride // 8 <= 258 and np.all((data >= 0) & (data <= 255) & (data == np.rint(data))))
+
+
+def u8_roofline(mets, n, d, k, imma_tops, fp32_tflops, config):
+    """Roofline of the byte-valued join kernel (join_u8_kernel).
+
+    Per launch: Q = sum_u (nn_u + no_u) * (8 Kl + 32 + 8) + 12 n k bytes (the
+    byte rows with Kl = ceil64(stride / 8) bytes per reference lane, the 8
+    lane norms, id and row maximum per listed candidate, the graph) and
+    F = evals * 2 d integer ops (the per-lane dot products); t* =
+    max(F / pi_imma, Q / beta_hbm), frac = sum(t*) / sum(t).  The byte copy
+    of C2 (70 MB) is L2-resident, so the HBM bound is conservative; ncu's L1
+    throughput is the limiter (profiles/README.md).
+    """
+    stride = (d + 7) // 8 * 8
+    kl = (stride // 8 + 63) // 64 * 64
+    beta, beta_src = 6650.0, "fallback 6650 GB/s (B200_PROFILING.md)"
+    mp = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(mp):
+        beta = float(json.load(open(mp))["hbm_gbs"])
+        beta_src = "MEASURED_PEAKS.json hbm_gbs (measured)"
+    pi = imma_tops or 500.0
+    pi_src = ("measured mma.sync m16n8k32 u8 microbenchmark (libknng_diag), this box" if imma_tops
+              else "fallback 500 TOPS")
+    F = Q = t = t_star = t_int = t_hbm = E = 0.0
+    launches = 0
+    for m in mets:
+        for it in m.iterations[1:]:
+            if it.join_ms <= 0:
+                continue
+            f = it.dist_evals * 2.0 * d
+            q = it.join_candidates * (8 * kl + 32 + 8) + 12.0 * n * k
+            ti, th = f / (pi * 1e12), q / (beta * 1e9)
+            F += f
+            Q += q
+            E += it.dist_evals
+            t += it.join_ms * 1e-3
+            t_int += ti
+            t_hbm += th
+            t_star += max(ti, th)
+            launches += 1
+    frac = t_star / t if t else 0.0
+    traffic, traffic_note = _traffic(config)
+    if t_int >= t_hbm:
+        roof = {"bound": "tensor", "achieved": round(frac * pi, 2), "peak": round(pi, 1),
+                "unit": "TOPS (int8)", "peak_source": pi_src}
+    else:
+        roof = {"bound": "hbm", "achieved": round(frac * beta, 1), "peak": beta, "unit": "GB/s",
+                "peak_source": beta_src}
+    roof.update({
+        "frac": round(frac, 4), "traffic": traffic, "traffic_note": traffic_note,
+        "kernel": "join_u8_kernel (local-join distance stage, byte-valued data: per-lane integer "
+                  "dot products on the tensor cores, bit-identical to the reference)",
+        "frac_definition": "sum over launches of max(F_int/pi_imma, Q/beta) / sum of launch times",
+        "gather_gbs_achieved": round(Q / t / 1e9, 1) if t else None,
+        "int_tops_achieved": round(F / t / 1e12, 2) if t else None,
+        "fp32_equiv_tflops_achieved": round(E * (3 * d - 1) / t / 1e12, 2) if t else None,
+        "fp32_peak_tflops": round(fp32_tflops, 2) if fp32_tflops else None,
+        "algorithmic_int_ops_per_launch": int(F / max(1, launches)),
+        "algorithmic_bytes_per_launch": int(Q / max(1, launches)),
+        "avg_launch_ms": round(t * 1e3 / max(1, launches), 4),
+        "launches": launches, "imma_peak_tops": round(pi, 1), "hbm_peak_gbs": beta,
+    })
+    return roof
+
+
+def _traffic(config):
+    traffic = traffic_note = None
+    if os.path.exists(PROFILE_TRAFFIC):
+        try:
+            tr = json.load(open(PROFILE_TRAFFIC)).get(config)
+            if isinstance(tr, dict):
+                traffic = tr.get("bytes_per_launch")
+                traffic_note = (f"ncu dram bytes of the {tr.get('launch')} launch of "
+                                f"{tr.get('kernel', 'the join')}; algorithmic bytes of that launch "
+                                f"{tr.get('algorithmic_bytes_same_launch'):.4g} ({tr.get('source')})")
+            else:
+                traffic = tr
+        except (OSError, ValueError, TypeError):
+            traffic = None
+    return traffic, traffic_note
+
+
 def join_roofline(mets, n, d, k, peak_tflops, config):
     """Roofline of the local-join distance kernel (join_distances_kernel).
 
@@ -149,19 +252,7 @@ def join_roofline(mets, n, d, k, peak_tflops, config):
             t_hbm += th
             t_star += max(tf, th)
             launches += 1
-    traffic = traffic_note = None
-    if os.path.exists(PROFILE_TRAFFIC):
-        try:
-            tr = json.load(open(PROFILE_TRAFFIC)).get(config)
-            if isinstance(tr, dict):
-                traffic = tr.get("bytes_per_launch")
-                traffic_note = (f"ncu dram bytes of the {tr.get('launch')} launch; algorithmic "
-                                f"bytes of that launch {tr.get('algorithmic_bytes_same_launch'):.4g}"
-                                f" ({tr.get('source')})")
-            else:
-                traffic = tr
-        except (OSError, ValueError, TypeError):
-            traffic = None
+    traffic, traffic_note = _traffic(config)
     frac = t_star / t if t else 0.0
     if t_fp >= t_hbm:
         roof = {"bound": "fp32", "achieved": round(frac * pi, 3), "peak": round(pi, 2),
@@ -311,6 +402,8 @@ def run_ours(args, rank, world, local):
     params = kg.RunParams(k=k, max_candidates=cap, termination_delta=cfg.delta, seed=cfg_r.seed,
                           device=local, profile=True)
     peak = ffma_peak_tflops(local)
+    u8 = byte_valued(data)
+    ipeak = imma_peak_tops(local) if u8 else None
 
     d_data = torch.from_numpy(data).to(f"cuda:{local}")
     d_ids = torch.empty((n, k), dtype=torch.int32, device=f"cuda:{local}")
@@ -383,7 +476,8 @@ def run_ours(args, rank, world, local):
 
     out = None
     if rank == 0:
-        roof = join_roofline(mets, n, d, k, peak, args.config)
+        roof = (u8_roofline(mets, n, d, k, ipeak, peak, args.config) if u8
+                else join_roofline(mets, n, d, k, peak, args.config))
         roof["share_of_step"] = round(join_ms / ms, 3)
 
         # matched recall on a node sample vs the reference (same data, same seed)
