@@ -1069,6 +1069,7 @@ int knng_cuda_shard_create(const float* d_data, uint32_t n, uint32_t d,
             e.lo = std::min(n, rank * sh->chunk);
             e.hi = std::min(n, (rank + 1) * sh->chunk);
             e.upload(d_data, true);
+            e.u8_state = 0;  // the sharded path keeps the FP32 join kernel
             sh->exp_counts.alloc(n, e.pool, e.s);
             sh->exp_off.alloc(n, e.pool, e.s);
             sh->rcnt.alloc(n, e.pool, e.s);

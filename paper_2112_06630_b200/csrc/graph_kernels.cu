@@ -27,7 +27,10 @@ __device__ __forceinline__ uint32_t full_mask_k(uint32_t k) {
 // eight strided lanes, UNFUSED square-accumulate, tree
 // ((0+1)+(2+3))+((4+5)+(6+7)).  Called by a full warp; the 8-lane group g
 // (lanes 8g..8g+7) evaluates the pair (a_row, b_row) of its choosing and every
-// lane of the group returns the distance.
+// lane of the group returns the distance.  (Thread-per-pair versions — 16-byte
+// float loads, or dp4a over the byte copy of byte-valued data — were 1.2-1.5x
+// slower: each load touches 16 bytes of a row where a group's touches a whole
+// 32-byte sector.)
 __device__ __forceinline__ float group8_l2_scalar(const float* __restrict__ a,
                                                   const float* __restrict__ b, uint32_t stride,
                                                   bool active) {
@@ -45,7 +48,6 @@ __device__ __forceinline__ float group8_l2_scalar(const float* __restrict__ a,
     return acc;
 }
 
-// One warp per node: k distinct uniform ids != u, true distances, sorted row.
 __global__ void __launch_bounds__(256) init_random_kernel(GraphView g, uint32_t seed_lo,
                                                           uint32_t seed_hi) {
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -72,8 +74,8 @@ __global__ void __launch_bounds__(256) init_random_kernel(GraphView g, uint32_t 
         if (__all_sync(0xffffffffu, accepted)) break;
     }
     // distances: four pairs per pass, one per 8-lane group
-    const float* ru = g.data + size_t(u) * g.stride;
     float mine = 0.0f;
+    const float* ru = g.data + size_t(u) * g.stride;
     for (uint32_t e = 0; e < k; e += 4) {
         const uint32_t pair = e + (lane >> 3);
         const uint32_t v = __shfl_sync(0xffffffffu, id, pair & 31u);

@@ -58,12 +58,7 @@ __device__ __forceinline__ size_t u8_prow(uint32_t r, uint32_t nn, uint32_t m) {
 // that MMA thread t's sixteen bytes (k = 4t..4t+3 and 16+4t..16+4t+3 of both
 // chunks) are contiguous at 16t: one 16-byte load per row per chunk pair.  The
 // permutation is the same for both MMA operands, and integer dot products do
-// not depend on the order of terms.
-__device__ __forceinline__ uint32_t u8_pos(uint32_t kk) {  // kk in [0, 64)
-    const uint32_t ch = kk >> 5, k = kk & 31u;
-    const uint32_t t = (k & 15u) >> 2, h = k >> 4, b = k & 3u;
-    return 16 * t + 8 * ch + 4 * h + b;
-}
+// not depend on the order of terms (u8_pack_kernel writes it).
 
 // All coordinates integral in [0, 255]?  flag starts at 1; any miss clears it.
 __global__ void u8_check_kernel(const float* __restrict__ data, size_t count, uint32_t* flag) {

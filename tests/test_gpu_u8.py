@@ -82,3 +82,19 @@ def test_u8_build_matches_fp32_build(gpu, monkeypatch):
     ex, _ = kg.brute_force_knng(data, 20)
     r0, r1 = kg.recall(res["0"].graph.ids, ex), kg.recall(res["1"].graph.ids, ex)
     assert abs(r0 - r1) <= 0.005, (r0, r1)
+
+
+@pytest.mark.parametrize("kind,d", [("C2", 784), ("U8", 100), ("U8", 24)])
+def test_u8_init_distances_bit_exact(gpu, restated, kind, d):
+    """init_random's distances from the integer lane sums equal the reference's
+    scalar l2_sq on the padded rows (graph.hpp:60), bit for bit."""
+    data = make_data("C2", 1500) if kind == "C2" else u8_data(1500, d, 9)
+    g, _, ev = kg.init_random(data, 10, 5)
+    n = data.shape[0]
+    stride = (data.shape[1] + 7) // 8 * 8
+    pdata = np.zeros((n, stride), np.float32)
+    pdata[:, :data.shape[1]] = data
+    for u in range(0, n, 29):
+        for i in range(10):
+            want = restated.l2_sq(pdata[u], pdata[g.ids[u, i]])
+            assert np.float32(g.dists[u, i]).view(np.uint32) == np.float32(want).view(np.uint32)
