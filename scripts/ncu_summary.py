@@ -13,6 +13,9 @@ METRICS = [
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
     "lts__t_sector_hit_rate.pct", "launch__registers_per_thread",
     "launch__occupancy_limit_registers", "launch__grid_size",
+    "l1tex__throughput.avg.pct_of_peak_sustained_active", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+    "l1tex__t_sector_hit_rate.pct", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
 ]
 rep = sys.argv[1]
 rows = list(csv.reader(subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"],
