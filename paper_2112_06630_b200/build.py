@@ -20,6 +20,7 @@ CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(PKG, "build")
 LIB = os.path.join(PKG, "lib", "libknng_cuda.so")
 DIAG = os.path.join(PKG, "lib", "libknng_diag.so")  # FFMA peak probe (bench only)
+CLI = os.path.join(ROOT, "proj", "tools", "build", "knng_cuda_cli")  # build / recall front end
 SOURCES = ["graph_kernels.cu", "join.cu", "join_tc.cu", "join_u8.cu", "bruteforce.cu", "reorder.cu", "api.cu"]
 HEADERS = ["common.cuh", "kernels.cuh"]
 # join.cu: no FMA contraction anywhere, so the unfused (multiply, then add)
@@ -64,6 +65,15 @@ def build(verbose: bool = False, force: bool = False) -> str:
         cmd = [nvcc(), *ARCH, "-shared", "-o", LIB, *objs, "-cudart", "static"]
         if verbose:
             print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+    # the CLI front end (proj/tools), against the C-ABI only
+    cli_src = os.path.join(ROOT, "proj", "tools", "knng_cuda_cli.cpp")
+    if force or _stale(CLI, [cli_src, LIB, os.path.join(ROOT, "include", "knng_cuda.h")]):
+        os.makedirs(os.path.dirname(CLI), exist_ok=True)
+        cmd = ["g++", "-std=c++17", "-O2", "-I", os.path.join(ROOT, "include"), "-o", CLI, cli_src,
+               "-L", os.path.dirname(LIB), "-lknng_cuda",
+               "-Wl,-rpath," + os.path.relpath(os.path.dirname(LIB), os.path.dirname(CLI)).join(
+                   ["$ORIGIN/", ""])]
         subprocess.run(cmd, check=True)
     diag_src = os.path.join(CSRC, "diag.cu")
     if force or _stale(DIAG, [diag_src]):

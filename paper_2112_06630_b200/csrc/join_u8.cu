@@ -247,8 +247,10 @@ __global__ void __launch_bounds__(kUWarps * 32, KNNG_U8_MINB) join_u8_kernel(Gra
         // padding rows of the last 16 / 8 blocks: any valid row (read, unused)
         for (uint32_t x = m + lane; x < kUMaxM; x += 32) W.rid[x] = W.rid[0];
         __syncwarp();
-        // the candidates' lane norms (32 bytes each), 4 threads per row
-        for (uint32_t q = lane; q < 4 * kUMaxM; q += 32) {
+        // the lane norms (32 bytes each, 4 threads per row) of the rows the
+        // tiles read: the candidates and the padding of the last blocks
+        const uint32_t rows = max(16 * ((nn + 15) / 16), 8 * ((m + 7) / 8));
+        for (uint32_t q = lane; q < 4 * rows; q += 32) {
             const uint2 v = __ldg(reinterpret_cast<const uint2*>(lnorm + size_t(W.rid[q >> 2]) * 8) +
                                   (q & 3u));
             W.nrm[q >> 2][2 * (q & 3u)] = int32_t(v.x);
