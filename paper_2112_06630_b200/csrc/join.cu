@@ -769,6 +769,10 @@ constexpr uint32_t kMergeWarps = 8;
 #define KNNG_MERGE_META 2
 #endif
 constexpr uint32_t kMergeMeta = KNNG_MERGE_META;  // reverse-index chunks per metadata round trip
+#ifndef KNNG_MERGE_DEPTH
+#define KNNG_MERGE_DEPTH 1
+#endif
+constexpr uint32_t kMergeDepth = KNNG_MERGE_DEPTH;  // proposal steps fetched ahead
 
 // Merges the proposals of t's reverse-index entries rv[0, cnt) into the row
 // held by the calling warp (lane i = entry i).  `fresh` tracks which entries
@@ -836,10 +840,17 @@ __device__ __forceinline__ void merge_entries(const CandView& c, const uint64_t*
                 }
                 return st;
             };
-            Step cur = fetch(0);
+            // kMergeDepth steps of proposals in flight
+            Step ring[kMergeDepth];
+#pragma unroll
+            for (uint32_t q = 0; q < kMergeDepth; ++q)
+                ring[q] = 32 * q < total ? fetch(32 * q) : Step{0.0f, 0u, false};
             for (uint32_t f0 = 0; f0 < total; f0 += 32) {
-                Step nxt{0.0f, 0u, false};
-                if (f0 + 32 < total) nxt = fetch(f0 + 32);
+                const Step cur = ring[0];
+#pragma unroll
+                for (uint32_t q = 0; q + 1 < kMergeDepth; ++q) ring[q] = ring[q + 1];
+                ring[kMergeDepth - 1] = f0 + 32 * kMergeDepth < total ? fetch(f0 + 32 * kMergeDepth)
+                                                                     : Step{0.0f, 0u, false};
                 uint32_t pass = __ballot_sync(0xffffffffu, cur.valid && cur.dist < cur_max);
                 while (pass) {
                     const uint32_t src = __ffs(pass) - 1u;
@@ -851,7 +862,6 @@ __device__ __forceinline__ void merge_entries(const CandView& c, const uint64_t*
                         cur_max = key_dist(__shfl_sync(0xffffffffu, key, k - 1));
                     }
                 }
-                cur = nxt;
             }
         }
     }
