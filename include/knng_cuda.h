@@ -65,6 +65,8 @@ typedef struct knng_cuda_params {
     uint64_t seed;                     /* default 0 */
     int32_t device;                    /* CUDA device ordinal, default 0 */
     int32_t profile;                   /* 1: time each kernel with CUDA events */
+    int32_t deterministic;             /* 1: seed-deterministic build (order-independent
+                                          sampling and merges; default 0) */
 } knng_cuda_params;
 
 /* knng::IterationMetrics (descent.hpp:38-43).  `changes` counts successful

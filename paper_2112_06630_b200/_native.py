@@ -74,6 +74,7 @@ class Params(C.Structure):
         ("seed", C.c_uint64),
         ("device", C.c_int32),
         ("profile", C.c_int32),
+        ("deterministic", C.c_int32),
     ]
 
 

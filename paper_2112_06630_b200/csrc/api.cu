@@ -226,6 +226,8 @@ struct Engine {
     DevBuf<uint64_t> rev;
     DevBuf<uint64_t> dblocks;
     int filter = 1;  // join proposals prefiltered by the row maxima (0: keep all)
+    bool det = false;            // deterministic mode (CandView::det)
+    DevBuf<uint32_t> rawlist;    // its raw sampled lists, n x 4 cap
     size_t rev_cap = 0, d_cap = 0;
     DevBuf<IterCounters> ctr;
     IterCounters* h_ctr = nullptr;
@@ -296,7 +298,7 @@ struct Engine {
     CandView cv() const {
         return CandView{cap,   cand.p,   raw_new.p, raw_old.p, nc.p, oc.p, dsz.p,
                         doff.p, revcnt.p, roff.p,   rcur.p,    rev.p, dblocks.p, filter,
-                        cmax.p, arec.p, hubs.p};
+                        cmax.p, arec.p, hubs.p, rawlist.p, det ? 1 : 0};
     }
 
     void reserve_join(uint64_t rev_entries, uint64_t dwords) {
@@ -341,7 +343,7 @@ struct Engine {
         launch_sample(g, c, indeg.p, seed, s);
         timer.end(h);
         h = timer.begin(KNNG_CUDA_KERNEL_FINALIZE);
-        launch_finalize(g, c, active.p, ctr.p, s);
+        launch_finalize(g, c, active.p, ctr.p, s, seed);
         timer.end(h);
         CK(cudaGetLastError());
     }
@@ -531,6 +533,10 @@ void run_engine(Engine& e, const float* data, bool data_on_device, const knng_cu
                 uint32_t* d_sigma = nullptr) {
     KernelTimer timer(p.profile != 0, e.s, m);
     bool reordered = false;
+    if (p.deterministic && !e.det) {
+        e.det = true;
+        e.rawlist.alloc(size_t(e.n) * 4 * e.cap, e.pool, e.s);
+    }
     std::mt19937_64 master(p.seed);
     double t0 = now_s();
     e.upload(data, data_on_device);
@@ -639,6 +645,7 @@ void knng_cuda_params_default(knng_cuda_params* p) {
     p->seed = 0;
     p->device = 0;
     p->profile = 0;
+    p->deterministic = 0;
 }
 
 const char* knng_cuda_last_error(void) { return g_err.c_str(); }

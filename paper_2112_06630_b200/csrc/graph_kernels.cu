@@ -18,6 +18,7 @@ namespace {
 
 constexpr uint32_t kSaltInit = 0x494e4954u;    // "INIT"
 constexpr uint32_t kSaltSample = 0x53414d50u;  // "SAMP"
+constexpr uint32_t kSaltDet = 0x44455457u;     // "DETW"
 
 __device__ __forceinline__ uint32_t full_mask_k(uint32_t k) {
     return k >= 32 ? 0xffffffffu : ((1u << k) - 1u);
@@ -161,6 +162,13 @@ __device__ __forceinline__ void offer(const CandView& c, uint32_t k, const uint3
     if (deg > c.cap && uint64_t(r_accept) * deg >= (uint64_t(c.cap) << 32)) return;
     uint32_t* counter = is_new ? c.raw_new : c.raw_old;
     const uint32_t slot = atomicAdd(counter + target, 1u);
+    if (c.det) {
+        // every accepted offer (the expected count is <= cap; 2 cap slots),
+        // kept or cut by finalize on its pair weight, not on arrival order
+        if (slot < 2 * c.cap)
+            c.raw[size_t(target) * 4 * c.cap + (is_new ? 0u : 2 * c.cap) + slot] = cand;
+        return;
+    }
     uint32_t* list = c.ids + size_t(target) * 2 * c.cap + (is_new ? 0u : c.cap);
     if (slot < c.cap) {
         list[slot] = cand;
@@ -361,6 +369,198 @@ __global__ void __launch_bounds__(kFinWarps * 32, 8) finalize_kernel(GraphView g
     flush_block_counters(acc, active, ctr);
 }
 
+// ---- deterministic mode ---------------------------------------------------
+
+// Bitonic sort of 32 E keys, E per lane (element E lane + r), ascending.
+template <uint32_t E, typename T>
+__device__ __forceinline__ void warp_sort(T (&v)[E]) {
+    const uint32_t lane = lane_id();
+#pragma unroll
+    for (uint32_t size = 2; size <= 32 * E; size <<= 1) {
+#pragma unroll
+        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+            if (stride >= E) {
+#pragma unroll
+                for (uint32_t r = 0; r < E; ++r) {
+                    const uint32_t i = E * lane + r;
+                    const T o = __shfl_xor_sync(0xffffffffu, v[r], stride / E);
+                    const bool asc = (i & size) == 0, lower = (i & stride) == 0;
+                    const T lo = v[r] < o ? v[r] : o, hi = v[r] < o ? o : v[r];
+                    v[r] = (asc == lower) ? lo : hi;
+                }
+            } else {
+#pragma unroll
+                for (uint32_t r = 0; r < E; ++r) {
+                    if (r & stride) continue;
+                    const uint32_t i = E * lane + r;
+                    const bool asc = (i & size) == 0;
+                    const T a = v[r], b = v[r | stride];
+                    if (asc ? (b < a) : (a < b)) {
+                        v[r] = b;
+                        v[r | stride] = a;
+                    }
+                }
+            }
+        }
+    }
+}
+
+// Pair weight of candidate x offered to u in list `kind` (order-free).
+__device__ __forceinline__ uint32_t det_weight(uint32_t u, uint32_t x, uint32_t kind,
+                                               uint32_t seed_lo, uint32_t seed_hi) {
+    return philox4x32_10(u, x, kind, kSaltDet, seed_lo, seed_hi).x;
+}
+
+// finalize for deterministic mode, one node: both raw lists sorted by id and
+// deduplicated; an id in both lists stays where the reference's first offer
+// would put it (forward edge u -> x iff u < x, selection.hpp:311-317); each
+// list then keeps its cap smallest pair weights, in weight order.  E = keys
+// per lane of the sorts (32 E >= both raw counts).  Returns (nn, no).
+template <uint32_t E>
+__device__ __forceinline__ void det_lists(const GraphView& g, const CandView& c, uint32_t u,
+                                          uint32_t nr, uint32_t orr, uint32_t hid,
+                                          uint32_t hflags, uint32_t* s_new, uint8_t* s_kill,
+                                          const uint32_t* s_hid, uint32_t seed_lo,
+                                          uint32_t seed_hi, uint32_t& nn, uint32_t& no) {
+    const uint32_t lane = lane_id(), cap = c.cap, k = g.k;
+    const uint32_t* raw = c.raw + size_t(u) * 4 * cap;
+    uint32_t vn[E], vo[E];
+#pragma unroll
+    for (uint32_t r = 0; r < E; ++r) {
+        const uint32_t i = E * lane + r;
+        vn[r] = i < nr ? raw[i] : kTomb;
+        vo[r] = i < orr ? raw[2 * cap + i] : kTomb;
+    }
+    warp_sort<E>(vn);
+    warp_sort<E>(vo);
+    // duplicates -> kTomb (kTomb - 1 never equals an id: ids < n < 2^31)
+    auto dedup = [&](uint32_t (&v)[E]) {
+        const uint32_t prev_last = __shfl_up_sync(0xffffffffu, v[E - 1], 1);
+        uint32_t prev = lane == 0 ? kTomb - 1u : prev_last;
+#pragma unroll
+        for (uint32_t r = 0; r < E; ++r) {
+            const uint32_t cur = v[r];
+            if (cur == prev) v[r] = kTomb;
+            prev = cur;
+        }
+    };
+    dedup(vn);
+    dedup(vo);
+#pragma unroll
+    for (uint32_t r = 0; r < E; ++r) {
+        s_new[E * lane + r] = vn[r];
+        s_kill[E * lane + r] = 0;
+    }
+    __syncwarp();
+    // across lists: binary search of each old id in the sorted new ids
+    // (matches are disjoint pairs; kills go to s_kill, s_new stays sorted)
+#pragma unroll
+    for (uint32_t r = 0; r < E; ++r) {
+        const uint32_t x = vo[r];
+        if (x == kTomb) continue;
+        uint32_t lo = 0, hi = 32 * E;
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (s_new[mid] < x) lo = mid + 1; else hi = mid;
+        }
+        if (lo < 32 * E && s_new[lo] == x) {
+            uint32_t f_fwd = 1u;
+            for (uint32_t i = 0; i < k; ++i)
+                if (s_hid[i] == x) {
+                    f_fwd = (hflags >> i) & 1u;
+                    break;
+                }
+            const bool keep_new = (u < x) ? (f_fwd != 0u) : (f_fwd == 0u);
+            if (keep_new)
+                vo[r] = kTomb;
+            else
+                s_kill[lo] = 1;  // dropped from the new list
+        }
+    }
+    __syncwarp();
+#pragma unroll
+    for (uint32_t r = 0; r < E; ++r)
+        if (s_kill[E * lane + r]) vn[r] = kTomb;
+    // each list: cap smallest pair weights, in weight order
+    auto keep = [&](uint32_t (&v)[E], uint32_t kind, uint32_t* out, uint32_t& count) {
+        unsigned long long key[E];
+#pragma unroll
+        for (uint32_t r = 0; r < E; ++r)
+            key[r] = v[r] == kTomb
+                         ? ~0ull
+                         : (uint64_t(det_weight(u, v[r], kind, seed_lo, seed_hi)) << 32) | v[r];
+        warp_sort<E>(key);
+        uint32_t valid = 0;
+#pragma unroll
+        for (uint32_t r = 0; r < E; ++r) valid += key[r] != ~0ull;
+#pragma unroll
+        for (uint32_t o = 16; o > 0; o >>= 1) valid += __shfl_xor_sync(0xffffffffu, valid, o);
+        count = min(valid, cap);
+#pragma unroll
+        for (uint32_t r = 0; r < E; ++r) {
+            const uint32_t i = E * lane + r;
+            if (i < count) out[i] = uint32_t(key[r]);
+        }
+    };
+    uint32_t* const list = c.ids + size_t(u) * 2 * cap;
+    keep(vn, 1u, list, nn);
+    keep(vo, 2u, list + cap, no);
+    (void)hid;
+}
+
+__global__ void __launch_bounds__(kFinWarps * 32, 4) finalize_det_kernel(GraphView g, CandView c,
+                                                                      uint32_t* active,
+                                                                      IterCounters* ctr,
+                                                                      uint32_t seed_lo,
+                                                                      uint32_t seed_hi) {
+    __shared__ uint32_t s_new[kFinWarps][128];
+    __shared__ uint8_t s_kill[kFinWarps][128];
+    __shared__ uint32_t s_hid[kFinWarps][kMaxK];
+    __shared__ BlockCounters acc;
+    init_block_counters(acc);
+    const uint32_t w = threadIdx.x >> 5, lane = lane_id();
+    const uint32_t cap = c.cap, k = g.k;
+    for (uint32_t it = 0; it < kFinNodesPerWarp; ++it) {
+        const uint32_t u = g.lo + (blockIdx.x * kFinNodesPerWarp + it) * kFinWarps + w;
+        if (u >= g.hi) break;
+        __syncwarp();  // the previous node's shared rows are no longer read
+        const uint32_t nr = min(c.raw_new[u], 2 * cap), orr = min(c.raw_old[u], 2 * cap);
+        const uint32_t hid = lane < k ? key_id(g.keys[size_t(u) * k + lane]) : kTomb;
+        s_hid[w][lane] = hid;
+        const uint32_t hflags = g.flags[u];
+        __syncwarp();
+        uint32_t nn = 0, no = 0;
+        const uint32_t most = max(nr, orr);
+        if (most <= 32)
+            det_lists<1>(g, c, u, nr, orr, hid, hflags, s_new[w], s_kill[w], s_hid[w], seed_lo,
+                         seed_hi, nn, no);
+        else if (most <= 64)
+            det_lists<2>(g, c, u, nr, orr, hid, hflags, s_new[w], s_kill[w], s_hid[w], seed_lo,
+                         seed_hi, nn, no);
+        else
+            det_lists<4>(g, c, u, nr, orr, hid, hflags, s_new[w], s_kill[w], s_hid[w], seed_lo,
+                         seed_hi, nn, no);
+        __syncwarp();
+        // flag_consumed: heap entries named by the final new list
+        const uint32_t* const list = c.ids + size_t(u) * 2 * cap;
+        bool named = false;
+        if (lane < k)
+            for (uint32_t q = 0; q < nn; ++q)
+                if (list[q] == hid) {
+                    named = true;
+                    break;
+                }
+        const uint32_t clear = __ballot_sync(0xffffffffu, named);
+        if (lane == 0) {
+            c.nc[u] = nn;
+            c.oc[u] = no;
+            g.flags[u] = hflags & ~clear;
+        }
+        join_bookkeeping(g, c, u, nn, no, acc);
+    }
+    flush_block_counters(acc, active, ctr);
+}
+
 // Bookkeeping only, for candidate lists supplied from outside (the
 // fixed-state local-join entry): same accounting as finalize.
 __global__ void __launch_bounds__(kFinWarps * 32, 8) bookkeeping_kernel(GraphView g, CandView c,
@@ -413,9 +613,14 @@ void launch_sample(const GraphView& g, const CandView& c, const uint32_t* indeg,
 }
 
 void launch_finalize(const GraphView& g, const CandView& c, uint32_t* active,
-                     IterCounters* ctr, cudaStream_t s) {
+                     IterCounters* ctr, cudaStream_t s, uint64_t seed) {
     cudaMemsetAsync(c.revcnt, 0, sizeof(uint32_t) * g.n, s);
     if (g.hi <= g.lo) return;
+    if (c.det) {
+        finalize_det_kernel<<<blocks_for(g.hi - g.lo, kFinNodes), kFinWarps * 32, 0, s>>>(
+            g, c, active, ctr, uint32_t(seed), uint32_t(seed >> 32));
+        return;
+    }
     finalize_kernel<<<blocks_for(g.hi - g.lo, kFinNodes), kFinWarps * 32, 0, s>>>(g, c, active,
                                                                                   ctr);
 }

@@ -746,21 +746,47 @@ __global__ void __launch_bounds__(kThreads, KNNG_JOIN_MINBLOCKS) join_distances_
 
 // Warp-wide bounded insert into a sorted row held one key per lane (lanes
 // >= k hold kEmptyKey).  try_insert semantics (graph.hpp:116-129).
+// Deterministic mode (det): a present id takes the smaller of its two
+// distances (the same pair evaluated in two joins; the reference keeps
+// whichever its sequential order offered first), and `fresh` marks only ids
+// absent from the target's initial row (lane i's initial id: init_id), so the
+// final row and its change count do not depend on the insertion order.
 __device__ __forceinline__ bool warp_try_insert(uint64_t& key, uint32_t& flags, uint32_t k,
                                                 float dist, uint32_t cand,
-                                                uint32_t* fresh = nullptr) {
+                                                uint32_t* fresh = nullptr, bool det = false,
+                                                uint32_t init_id = 0xffffffffu) {
     const uint32_t lane = lane_id();
     const uint64_t max_key = __shfl_sync(0xffffffffu, key, k - 1);
     if (!(dist < key_dist(max_key))) return false;
-    if (__ballot_sync(0xffffffffu, lane < k && key_id(key) == cand)) return false;
+    const uint32_t kmask = k >= 32 ? 0xffffffffu : ((1u << k) - 1u);
     const uint64_t nk = pack_key(dist, cand);
+    const uint32_t present = __ballot_sync(0xffffffffu, lane < k && key_id(key) == cand);
+    if (present) {
+        if (!det) return false;
+        const uint32_t p = __ffs(present) - 1u;
+        if (!(nk < __shfl_sync(0xffffffffu, key, p))) return false;
+        // move the entry from p down to its new position pos <= p
+        const uint32_t pos = __popc(__ballot_sync(0xffffffffu, lane < k && key < nk));
+        const uint64_t up = __shfl_up_sync(0xffffffffu, key, 1);
+        if (lane < k) key = (lane < pos || lane > p) ? key : (lane == pos ? nk : up);
+        auto carry = [&](uint32_t b) {
+            const uint32_t bp = (b >> p) & 1u;
+            const uint32_t mid = ((1u << p) - 1u) & ~((1u << pos) - 1u);  // bits [pos, p)
+            return ((b & ~(mid | (1u << p))) | ((b & mid) << 1) | (bp << pos)) & kmask;
+        };
+        flags = carry(flags);
+        if (fresh) *fresh = carry(*fresh);
+        return true;
+    }
     const uint32_t pos = __popc(__ballot_sync(0xffffffffu, lane < k && key < nk));
     const uint64_t up = __shfl_up_sync(0xffffffffu, key, 1);
     if (lane < k) key = lane < pos ? key : (lane == pos ? nk : up);
     const uint32_t low = (1u << pos) - 1u;
-    const uint32_t kmask = k >= 32 ? 0xffffffffu : ((1u << k) - 1u);
     flags = ((flags & low) | (1u << pos) | ((flags & ~low) << 1)) & kmask;
-    if (fresh) *fresh = ((*fresh & low) | (1u << pos) | ((*fresh & ~low) << 1)) & kmask;
+    if (fresh) {
+        const uint32_t came = det ? (__ballot_sync(0xffffffffu, init_id == cand) == 0u) : 1u;
+        *fresh = ((*fresh & low) | (came << pos) | ((*fresh & ~low) << 1)) & kmask;
+    }
     return true;
 }
 
@@ -777,10 +803,11 @@ constexpr uint32_t kMergeDepth = KNNG_MERGE_DEPTH;  // proposal steps fetched ah
 // Merges the proposals of t's reverse-index entries rv[0, cnt) into the row
 // held by the calling warp (lane i = entry i).  `fresh` tracks which entries
 // came in (shifted like the flags).
+template <bool kDet>
 __device__ __forceinline__ void merge_entries(const CandView& c, const uint64_t* rv, uint32_t cnt,
                                               uint32_t k, uint64_t& key, uint32_t& flags,
                                               uint32_t& fresh, float& cur_max,
-                                              uint32_t& inserted) {
+                                              uint32_t& inserted, uint32_t init_id) {
     const uint32_t lane = lane_id();
     // Metadata of kMergeMeta chunks of 32 entries at once, one entry per lane
     // per chunk: where t's row of the node's proposal block starts and how
@@ -857,7 +884,8 @@ __device__ __forceinline__ void merge_entries(const CandView& c, const uint64_t*
                     pass &= pass - 1u;
                     const float dd = __shfl_sync(0xffffffffu, cur.dist, src);
                     const uint32_t cc = __shfl_sync(0xffffffffu, cur.cand, src);
-                    if (dd < cur_max && warp_try_insert(key, flags, k, dd, cc, &fresh)) {
+                    if (dd < cur_max &&
+                        warp_try_insert(key, flags, k, dd, cc, &fresh, kDet, init_id)) {
                         ++inserted;
                         cur_max = key_dist(__shfl_sync(0xffffffffu, key, k - 1));
                     }
@@ -877,6 +905,7 @@ __device__ __forceinline__ void merge_entries(const CandView& c, const uint64_t*
 #endif
 constexpr uint32_t kHubEntries = KNNG_HUB_ENTRIES;
 
+template <bool kDet>
 __global__ void __launch_bounds__(kMergeWarps * 32, KNNG_MERGE_MINBLOCKS) join_merge_kernel(GraphView g, CandView c,
                                                                      IterCounters* ctr,
                                                                      uint32_t* hubs) {
@@ -906,13 +935,17 @@ __global__ void __launch_bounds__(kMergeWarps * 32, KNNG_MERGE_MINBLOCKS) join_m
         uint32_t fresh = 0;
         float cur_max = key_dist(__shfl_sync(0xffffffffu, key, k - 1));
         uint32_t inserted = 0;
-        merge_entries(c, c.rev + roff, cnt, k, key, flags, fresh, cur_max, inserted);
+        const uint32_t init_id = kDet ? key_id(key) : 0xffffffffu;
+        merge_entries<kDet>(c, c.rev + roff, cnt, k, key, flags, fresh, cur_max, inserted, init_id);
         if (inserted) {
             if (lane < k) g.keys[size_t(t) * k + lane] = key;
             if (lane == 0) {
                 g.flags[t] = flags;
                 g.maxd[t] = cur_max;
-                atomicAdd(&s_changes, (unsigned long long)inserted);
+                // deterministic mode: |final row \ initial row| (order-free)
+                const uint32_t ch = kDet ? __popc(fresh & (k >= 32 ? 0xffffffffu : ((1u << k) - 1u)))
+                                         : inserted;
+                if (ch) atomicAdd(&s_changes, (unsigned long long)ch);
             }
         }
     }
@@ -931,6 +964,7 @@ __global__ void __launch_bounds__(kMergeWarps * 32, KNNG_MERGE_MINBLOCKS) join_m
 // incoming entries.  The result is the k smallest distinct candidates of the
 // row and all proposals, as in one warp (ties aside); the change count is the
 // number of entries that came in (the order-free count).
+template <bool kDet>
 __global__ void __launch_bounds__(kMergeWarps * 32) hub_merge_kernel(GraphView g, CandView c,
                                                                     IterCounters* ctr,
                                                                     const uint32_t* hubs) {
@@ -947,7 +981,9 @@ __global__ void __launch_bounds__(kMergeWarps * 32) hub_merge_kernel(GraphView g
         uint64_t key = lane < k ? g.keys[size_t(t) * k + lane] : kEmptyKey;
         uint32_t flags = g.flags[t], fresh = 0, inserted = 0;
         float cur_max = key_dist(__shfl_sync(0xffffffffu, key, k - 1));
-        merge_entries(c, c.rev + c.roff[t] + b, e - b, k, key, flags, fresh, cur_max, inserted);
+        const uint32_t init_id = kDet ? key_id(key) : 0xffffffffu;
+        merge_entries<kDet>(c, c.rev + c.roff[t] + b, e - b, k, key, flags, fresh, cur_max, inserted,
+                            init_id);
         s_keys[w][lane] = key;
         if (lane == 0) s_fresh[w] = fresh;
         __syncthreads();
@@ -955,21 +991,24 @@ __global__ void __launch_bounds__(kMergeWarps * 32) hub_merge_kernel(GraphView g
             for (uint32_t o = 1; o < kMergeWarps; ++o) {
                 const uint32_t fr = s_fresh[o];
                 for (uint32_t i = 0; i < k; ++i) {
-                    if (!((fr >> i) & 1u)) continue;
+                    // deterministic mode: every entry (smaller copies of
+                    // initial ids carry no fresh bit)
+                    if (!((fr >> i) & 1u) && !kDet) continue;
                     const uint64_t pk = s_keys[o][i];
                     const float dd = key_dist(pk);
-                    if (dd < cur_max && warp_try_insert(key, flags, k, dd, key_id(pk), &fresh))
+                    if (dd < cur_max &&
+                        warp_try_insert(key, flags, k, dd, key_id(pk), &fresh, kDet, init_id))
                         cur_max = key_dist(__shfl_sync(0xffffffffu, key, k - 1));
                 }
             }
             const uint32_t kmask = k >= 32 ? 0xffffffffu : ((1u << k) - 1u);
             const uint32_t came = __popc(fresh & kmask);
-            if (came) {
+            if (came || kDet) {
                 if (lane < k) g.keys[size_t(t) * k + lane] = key;
                 if (lane == 0) {
                     g.flags[t] = flags;
                     g.maxd[t] = cur_max;
-                    atomicAdd(&ctr->changes, (unsigned long long)came);
+                    if (came) atomicAdd(&ctr->changes, (unsigned long long)came);
                 }
             }
         }
@@ -1072,11 +1111,16 @@ void launch_join_distances(const GraphView& g, const CandView& c, const uint32_t
 void launch_join_merge(const GraphView& g, const CandView& c, IterCounters* ctr,
                        cudaStream_t s) {
     if (g.hi <= g.lo) return;
-    join_merge_kernel<<<(g.hi - g.lo + kMergeWarps - 1) / kMergeWarps, kMergeWarps * 32, 0, s>>>(
-        g, c, ctr, c.hubs);
+    const uint32_t blocks = (g.hi - g.lo + kMergeWarps - 1) / kMergeWarps;
     // the hubs it left: a CTA each, blocks looping over the device-side count
-    hub_merge_kernel<<<std::min<uint32_t>(2 * sm_count(), (g.hi - g.lo + 1) / 2 + 1),
-                       kMergeWarps * 32, 0, s>>>(g, c, ctr, c.hubs);
+    const uint32_t hub_blocks = std::min<uint32_t>(2 * sm_count(), (g.hi - g.lo + 1) / 2 + 1);
+    if (c.det) {
+        join_merge_kernel<true><<<blocks, kMergeWarps * 32, 0, s>>>(g, c, ctr, c.hubs);
+        hub_merge_kernel<true><<<hub_blocks, kMergeWarps * 32, 0, s>>>(g, c, ctr, c.hubs);
+    } else {
+        join_merge_kernel<false><<<blocks, kMergeWarps * 32, 0, s>>>(g, c, ctr, c.hubs);
+        hub_merge_kernel<false><<<hub_blocks, kMergeWarps * 32, 0, s>>>(g, c, ctr, c.hubs);
+    }
 }
 
 // ---------------------------------------------------------------------------

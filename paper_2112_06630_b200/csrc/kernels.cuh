@@ -47,6 +47,13 @@ struct CandView {
                          // (iteration start), beside ids
     uint4* arec;         // per active index: {u, nn | no << 16, doff lo, doff hi}
     uint32_t* hubs;      // n: targets with more than kHubEntries reverse entries
+    // deterministic mode (knng_cuda_params.deterministic): sampling appends
+    // every accepted offer to n x 4cap raw lists (new 2cap, old 2cap; no
+    // reservoir), finalize keeps the cap offers of smallest pair weight, and
+    // the merges keep the smaller copy of a present id and count changes as
+    // |final row \ initial row|
+    uint32_t* raw;
+    int det;
 };
 
 // Device counters for one iteration.
@@ -75,7 +82,7 @@ void launch_sample(const GraphView& g, const CandView& c, const uint32_t* indeg,
                    cudaStream_t s);
 // dedup + flag_consumed + join bookkeeping (active list, block sizes, reverse counts)
 void launch_finalize(const GraphView& g, const CandView& c, uint32_t* active,
-                     IterCounters* ctr, cudaStream_t s);
+                     IterCounters* ctr, cudaStream_t s, uint64_t seed = 0);
 // join bookkeeping only, for externally supplied candidate lists (fixed-state entries)
 void launch_bookkeeping(const GraphView& g, const CandView& c, uint32_t* active,
                         IterCounters* ctr, cudaStream_t s);

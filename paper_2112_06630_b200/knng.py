@@ -46,6 +46,9 @@ class RunParams:
     seed: int = 0
     device: int = 0
     profile: bool = False
+    # seed-deterministic build: the same graph for the same seed
+    # (acceptance.cpp:383-408); DESIGN.md §4
+    deterministic: bool = False
 
     def validate(self) -> None:
         """RunParams::validate (descent.hpp:29-35)."""
@@ -67,6 +70,7 @@ class RunParams:
         p.seed = self.seed & 0xFFFFFFFFFFFFFFFF
         p.device = self.device
         p.profile = int(self.profile)
+        p.deterministic = int(self.deterministic)
         return p
 
 
