@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(kUWarps * 32, KNNG_U8_MINB) join_u8_kernel(Gra
                                                                IterCounters* ctr,
                                                                const uint8_t* __restrict__ packed,
                                                                const int32_t* __restrict__ lnorm,
-                                                               uint32_t kl) {
+                                                               uint32_t kl, uint32_t heavy_nn) {
     __shared__ U8Warp shw[kUWarps];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
     U8Warp& W = shw[warp];
@@ -236,6 +236,7 @@ __global__ void __launch_bounds__(kUWarps * 32, KNNG_U8_MINB) join_u8_kernel(Gra
         if (a >= n_active) break;
         const uint4 rec = c.arec[a];
         const uint32_t u = rec.x, nn = rec.y & 0xffffu, no = rec.y >> 16, m = nn + no;
+        if (nn > heavy_nn) continue;  // join_u8_staged_kernel's node
         uint64_t* const D = c.D + (uint64_t(rec.z) | (uint64_t(rec.w) << 32));
         for (uint32_t x = lane; x < m; x += 32) {
             const size_t pos = size_t(u) * 2 * cap + (x < nn ? x : cap + x - nn);
@@ -265,6 +266,252 @@ __global__ void __launch_bounds__(kUWarps * 32, KNNG_U8_MINB) join_u8_kernel(Gra
         __syncwarp();
         for (uint32_t x = lane; x < m; x += 32) D[u8_prow(x, nn, m)] = W.rowcnt[x];
         __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Staged variant: one CTA per active node, the node's byte rows and lane
+// norms copied once into shared memory (16-byte cp.async, L2 -> SMEM), then
+// the CTA's warps split the node's (16-row block, 2 column blocks) tiles.  The
+// warp-per-node kernel above reads every fragment from L2 once per tile that
+// uses it (A rows once per column-block pair, B rows once per row block); here
+// each row crosses L2 once per node.  Two CTAs per SM: one stages while the
+// other computes; the next node's record, ids and row maxima are loaded into
+// registers while the current node's copies are in flight.  Arithmetic,
+// tree order and proposal epilogue are those of tile_pairs (bit-identical).
+// Nodes with more than heavy_nn new candidates (KNNG_U8_HEAVY, default 16)
+// come here, claimed 32 active indices at a time; the rest stay with the
+// warp-per-node kernel, which skips them.
+//
+// Measured slower on B200 and kept opt-in (KNNG_U8_STAGED=1): C2 join 6.0 ->
+// 7.4 ms per build (heavy > 16), 8.3 ms (> 8), 10.3 ms (every node);
+// iteration 1 1.63 -> 2.09 ms.  ncu (profiles/round1_ncu_join_u8_staged_c2.json):
+// 57% more instructions than the warp kernel (swizzled shared addressing, no
+// immediate offsets), issue active 36%, the top stall the node barriers: with
+// 7 tile units per iteration-1 node and 8 warps, each warp runs one
+// dependent load -> MMA chain per node, and two CTAs per SM do not hide the
+// staging round trip.
+//
+// Shared rows are 8 Kl bytes with no padding; the 16-byte chunks of odd rows
+// are XOR-swizzled by 64 bytes, so the two rows a quarter-warp's 16-byte
+// fragment loads touch (gq, gq + 1) fall in different bank halves.
+constexpr uint32_t kSWarps = 8;
+
+__device__ __forceinline__ void cp_async16_u8(void* smem_dst, const void* gmem_src) {
+    const uint32_t dst = uint32_t(__cvta_generic_to_shared(smem_dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(gmem_src));
+}
+
+struct U8Stage {
+    const uint8_t* rows;  // m x 8 Kl bytes, swizzled
+    const int32_t* nrm;   // m x 8
+    const uint32_t* rid;  // m
+    const float* rmx;     // m
+    uint32_t* rowcnt;     // m
+};
+
+template <uint32_t C2>
+__device__ __forceinline__ void tile_pairs_staged(const U8Stage& S, uint32_t mi, uint32_t njb,
+                                                  uint32_t nn, uint32_t m, uint32_t nnj, int filter,
+                                                  uint64_t* D) {
+    constexpr uint32_t kl = 64 * C2, RB = 8 * kl;
+    const uint32_t lane = threadIdx.x & 31u, gq = lane >> 2, t = lane & 3u;
+    // rows past the node's list (padding of the last 16 / 8 blocks) read row 0
+    auto srow = [&](uint32_t r) { return r < m ? r : 0u; };
+    const uint32_t ra0 = srow(16 * mi + gq), ra1 = srow(16 * mi + gq + 8);
+    // byte offsets of this thread's fragment rows; the swizzle of a row's
+    // chunk offset o is o ^ ((row & 1) << 6)
+    const uint32_t oa0 = ra0 * RB, oa1 = ra1 * RB, sa0 = (ra0 & 1u) << 6, sa1 = (ra1 & 1u) << 6;
+    uint32_t ob[kUNB], sb[kUNB], cb0[kUNB], cb1[kUNB];
+    bool live[kUNB];
+#pragma unroll
+    for (uint32_t q = 0; q < kUNB; ++q) {
+        live[q] = njb + q < nnj;
+        const uint32_t col = srow(8 * (njb + q) + gq);
+        ob[q] = col * RB;
+        sb[q] = (col & 1u) << 6;
+        cb0[q] = srow(8 * (njb + q) + 2 * t) * 8;
+        cb1[q] = srow(8 * (njb + q) + 2 * t + 1) * 8;
+    }
+    float part[kUNB][4][3];
+#pragma unroll
+    for (uint32_t l = 0; l < 8; ++l) {
+        uint4 A0[C2], A1[C2], B[kUNB][C2];
+#pragma unroll
+        for (uint32_t g2 = 0; g2 < C2; ++g2) {
+            const uint32_t o = l * kl + 64 * g2 + 16 * t;
+            A0[g2] = *reinterpret_cast<const uint4*>(S.rows + (oa0 + (o ^ sa0)));
+            A1[g2] = *reinterpret_cast<const uint4*>(S.rows + (oa1 + (o ^ sa1)));
+#pragma unroll
+            for (uint32_t q = 0; q < kUNB; ++q)
+                B[q][g2] = *reinterpret_cast<const uint4*>(S.rows + (ob[q] + (o ^ sb[q])));
+        }
+        int acc[kUNB][4];
+#pragma unroll
+        for (uint32_t q = 0; q < kUNB; ++q)
+#pragma unroll
+            for (uint32_t r = 0; r < 4; ++r) acc[q][r] = 0;
+#pragma unroll
+        for (uint32_t g2 = 0; g2 < C2; ++g2)
+#pragma unroll
+            for (uint32_t q = 0; q < kUNB; ++q) {
+                mma_u8(acc[q], A0[g2].x, A1[g2].x, A0[g2].y, A1[g2].y, B[q][g2].x, B[q][g2].y);
+                mma_u8(acc[q], A0[g2].z, A1[g2].z, A0[g2].w, A1[g2].w, B[q][g2].z, B[q][g2].w);
+            }
+        // the reference's tree, as in tile_pairs
+        const int32_t a_n0 = S.nrm[ra0 * 8 + l], a_n1 = S.nrm[ra1 * 8 + l];
+#pragma unroll
+        for (uint32_t q = 0; q < kUNB; ++q) {
+            const int32_t b_n0 = S.nrm[cb0[q] + l], b_n1 = S.nrm[cb1[q] + l];
+#pragma unroll
+            for (uint32_t r = 0; r < 4; ++r) {
+                const int32_t an = r < 2 ? a_n0 : a_n1;
+                const int32_t bn = (r & 1u) ? b_n1 : b_n0;
+                const float sl = float(an + bn - 2 * acc[q][r]);
+                float* p = part[q][r];
+                if (l == 0 || l == 4)
+                    p[0] = sl;
+                else if (l == 2 || l == 6)
+                    p[1] = sl;
+                else if (l == 1 || l == 5)
+                    p[0] = __fadd_rn(p[0], sl);
+                else if (l == 3)
+                    p[2] = __fadd_rn(p[0], __fadd_rn(p[1], sl));
+                else
+                    p[0] = __fadd_rn(p[2], __fadd_rn(p[0], __fadd_rn(p[1], sl)));
+            }
+        }
+    }
+#pragma unroll
+    for (uint32_t q = 0; q < kUNB; ++q) {
+        if (!live[q]) continue;
+#pragma unroll
+        for (uint32_t r = 0; r < 4; ++r) {
+            const uint32_t i = 16 * mi + gq + 8 * (r >> 1);
+            const uint32_t j = 8 * (njb + q) + 2 * t + (r & 1u);
+            if (i >= nn || j >= m || (j < nn && j <= i)) continue;
+            const uint32_t id_i = S.rid[i], id_j = S.rid[j];
+            if (filter && id_i == id_j) continue;  // try_insert ignores self
+            const float dist = part[q][r][0];
+            if (dist < S.rmx[i]) {
+                const uint32_t pos = atomicAdd(&S.rowcnt[i], 1u);
+                D[u8_prow(i, nn, m) + 1 + pos] = pack_key(dist, id_j);
+            }
+            if (dist < S.rmx[j]) {
+                const uint32_t pos = atomicAdd(&S.rowcnt[j], 1u);
+                D[u8_prow(j, nn, m) + 1 + pos] = pack_key(dist, id_i);
+            }
+        }
+    }
+}
+
+__host__ __device__ constexpr size_t u8_staged_smem(uint32_t C2, uint32_t mmax) {
+    return size_t(mmax) * (512u * C2 + 32u + 12u);
+}
+
+template <uint32_t C2>
+__global__ void __launch_bounds__(kSWarps * 32, 2)
+    join_u8_staged_kernel(GraphView g, CandView c, IterCounters* ctr,
+                          const uint8_t* __restrict__ packed, const int32_t* __restrict__ lnorm,
+                          uint32_t heavy_nn) {
+    constexpr uint32_t RB = 512 * C2, CH = RB / 16;  // row bytes, 16-byte chunks per row
+    extern __shared__ __align__(16) uint8_t u8s[];
+    const uint32_t cap = c.cap, mmax = 2 * cap, tid = threadIdx.x, warp = tid >> 5;
+    U8Stage S;
+    uint8_t* rows = u8s;
+    int32_t* nrm = reinterpret_cast<int32_t*>(u8s + size_t(mmax) * RB);
+    uint32_t* rid = reinterpret_cast<uint32_t*>(nrm + size_t(mmax) * 8);
+    float* rmx = reinterpret_cast<float*>(rid + mmax);
+    uint32_t* rowcnt = reinterpret_cast<uint32_t*>(rmx + mmax);
+    S.rows = rows;
+    S.nrm = nrm;
+    S.rid = rid;
+    S.rmx = rmx;
+    S.rowcnt = rowcnt;
+    if (ctr->overflow) return;
+    const uint32_t n_active = ctr->active, lane = tid & 31u;
+    const float inf = __int_as_float(0x7f800000);
+    // work queue: warp 0 claims 32 active indices at a time and keeps the
+    // records of the heavy ones (nn > heavy_nn); the rest are the warp-per-node
+    // kernel's
+    __shared__ uint4 q_rec[32];
+    __shared__ uint32_t q_n;
+    auto refill = [&]() -> uint32_t {
+        for (;;) {
+            if (warp == 0) {
+                uint32_t base = 0;
+                if (lane == 0) base = atomicAdd(&ctr->work2, 32u);
+                base = __shfl_sync(0xffffffffu, base, 0);
+                const uint32_t idx = base + lane;
+                uint4 r = make_uint4(0, 0, 0, 0);
+                if (idx < n_active) r = c.arec[idx];
+                const bool heavy = idx < n_active && (r.y & 0xffffu) > heavy_nn;
+                const uint32_t mask = __ballot_sync(0xffffffffu, heavy);
+                if (heavy) q_rec[__popc(mask & ((1u << lane) - 1u))] = r;
+                if (lane == 0) q_n = base >= n_active ? 0xffffffffu : __popc(mask);
+            }
+            __syncthreads();
+            const uint32_t qn = q_n;
+            if (qn) return qn == 0xffffffffu ? 0u : qn;
+            __syncthreads();  // q_n is rewritten by the next claim
+        }
+    };
+    // this thread's candidate (x = tid) of a node: id and row maximum
+    auto fetch = [&](const uint4& rec, uint32_t& id, float& mx) {
+        const uint32_t nn = rec.y & 0xffffu, m = nn + (rec.y >> 16);
+        if (tid < m) {
+            const size_t pos = size_t(rec.x) * 2 * cap + (tid < nn ? tid : cap + tid - nn);
+            id = c.ids[pos];
+            mx = c.filter ? c.cmax[pos] : inf;
+        }
+    };
+    uint32_t qn = refill(), qi = 0;
+    if (!qn) return;
+    uint4 rec = q_rec[0];
+    uint32_t pid = 0;
+    float pmx = inf;
+    fetch(rec, pid, pmx);
+    for (;;) {
+        const uint32_t nn = rec.y & 0xffffu, m = nn + (rec.y >> 16);
+        uint64_t* const D = c.D + (uint64_t(rec.z) | (uint64_t(rec.w) << 32));
+        if (tid < m) {
+            rid[tid] = pid;
+            rmx[tid] = pmx;
+            rowcnt[tid] = 0;
+        }
+        __syncthreads();
+        for (uint32_t q = tid; q < m * CH; q += kSWarps * 32) {
+            const uint32_t x = q / CH, ch = q % CH;
+            cp_async16_u8(rows + size_t(x) * RB + ((16 * ch) ^ ((x & 1u) << 6)),
+                          packed + size_t(rid[x]) * RB + 16 * ch);
+        }
+        for (uint32_t q = tid; q < 2 * m; q += kSWarps * 32)
+            cp_async16_u8(nrm + 4 * q, lnorm + size_t(rid[q >> 1]) * 8 + 4 * (q & 1u));
+        asm volatile("cp.async.commit_group;\n" ::);
+        // the next queued node's candidates load while the copies are in flight
+        uint4 rec_next = rec;
+        if (qi + 1 < qn) {
+            rec_next = q_rec[qi + 1];
+            fetch(rec_next, pid, pmx);
+        }
+        asm volatile("cp.async.wait_group 0;\n" ::);
+        __syncthreads();
+        const uint32_t nmi = (nn + 15) / 16, nnj = (m + 7) / 8;
+        uint32_t unit = 0;
+        for (uint32_t mi = 0; mi < nmi; ++mi)
+            for (uint32_t njb = 2 * mi; njb < nnj; njb += kUNB, ++unit)
+                if (unit % kSWarps == warp) tile_pairs_staged<C2>(S, mi, njb, nn, m, nnj, c.filter, D);
+        __syncthreads();
+        if (tid < m) D[u8_prow(tid, nn, m)] = rowcnt[tid];
+        if (++qi < qn) {
+            rec = rec_next;
+        } else {
+            qn = refill();
+            if (!qn) break;
+            qi = 0;
+            rec = q_rec[0];
+            fetch(rec, pid, pmx);
+        }
     }
 }
 
@@ -306,6 +553,32 @@ void launch_join_u8(const GraphView& g, const CandView& c, IterCounters* ctr, ui
                     const uint8_t* packed, const int32_t* lnorm, cudaStream_t s) {
     if (!max_active) return;
     const uint32_t kl = u8_lane_bytes(g.stride);
+    // staged variant (opt-in, KNNG_U8_STAGED=1; measured slower, see the
+    // comment above join_u8_staged_kernel) when two CTAs' node stages fit an
+    // SM's shared memory (C2: 100 rows x 1 KB)
+    const char* senv = getenv("KNNG_U8_STAGED");
+    const bool staged_env = senv && senv[0] == '1';
+    const uint32_t c2 = kl / 64;
+    const size_t ssm = u8_staged_smem(c2, 2 * c.cap);
+    uint32_t heavy_nn = 0xffffffffu;  // nodes with nn > heavy_nn take the staged kernel
+    if (staged_env && c2 <= 2 && 2 * (ssm + 1024) <= 233472) {
+        const char* hv = getenv("KNNG_U8_HEAVY");
+        heavy_nn = hv ? uint32_t(atoi(hv)) : 16u;
+        uint32_t grid = 2 * u8_sm_count();
+        if (grid > max_active) grid = max_active;
+        cudaMemsetAsync(&ctr->work2, 0, sizeof(uint32_t), s);
+        if (c2 == 1) {
+            cudaFuncSetAttribute(join_u8_staged_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(ssm));
+            join_u8_staged_kernel<1><<<grid, kSWarps * 32, ssm, s>>>(g, c, ctr, packed, lnorm,
+                                                                      heavy_nn);
+        } else {
+            cudaFuncSetAttribute(join_u8_staged_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(ssm));
+            join_u8_staged_kernel<2><<<grid, kSWarps * 32, ssm, s>>>(g, c, ctr, packed, lnorm,
+                                                                      heavy_nn);
+        }
+    }
     static int per_sm = 0;
     if (!per_sm) {
         int v = 0;
@@ -318,14 +591,15 @@ void launch_join_u8(const GraphView& g, const CandView& c, IterCounters* ctr, ui
     cudaMemsetAsync(&ctr->work, 0, sizeof(uint32_t), s);
 #define KNNG_U8_CASE(CH)                                                                   \
     case CH:                                                                               \
-        join_u8_kernel<CH><<<grid, kUWarps * 32, 0, s>>>(g, c, ctr, packed, lnorm, kl);  \
+        join_u8_kernel<CH><<<grid, kUWarps * 32, 0, s>>>(g, c, ctr, packed, lnorm, kl, heavy_nn); \
         break;
     switch (kl / 64) {
         KNNG_U8_CASE(1)
         KNNG_U8_CASE(2)
         KNNG_U8_CASE(3)
         KNNG_U8_CASE(4)
-        default: join_u8_kernel<5><<<grid, kUWarps * 32, 0, s>>>(g, c, ctr, packed, lnorm, kl);
+        default:
+            join_u8_kernel<5><<<grid, kUWarps * 32, 0, s>>>(g, c, ctr, packed, lnorm, kl, heavy_nn);
     }
 #undef KNNG_U8_CASE
 }

@@ -67,6 +67,7 @@ struct IterCounters {
     uint32_t work;               // dynamic work counter
     uint32_t overflow;           // distance blocks exceed the buffer: join skipped
     uint32_t hubs;               // merge: targets left to the per-CTA hub merge
+    uint32_t work2;              // second work counter (byte-valued join: staged nodes)
     unsigned long long screened;   // screened join: pairs bounded
     unsigned long long survivors;  // screened join: pairs evaluated exactly
 };

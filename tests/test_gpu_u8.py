@@ -34,11 +34,21 @@ def test_u8_step_equals_fp32_kernel_and_oracle(gpu, restated, monkeypatch, kind,
     gi, c, go, _, ev_ref = restated.capture_step(data, k, cap, seed, t)
     cands = kg.CandidateSet(c.ids, c.new_counts, c.old_counts)
     out = {}
-    for mode in ("0", "1"):
-        monkeypatch.setenv("KNNG_JOIN_U8", mode)
+    for mode in ("0", "1", "warp", "staged"):
+        # "1": the default (warp-per-node kernel); "warp": nodes with more
+        # than 16 new candidates through the opt-in staged kernel (CTA per
+        # node, rows in shared memory) where it fits, the rest through the
+        # warp-per-node kernel; "staged": every node through the staged kernel
+        monkeypatch.setenv("KNNG_JOIN_U8", "0" if mode == "0" else "1")
+        monkeypatch.setenv("KNNG_U8_STAGED", "0" if mode == "1" else "1")
+        monkeypatch.setenv("KNNG_U8_HEAVY", "0" if mode == "staged" else "16")
         out[mode] = kg.compute_step(data, gi.ids, gi.dists, gi.flags, cands)
     g8 = out["1"][0]
     assert out["1"][3] == ev_ref
+    for mode in ("warp", "staged"):
+        assert out[mode][3] == ev_ref
+        st3 = compare_step(gi, out[mode][0], g8)
+        assert st3["mismatch"] == 0 and st3["bit_exact"] == st3["common"], (mode, st3)
     st = compare_step(gi, go, g8, restated=restated, data=data)
     assert st["mismatch"] == 0 and st["flag_mismatch"] == 0, st
     # byte-valued data: fused and unfused paths agree, so every stored
