@@ -30,7 +30,10 @@ namespace knng_cuda {
 
 namespace {
 
-constexpr uint32_t kUWarps = 8;                 // warps per CTA, one node each
+#ifndef KNNG_U8_WARPS
+#define KNNG_U8_WARPS 8
+#endif
+constexpr uint32_t kUWarps = KNNG_U8_WARPS;  // warps per CTA, one node each
 constexpr uint32_t kUMaxM = 2 * kMaxCap;
 
 struct U8Warp {
@@ -111,7 +114,28 @@ __global__ void u8_pack_kernel(const float* __restrict__ data, uint32_t n, uint3
     if (lane < 8) lnorm[size_t(row) * 8 + lane] = nrm;
 }
 
-constexpr uint32_t kUNB = 2;  // column blocks per pass
+#ifndef KNNG_U8_NB
+#define KNNG_U8_NB 1  // 1 measured 10% faster than 2 and 4 (C2 join per build)
+#endif
+constexpr uint32_t kUNB = KNNG_U8_NB;  // column blocks per pass
+// fragment loads from the byte copy: 0 read-only path (__ldg), 1 L2 only
+// (__ldcg), 2 read-only without L1 allocation (A/B builds: scripts/build_variants.py)
+#ifndef KNNG_U8_LD
+#define KNNG_U8_LD 0
+#endif
+__device__ __forceinline__ uint4 ld_frag(const uint8_t* p) {
+#if KNNG_U8_LD == 1
+    return __ldcg(reinterpret_cast<const uint4*>(p));
+#elif KNNG_U8_LD == 2
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];\n"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+#else
+    return __ldg(reinterpret_cast<const uint4*>(p));
+#endif
+}
 #ifndef KNNG_U8_MINB
 #define KNNG_U8_MINB 2  // CTAs per SM the register budget is sized for
 #endif
@@ -121,7 +145,11 @@ constexpr uint32_t kUNB = 2;  // column blocks per pass
 // the MMAs (the byte rows come from L2: latency, not bandwidth, bounds a
 // dependent load -> MMA chain), then the lane sums enter the FP32 tree; the
 // pairs' proposals are written at the end.
-template <uint32_t C2>
+//
+// SW (swapped, nodes with nn <= 8): the 16 MMA rows run over candidates j
+// (block mi of all m) and the 8 columns over the new candidates i (block 0),
+// so a short new list fills 8 rather than 16 MMA rows: half the tiles.
+template <uint32_t C2, bool SW = false>
 __device__ __forceinline__ void tile_pairs(U8Warp& W, const uint8_t* __restrict__ packed,
                                            uint32_t kl, uint32_t mi, uint32_t njb, uint32_t nn,
                                            uint32_t m, uint32_t nnj, int filter, uint64_t* D) {
@@ -149,11 +177,10 @@ __device__ __forceinline__ void tile_pairs(U8Warp& W, const uint8_t* __restrict_
 #pragma unroll
         for (uint32_t g2 = 0; g2 < C2; ++g2) {
             const size_t o = size_t(l) * kl + 64 * g2;
-            A0[g2] = __ldg(reinterpret_cast<const uint4*>(pa0 + o));
-            A1[g2] = __ldg(reinterpret_cast<const uint4*>(pa1 + o));
+            A0[g2] = ld_frag(pa0 + o);
+            A1[g2] = ld_frag(pa1 + o);
 #pragma unroll
-            for (uint32_t q = 0; q < kUNB; ++q)
-                B[q][g2] = __ldg(reinterpret_cast<const uint4*>(pb[q] + o));
+            for (uint32_t q = 0; q < kUNB; ++q) B[q][g2] = ld_frag(pb[q] + o);
         }
         int acc[kUNB][4];
 #pragma unroll
@@ -198,8 +225,9 @@ __device__ __forceinline__ void tile_pairs(U8Warp& W, const uint8_t* __restrict_
         if (!live[q]) continue;
 #pragma unroll
         for (uint32_t r = 0; r < 4; ++r) {
-            const uint32_t i = 16 * mi + gq + 8 * (r >> 1);
-            const uint32_t j = 8 * (njb + q) + 2 * t + (r & 1u);
+            const uint32_t ra = 16 * mi + gq + 8 * (r >> 1);
+            const uint32_t cb_ = 8 * (njb + q) + 2 * t + (r & 1u);
+            const uint32_t i = SW ? cb_ : ra, j = SW ? ra : cb_;
             if (i >= nn || j >= m || (j < nn && j <= i)) continue;
             const uint32_t id_i = W.rid[i], id_j = W.rid[j];
             // an id listed twice pairs with itself: try_insert ignores self
@@ -223,7 +251,8 @@ __global__ void __launch_bounds__(kUWarps * 32, KNNG_U8_MINB) join_u8_kernel(Gra
                                                                IterCounters* ctr,
                                                                const uint8_t* __restrict__ packed,
                                                                const int32_t* __restrict__ lnorm,
-                                                               uint32_t kl, uint32_t heavy_nn) {
+                                                               uint32_t kl, uint32_t heavy_nn,
+                                                               int no_swap) {
     __shared__ U8Warp shw[kUWarps];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
     U8Warp& W = shw[warp];
@@ -250,7 +279,9 @@ __global__ void __launch_bounds__(kUWarps * 32, KNNG_U8_MINB) join_u8_kernel(Gra
         __syncwarp();
         // the lane norms (32 bytes each, 4 threads per row) of the rows the
         // tiles read: the candidates and the padding of the last blocks
-        const uint32_t rows = max(16 * ((nn + 15) / 16), 8 * ((m + 7) / 8));
+        const bool swapped = nn <= 8 && !no_swap;
+        const uint32_t rows =
+            swapped ? 16 * ((m + 15) / 16) : max(16 * ((nn + 15) / 16), 8 * ((m + 7) / 8));
         for (uint32_t q = lane; q < 4 * rows; q += 32) {
             const uint2 v = __ldg(reinterpret_cast<const uint2*>(lnorm + size_t(W.rid[q >> 2]) * 8) +
                                   (q & 3u));
@@ -259,10 +290,15 @@ __global__ void __launch_bounds__(kUWarps * 32, KNNG_U8_MINB) join_u8_kernel(Gra
         }
         __syncwarp();
         const uint32_t nmi = (nn + 15) / 16, nnj = (m + 7) / 8;
-        for (uint32_t mi = 0; mi < nmi; ++mi)
-            // column blocks left of the diagonal block hold only pairs j <= i
-            for (uint32_t njb = 2 * mi; njb < nnj; njb += kUNB)
-                tile_pairs<C>(W, packed, kl, mi, njb, nn, m, nnj, c.filter, D);
+        if (swapped) {
+            for (uint32_t mj = 0; mj < (m + 15) / 16; ++mj)
+                tile_pairs<C, true>(W, packed, kl, mj, 0, nn, m, 1, c.filter, D);
+        } else {
+            for (uint32_t mi = 0; mi < nmi; ++mi)
+                // column blocks left of the diagonal block hold only pairs j <= i
+                for (uint32_t njb = 2 * mi; njb < nnj; njb += kUNB)
+                    tile_pairs<C>(W, packed, kl, mi, njb, nn, m, nnj, c.filter, D);
+        }
         __syncwarp();
         for (uint32_t x = lane; x < m; x += 32) D[u8_prow(x, nn, m)] = W.rowcnt[x];
         __syncwarp();
@@ -579,6 +615,9 @@ void launch_join_u8(const GraphView& g, const CandView& c, IterCounters* ctr, ui
                                                                       heavy_nn);
         }
     }
+    // nodes with nn <= 8 take the swapped tile shape; KNNG_U8_SWAP=0 turns it off (A/B)
+    const char* wenv = getenv("KNNG_U8_SWAP");
+    const int no_swap = (wenv && wenv[0] == '0') ? 1 : 0;
     static int per_sm = 0;
     if (!per_sm) {
         int v = 0;
@@ -591,7 +630,8 @@ void launch_join_u8(const GraphView& g, const CandView& c, IterCounters* ctr, ui
     cudaMemsetAsync(&ctr->work, 0, sizeof(uint32_t), s);
 #define KNNG_U8_CASE(CH)                                                                   \
     case CH:                                                                               \
-        join_u8_kernel<CH><<<grid, kUWarps * 32, 0, s>>>(g, c, ctr, packed, lnorm, kl, heavy_nn); \
+        join_u8_kernel<CH><<<grid, kUWarps * 32, 0, s>>>(g, c, ctr, packed, lnorm, kl, heavy_nn, \
+                                                          no_swap);                         \
         break;
     switch (kl / 64) {
         KNNG_U8_CASE(1)
@@ -599,7 +639,8 @@ void launch_join_u8(const GraphView& g, const CandView& c, IterCounters* ctr, ui
         KNNG_U8_CASE(3)
         KNNG_U8_CASE(4)
         default:
-            join_u8_kernel<5><<<grid, kUWarps * 32, 0, s>>>(g, c, ctr, packed, lnorm, kl, heavy_nn);
+            join_u8_kernel<5><<<grid, kUWarps * 32, 0, s>>>(g, c, ctr, packed, lnorm, kl, heavy_nn,
+                                                            no_swap);
     }
 #undef KNNG_U8_CASE
 }

@@ -34,18 +34,20 @@ def test_u8_step_equals_fp32_kernel_and_oracle(gpu, restated, monkeypatch, kind,
     gi, c, go, _, ev_ref = restated.capture_step(data, k, cap, seed, t)
     cands = kg.CandidateSet(c.ids, c.new_counts, c.old_counts)
     out = {}
-    for mode in ("0", "1", "warp", "staged"):
-        # "1": the default (warp-per-node kernel); "warp": nodes with more
+    for mode in ("0", "1", "noswap", "mixed", "staged"):
+        # "1": the default (warp-per-node kernel); "mixed": nodes with more
         # than 16 new candidates through the opt-in staged kernel (CTA per
         # node, rows in shared memory) where it fits, the rest through the
         # warp-per-node kernel; "staged": every node through the staged kernel
         monkeypatch.setenv("KNNG_JOIN_U8", "0" if mode == "0" else "1")
-        monkeypatch.setenv("KNNG_U8_STAGED", "0" if mode == "1" else "1")
+        monkeypatch.setenv("KNNG_U8_STAGED", "1" if mode in ("mixed", "staged") else "0")
         monkeypatch.setenv("KNNG_U8_HEAVY", "0" if mode == "staged" else "16")
+        # "noswap": nodes with nn <= 8 keep the 16 (new) x 8 tile shape
+        monkeypatch.setenv("KNNG_U8_SWAP", "0" if mode == "noswap" else "1")
         out[mode] = kg.compute_step(data, gi.ids, gi.dists, gi.flags, cands)
     g8 = out["1"][0]
     assert out["1"][3] == ev_ref
-    for mode in ("warp", "staged"):
+    for mode in ("noswap", "mixed", "staged"):
         assert out[mode][3] == ev_ref
         st3 = compare_step(gi, out[mode][0], g8)
         assert st3["mismatch"] == 0 and st3["bit_exact"] == st3["common"], (mode, st3)
