@@ -542,8 +542,10 @@ void run_engine(Engine& e, const float* data, bool data_on_device, const knng_cu
     e.upload(data, data_on_device);
     const uint64_t init_seed = master();
     int h = timer.begin(KNNG_CUDA_KERNEL_INIT);
-    e.use_u8_join();  // per-build data preparation (byte-valued data check + packing)
-    launch_init_random(e.gv(), init_seed, e.s);
+    // per-build data preparation (byte-valued data check + packing); init then
+    // reads the byte copy
+    const bool u8 = e.use_u8_join();
+    launch_init_random(e.gv(), init_seed, e.s, u8 ? e.packed.p : nullptr, u8 ? e.lnorm.p : nullptr);
     timer.end(h);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(e.s));
@@ -857,7 +859,8 @@ int knng_cuda_init_random(const float* data, uint32_t n, uint32_t d, uint32_t k,
         StreamHolder sh(nullptr);
         Engine e(device, n, d, k, 0, sh.s);
         e.upload(data, false);
-        launch_init_random(e.gv(), seed, e.s);
+        const bool u8 = e.use_u8_join();
+        launch_init_random(e.gv(), seed, e.s, u8 ? e.packed.p : nullptr, u8 ? e.lnorm.p : nullptr);
         const size_t nk = size_t(n) * k;
         DevBuf<uint32_t> ids;
         DevBuf<float> dists;

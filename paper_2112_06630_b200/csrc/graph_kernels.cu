@@ -49,8 +49,62 @@ __device__ __forceinline__ float group8_l2_scalar(const float* __restrict__ a,
     return acc;
 }
 
+// The same distance for byte-valued data (join_u8.cu's exactness argument:
+// every lane sum is an exact integer, so lane_l = |a|_l^2 + |b|_l^2 -
+// 2 <a, b>_l whichever order the reference sums in) from the lane-major byte
+// copy: group thread j reads bytes [8 (j + 8c), +8) of every lane segment of
+// both rows (8 threads cover 64 contiguous bytes), dp4a partial dots per lane,
+// an 8-thread reduce-scatter leaves lane j's dot on thread j, then the
+// reference's FP32 tree.  Rows of 8 Kl bytes, Kl = 64 C.
+__device__ __forceinline__ float group8_l2_u8(const uint8_t* __restrict__ a,
+                                              const uint8_t* __restrict__ b,
+                                              const int32_t* __restrict__ na,
+                                              const int32_t* __restrict__ nb, uint32_t kl) {
+    const uint32_t j = lane_id() & 7u;
+    uint32_t part[8];
+#pragma unroll
+    for (uint32_t l = 0; l < 8; ++l) {
+        uint32_t acc = 0;
+        for (uint32_t o = 8 * j; o < kl; o += 64) {
+            const uint2 x = __ldg(reinterpret_cast<const uint2*>(a + l * kl + o));
+            const uint2 y = __ldg(reinterpret_cast<const uint2*>(b + l * kl + o));
+            acc = __dp4a(x.x, y.x, acc);
+            acc = __dp4a(x.y, y.y, acc);
+        }
+        part[l] = acc;
+    }
+    // reduce-scatter over the group: after the xor-4 / 2 / 1 rounds thread j
+    // holds lane j's whole dot product
+#pragma unroll
+    for (uint32_t i = 0; i < 4; ++i) {
+        const bool hi = j & 4u;
+        const uint32_t send = hi ? part[i] : part[i + 4], keep = hi ? part[i + 4] : part[i];
+        part[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+#pragma unroll
+    for (uint32_t i = 0; i < 2; ++i) {
+        const bool hi = j & 2u;
+        const uint32_t send = hi ? part[i] : part[i + 2], keep = hi ? part[i + 2] : part[i];
+        part[i] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+    }
+    {
+        const bool hi = j & 1u;
+        const uint32_t send = hi ? part[0] : part[1], keep = hi ? part[1] : part[0];
+        part[0] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+    }
+    float acc = float(__ldg(na + j) + __ldg(nb + j) - 2 * int32_t(part[0]));
+    acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 1));
+    acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 2));
+    acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 4));
+    return acc;
+}
+
+template <bool kU8>
 __global__ void __launch_bounds__(256) init_random_kernel(GraphView g, uint32_t seed_lo,
-                                                          uint32_t seed_hi) {
+                                                          uint32_t seed_hi,
+                                                          const uint8_t* __restrict__ packed,
+                                                          const int32_t* __restrict__ lnorm,
+                                                          uint32_t kl) {
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (g.lo + warp >= g.hi) return;
     const uint32_t u = g.lo + warp, lane = lane_id(), k = g.k, n = g.n;
@@ -81,8 +135,11 @@ __global__ void __launch_bounds__(256) init_random_kernel(GraphView g, uint32_t 
         const uint32_t pair = e + (lane >> 3);
         const uint32_t v = __shfl_sync(0xffffffffu, id, pair & 31u);
         const bool act = pair < k;
-        const float dist = group8_l2_scalar(ru, g.data + size_t(act ? v : u) * g.stride,
-                                            g.stride, act);
+        const uint32_t w = act ? v : u;
+        const float dist =
+            kU8 ? group8_l2_u8(packed + size_t(u) * 8 * kl, packed + size_t(w) * 8 * kl,
+                               lnorm + size_t(u) * 8, lnorm + size_t(w) * 8, kl)
+                : group8_l2_scalar(ru, g.data + size_t(w) * g.stride, g.stride, act);
         // lane (e + j) takes the result of group j (lane 8j)
         const uint32_t src = ((lane - e) & 3u) << 3;
         const float got = __shfl_sync(0xffffffffu, dist, src);
@@ -581,10 +638,16 @@ inline uint32_t blocks_for(size_t items, uint32_t per_block) {
 
 }  // namespace
 
-void launch_init_random(const GraphView& g, uint64_t seed, cudaStream_t s) {
+void launch_init_random(const GraphView& g, uint64_t seed, cudaStream_t s, const uint8_t* packed,
+                        const int32_t* lnorm) {
     if (g.hi <= g.lo) return;
-    init_random_kernel<<<blocks_for(size_t(g.hi - g.lo) * 32, 256), 256, 0, s>>>(
-        g, uint32_t(seed), uint32_t(seed >> 32));
+    const uint32_t blocks = blocks_for(size_t(g.hi - g.lo) * 32, 256);
+    if (packed)
+        init_random_kernel<true><<<blocks, 256, 0, s>>>(g, uint32_t(seed), uint32_t(seed >> 32),
+                                                        packed, lnorm, u8_lane_bytes(g.stride));
+    else
+        init_random_kernel<false><<<blocks, 256, 0, s>>>(g, uint32_t(seed), uint32_t(seed >> 32),
+                                                         nullptr, nullptr, 0);
 }
 
 void launch_load_rows(const GraphView& g, const uint32_t* ids, const float* dists,

@@ -73,7 +73,10 @@ struct IterCounters {
 };
 
 // --- graph_kernels.cu ------------------------------------------------------
-void launch_init_random(const GraphView& g, uint64_t seed, cudaStream_t s);
+// packed / lnorm: byte-valued data's lane-major copy (join_u8.cu); distances
+// then come from exact integer lane sums (bit-identical to the FP32 path)
+void launch_init_random(const GraphView& g, uint64_t seed, cudaStream_t s,
+                        const uint8_t* packed = nullptr, const int32_t* lnorm = nullptr);
 void launch_load_rows(const GraphView& g, const uint32_t* ids, const float* dists,
                       const uint8_t* flags, cudaStream_t s);
 void launch_export_rows(const GraphView& g, uint32_t* ids, float* dists, uint8_t* flags,
