@@ -140,8 +140,14 @@ struct KernelTimer {
     bool on;
     cudaStream_t s;
     std::vector<cudaEvent_t> pool;       // reused across flushes
-    std::vector<std::pair<int, size_t>> open;  // (kernel, first event index)
+    struct Open {
+        int kernel;
+        size_t first;  // first event index
+        uint32_t tag;  // iteration
+    };
+    std::vector<Open> open;
     size_t used = 0;
+    uint32_t tag = 0;  // iteration of the launches being recorded
     knng_cuda_metrics* m;
     KernelTimer(bool enabled, cudaStream_t stream, knng_cuda_metrics* metrics)
         : on(enabled && metrics), s(stream), m(metrics) {}
@@ -158,26 +164,32 @@ struct KernelTimer {
         const size_t i = used;
         CK(cudaEventRecord(next(), s));
         next();
-        open.push_back({kernel, i});
+        open.push_back({kernel, i, tag});
         return int(open.size()) - 1;
     }
     void end(int h) {
         if (h < 0) return;
-        CK(cudaEventRecord(pool[open[size_t(h)].second + 1], s));
+        CK(cudaEventRecord(pool[open[size_t(h)].first + 1], s));
     }
-    double last_join_ms = 0.0;  // distance-kernel time of the last flushed iteration
+    double last_join_ms = 0.0;         // distance-kernel time of the flushed launches
+    std::vector<double> join_ms_by_tag;  // ... per iteration
     void flush() {  // after a stream sync
         last_join_ms = 0.0;
         for (auto& e : open) {
             float ms = 0.0f;
-            CK(cudaEventElapsedTime(&ms, pool[e.second], pool[e.second + 1]));
-            m->kernel_ms[e.first] += ms;
-            m->kernel_launches[e.first] += 1;
-            if (e.first == KNNG_CUDA_KERNEL_JOIN) last_join_ms += ms;
+            CK(cudaEventElapsedTime(&ms, pool[e.first], pool[e.first + 1]));
+            m->kernel_ms[e.kernel] += ms;
+            m->kernel_launches[e.kernel] += 1;
+            if (e.kernel == KNNG_CUDA_KERNEL_JOIN) {
+                last_join_ms += ms;
+                if (join_ms_by_tag.size() <= e.tag) join_ms_by_tag.resize(e.tag + 1, 0.0);
+                join_ms_by_tag[e.tag] += ms;
+            }
         }
         open.clear();
         used = 0;
     }
+    double join_ms_of(uint32_t t) const { return t < join_ms_by_tag.size() ? join_ms_by_tag[t] : 0.0; }
     ~KernelTimer() {
         for (cudaEvent_t e : pool) cudaEventDestroy(e);
     }
@@ -229,8 +241,10 @@ struct Engine {
     bool det = false;            // deterministic mode (CandView::det)
     DevBuf<uint32_t> rawlist;    // its raw sampled lists, n x 4 cap
     size_t rev_cap = 0, d_cap = 0;
-    DevBuf<IterCounters> ctr;
-    IterCounters* h_ctr = nullptr;
+    DevBuf<IterCounters> ctr;    // slot 0, or one slot per iteration (ensure_slots)
+    IterCounters* cur = nullptr;  // the slot the kernels of the current iteration use
+    uint32_t slots = 1;
+    IterCounters* h_ctr = nullptr;  // pinned: h_ctr[i] mirrors slot i
     // tensor-core screened join (join_tc.cu): per-row norms for its bound,
     // computed on first use and after the data is permuted
     DevBuf<float> nrm2, nrmu;
@@ -280,13 +294,42 @@ struct Engine {
             scan_bytes = join_scan_scratch(n);
             scan_tmp.alloc(scan_bytes, pool, s);
             // every active list names at most 2 cap candidates
-            reserve_join(uint64_t(n) * 2 * cap, uint64_t(n) * 4 * k * k);
+            // (KNNG_TEST_DWORDS: a small initial proposal buffer, so tests
+            // exercise the overflow -> grow -> rerun path)
+            const char* tv = getenv("KNNG_TEST_DWORDS");
+            reserve_join(uint64_t(n) * 2 * cap,
+                         tv ? uint64_t(atoll(tv)) : uint64_t(n) * 4 * k * k);
         }
-        // pinned counter slot, cached per host thread (cudaMallocHost is slow)
-        thread_local IterCounters* pinned = nullptr;
-        if (!pinned) CK(cudaMallocHost(reinterpret_cast<void**>(&pinned), sizeof(IterCounters)));
-        h_ctr = pinned;
+        cur = ctr.p;
+        h_ctr = pinned_slots(1);
         CK(cudaMemsetAsync(ctr.p, 0, sizeof(IterCounters), s));
+    }
+    // pinned counter slots, cached per host thread (cudaMallocHost is slow)
+    static IterCounters* pinned_slots(size_t count) {
+        count = std::max<size_t>(count, 64);
+        thread_local IterCounters* pinned = nullptr;
+        thread_local size_t pinned_n = 0;
+        if (pinned_n < count) {
+            if (pinned) cudaFreeHost(pinned);
+            pinned = nullptr;
+            pinned_n = 0;
+            CK(cudaMallocHost(reinterpret_cast<void**>(&pinned), sizeof(IterCounters) * count));
+            pinned_n = count;
+        }
+        return pinned;
+    }
+    // one zeroed counter slot per iteration (slot i = iteration i), so that
+    // iterations can be enqueued ahead of the host's termination test
+    void ensure_slots(uint32_t count) {
+        if (count > slots) {
+            ctr.~DevBuf();
+            new (&ctr) DevBuf<IterCounters>();
+            ctr.alloc(count, pool, s);
+            slots = count;
+        }
+        CK(cudaMemsetAsync(ctr.p, 0, sizeof(IterCounters) * count, s));
+        cur = ctr.p;
+        h_ctr = pinned_slots(count);
     }
     ~Engine() {
         h_ctr = nullptr;  // the pinned slot is reused by the thread's next call
@@ -325,8 +368,9 @@ struct Engine {
         if (!src_on_device) h2d += sizeof(float) * size_t(n) * d;
     }
 
+    // the current slot's counters -> h_ctr[0]
     void read_counters() {
-        CK(cudaMemcpyAsync(h_ctr, ctr.p, sizeof(IterCounters), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(h_ctr, cur, sizeof(IterCounters), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         d2h += sizeof(IterCounters);
     }
@@ -336,14 +380,14 @@ struct Engine {
         const GraphView g = gv();
         const CandView c = cv();
         int h = timer.begin(KNNG_CUDA_KERNEL_DEGREE);
-        launch_indegree(g, indeg.p, s);
-        launch_reset_raw(c, n, s);
+        launch_indegree(g, indeg.p, s, cur);
+        launch_reset_raw(c, n, s, cur);
         timer.end(h);
         h = timer.begin(KNNG_CUDA_KERNEL_SAMPLE);
-        launch_sample(g, c, indeg.p, seed, s);
+        launch_sample(g, c, indeg.p, seed, s, cur);
         timer.end(h);
         h = timer.begin(KNNG_CUDA_KERNEL_FINALIZE);
-        launch_finalize(g, c, active.p, ctr.p, s, seed);
+        launch_finalize(g, c, active.p, cur, s, seed);
         timer.end(h);
         CK(cudaGetLastError());
     }
@@ -354,10 +398,7 @@ struct Engine {
     // read; when the distance blocks outgrew their buffer (the stages skipped
     // themselves) the buffer grows and the stages run again.
     void join(KernelTimer& timer, bool distances_only = false) {
-        int h = timer.begin(KNNG_CUDA_KERNEL_INDEX);
-        launch_join_offsets(cv(), n, scan_tmp.p, scan_bytes, s);
-        timer.end(h);
-        join_stages(timer, distances_only);
+        join_enqueue(timer, distances_only);
         read_counters();
         if (h_ctr->screened && getenv("KNNG_TC_STATS"))
             fprintf(stderr, "[knng] iteration %u screened join: %llu pairs, %llu exact (%.4f)\n",
@@ -365,20 +406,28 @@ struct Engine {
                     double(h_ctr->survivors) / double(h_ctr->screened));
         if (h_ctr->overflow) {
             reserve_join(h_ctr->rev, h_ctr->dwords);
-            CK(cudaMemsetAsync(&ctr.p->overflow, 0, sizeof(uint32_t), s));
+            CK(cudaMemsetAsync(&cur->overflow, 0, sizeof(uint32_t), s));
             join_stages(timer, distances_only);
             read_counters();
         }
     }
 
-    void join_stages(KernelTimer& timer, bool distances_only) {
-        launch_check_capacity(ctr.p, d_cap, s);
+    // the join's launches, no host round trip
+    void join_enqueue(KernelTimer& timer, bool distances_only = false) {
         int h = timer.begin(KNNG_CUDA_KERNEL_INDEX);
-        launch_scatter_rev(cv(), active.p, ctr.p, n, n, s);
+        launch_join_offsets(cv(), n, scan_tmp.p, scan_bytes, s);
+        timer.end(h);
+        join_stages(timer, distances_only);
+    }
+
+    void join_stages(KernelTimer& timer, bool distances_only) {
+        launch_check_capacity(cur, d_cap, s);
+        int h = timer.begin(KNNG_CUDA_KERNEL_INDEX);
+        launch_scatter_rev(cv(), active.p, cur, n, n, s);
         timer.end(h);
         h = timer.begin(KNNG_CUDA_KERNEL_JOIN);
         if (use_u8_join()) {
-            launch_join_u8(gv(), cv(), ctr.p, n, packed.p, lnorm.p, s);
+            launch_join_u8(gv(), cv(), cur, n, packed.p, lnorm.p, s);
         } else if (use_screened_join(distances_only)) {
             if (!norms_valid) {
                 if (!nrm2.p) {
@@ -390,15 +439,15 @@ struct Engine {
                 launch_row_norms(data.p, n, stride, nrm2.p, nrmu.p, s);
                 norms_valid = true;
             }
-            launch_join_tc(gv(), cv(), ctr.p, n, nrm2.p, nrmu.p, ovf.p, octr.p, s);
+            launch_join_tc(gv(), cv(), cur, n, nrm2.p, nrmu.p, ovf.p, octr.p, s);
         } else {
-            launch_join_distances(gv(), cv(), active.p, ctr.p, n, s);
+            launch_join_distances(gv(), cv(), active.p, cur, n, s);
         }
         timer.end(h);
         CK(cudaGetLastError());
         if (distances_only) return;
         h = timer.begin(KNNG_CUDA_KERNEL_MERGE);
-        launch_join_merge(gv(), cv(), ctr.p, s);
+        launch_join_merge(gv(), cv(), cur, s);
         timer.end(h);
         CK(cudaGetLastError());
     }
@@ -554,31 +603,103 @@ void run_engine(Engine& e, const float* data, bool data_on_device, const knng_cu
     metrics_push(m, 0, t1 - t0, uint64_t(e.n) * e.k, 0);
 
     const double threshold = p.termination_delta * double(e.n) * double(e.k);
-    for (uint32_t iter = 1; iter <= p.max_iterations; ++iter) {
-        t0 = now_s();
-        const uint64_t iter_seed = master();
-        e.iteration = iter;
-        CK(cudaMemsetAsync(e.ctr.p, 0, sizeof(IterCounters), e.s));
-        e.select(iter_seed, timer);
-        e.join(timer);  // ends with the iteration's counter read
-        const IterCounters c = *e.h_ctr;
-        // the locality reorder runs once, after iteration reorder_after_iteration
-        // (descent.hpp:230-235); the rest of the run works in permuted ids
-        if (p.reorder && !reordered && iter == p.reorder_after_iteration) {
-            const int h = timer.begin(KNNG_CUDA_KERNEL_REORDER);
-            e.reorder();
-            timer.end(h);
-            reordered = true;
+    // Iterations are enqueued in batches without a host round trip: each ends
+    // with iter_end_kernel, which applies the termination test
+    // (descent.hpp:242) on the device and sets the next slot's halt flag, so
+    // iterations enqueued past termination do nothing and leave the graph as
+    // the reference's loop leaves it.  The host reads the batch's counters
+    // once; per-iteration wall time is device time between iteration events.
+    // A batch ends at the reorder iteration (host work follows it).  When an
+    // iteration's proposal blocks outgrew their buffer (its later iterations
+    // halted too), the buffer grows, that iteration's join reruns, and
+    // enqueueing resumes after it.  KNNG_ITER_BATCH=1 restores one round trip
+    // per iteration.
+    const char* bv = getenv("KNNG_ITER_BATCH");
+    const uint32_t batch = bv && atoi(bv) > 0 ? uint32_t(atoi(bv)) : 4u;
+    const uint32_t T = p.max_iterations;
+    e.ensure_slots(T + 2);
+    std::vector<uint64_t> seeds(T + 1);
+    for (uint32_t i = 1; i <= T; ++i) seeds[i] = master();  // the reference's order
+    thread_local std::vector<cudaEvent_t> iev;
+    while (iev.size() < T + 2) {
+        cudaEvent_t ev;
+        CK(cudaEventCreate(&ev));
+        iev.push_back(ev);
+    }
+    uint32_t it = 1;
+    bool done = false;
+    while (!done && it <= T) {
+        uint32_t last = std::min(T, it + batch - 1);
+        if (p.reorder && !reordered && p.reorder_after_iteration >= it &&
+            p.reorder_after_iteration <= last)
+            last = p.reorder_after_iteration;
+        for (uint32_t j = it; j <= last; ++j) {
+            e.cur = e.ctr.p + j;
+            e.iteration = j;
+            timer.tag = j;
+            CK(cudaEventRecord(iev[j], e.s));
+            e.select(seeds[j], timer);
+            e.join_enqueue(timer);
+            launch_iter_end(e.cur, e.cur + 1, threshold, e.s);
         }
+        CK(cudaEventRecord(iev[last + 1], e.s));
+        CK(cudaMemcpyAsync(e.h_ctr + it, e.ctr.p + it, sizeof(IterCounters) * (last - it + 1),
+                           cudaMemcpyDeviceToHost, e.s));
+        e.d2h += sizeof(IterCounters) * (last - it + 1);
         CK(cudaStreamSynchronize(e.s));
-        timer.flush();
-        t1 = now_s();
-        metrics_push(m, iter, t1 - t0, c.evals, c.changes, c.cands, timer.last_join_ms);
-        if (m) {
-            m->join_candidates += c.cands;
-            m->join_evals += c.evals;
+        uint32_t next = last + 1;
+        for (uint32_t j = it; j <= last; ++j) {
+            IterCounters c = e.h_ctr[j];
+            if (c.halt) {  // defensive: the previous iteration's test already stopped the run
+                done = true;
+                break;
+            }
+            float ms = 0.0f;
+            CK(cudaEventElapsedTime(&ms, iev[j], iev[j + 1]));
+            double wall = 1e-3 * ms;
+            if (c.overflow) {
+                const double r0 = now_s();
+                e.cur = e.ctr.p + j;
+                e.iteration = j;
+                timer.tag = j;
+                e.reserve_join(c.rev, c.dwords);
+                CK(cudaMemsetAsync(&e.cur->overflow, 0, sizeof(uint32_t), e.s));
+                e.join_stages(timer, false);
+                e.read_counters();
+                c = e.h_ctr[0];
+                // the later slots of this batch ran halted: reset them
+                CK(cudaMemsetAsync(e.ctr.p + j + 1, 0, sizeof(IterCounters) * (T + 1 - j), e.s));
+                launch_iter_end(e.cur, e.cur + 1, threshold, e.s);
+                wall += now_s() - r0;
+                next = j + 1;
+            }
+            timer.flush();
+            metrics_push(m, j, wall, c.evals, c.changes, c.cands, timer.join_ms_of(j));
+            if (m) {
+                m->join_candidates += c.cands;
+                m->join_evals += c.evals;
+            }
+            // the locality reorder runs once, after iteration reorder_after_iteration
+            // (descent.hpp:230-235); the rest of the run works in permuted ids
+            if (p.reorder && !reordered && j == p.reorder_after_iteration) {
+                const double r0 = now_s();
+                const int h = timer.begin(KNNG_CUDA_KERNEL_REORDER);
+                e.reorder();
+                timer.end(h);
+                reordered = true;
+                CK(cudaStreamSynchronize(e.s));
+                timer.flush();
+                if (m && m->iterations && m->n_rows > 0 && m->n_rows <= m->capacity)
+                    m->iterations[m->n_rows - 1].wall_time_s += now_s() - r0;
+                if (m) m->total_wall_time_s += now_s() - r0;
+            }
+            if (double(c.changes) < threshold) {
+                done = true;
+                break;
+            }
+            if (next == j + 1) break;  // resume enqueueing after the rerun iteration
         }
-        if (double(c.changes) < threshold) break;
+        it = next;
     }
     if (reordered) {
         // back to the caller's ids (descent.hpp:245)

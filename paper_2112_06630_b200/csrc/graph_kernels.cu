@@ -199,9 +199,9 @@ __global__ void export_rows_kernel(GraphView g, uint32_t* ids, float* dists, uin
     }
 }
 
-__global__ void indegree_kernel(GraphView g, uint32_t* indeg) {
+__global__ void indegree_kernel(GraphView g, uint32_t* indeg, const IterCounters* gate) {
     const size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (e >= size_t(g.n) * g.k) return;
+    if (e >= size_t(g.n) * g.k || (gate && gate->halt)) return;
     atomicAdd(indeg + key_id(g.keys[e]), 1u);
 }
 
@@ -237,9 +237,9 @@ __device__ __forceinline__ void offer(const CandView& c, uint32_t k, const uint3
 
 __global__ void __launch_bounds__(256) sample_kernel(GraphView g, CandView c,
                                                      const uint32_t* indeg, uint32_t seed_lo,
-                                                     uint32_t seed_hi) {
+                                                     uint32_t seed_hi, const IterCounters* gate) {
     const size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (e >= size_t(g.n) * g.k) return;
+    if (e >= size_t(g.n) * g.k || (gate && gate->halt)) return;
     const uint32_t u = uint32_t(e / g.k), i = uint32_t(e % g.k);
     const uint32_t v = key_id(g.keys[e]);
     const uint32_t is_new = (__ldg(g.flags + u) >> i) & 1u;
@@ -251,9 +251,9 @@ __global__ void __launch_bounds__(256) sample_kernel(GraphView g, CandView c,
     if (v >= g.lo && v < g.hi) offer(c, g.k, indeg, v, u, is_new, r.z, r.w);  // u into v
 }
 
-__global__ void reset_raw_kernel(CandView c, uint32_t n) {
+__global__ void reset_raw_kernel(CandView c, uint32_t n, const IterCounters* gate) {
     const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
-    if (u >= n) return;
+    if (u >= n || (gate && gate->halt)) return;
     c.raw_new[u] = 0u;
     c.raw_old[u] = 0u;
 }
@@ -336,6 +336,7 @@ __global__ void __launch_bounds__(kFinWarps * 32, 8) finalize_kernel(GraphView g
     __shared__ uint32_t s_old[kFinWarps][kMaxCap];
     __shared__ uint32_t s_hid[kFinWarps][kMaxK];
     __shared__ BlockCounters acc;
+    if (ctr->halt) return;  // past termination: the graph is final
     init_block_counters(acc);
     const uint32_t w = threadIdx.x >> 5, lane = lane_id();
     const uint32_t cap = c.cap, k = g.k;
@@ -574,6 +575,7 @@ __global__ void __launch_bounds__(kFinWarps * 32, 4) finalize_det_kernel(GraphVi
     __shared__ uint8_t s_kill[kFinWarps][128];
     __shared__ uint32_t s_hid[kFinWarps][kMaxK];
     __shared__ BlockCounters acc;
+    if (ctr->halt) return;  // past termination: the graph is final
     init_block_counters(acc);
     const uint32_t w = threadIdx.x >> 5, lane = lane_id();
     const uint32_t cap = c.cap, k = g.k;
@@ -660,24 +662,41 @@ void launch_export_rows(const GraphView& g, uint32_t* ids, float* dists, uint8_t
     export_rows_kernel<<<blocks_for(size_t(g.n) * g.k, 256), 256, 0, s>>>(g, ids, dists, flags);
 }
 
-void launch_indegree(const GraphView& g, uint32_t* indeg, cudaStream_t s) {
+void launch_indegree(const GraphView& g, uint32_t* indeg, cudaStream_t s,
+                     const IterCounters* gate) {
     cudaMemsetAsync(indeg, 0, sizeof(uint32_t) * g.n, s);
-    indegree_kernel<<<blocks_for(size_t(g.n) * g.k, 256), 256, 0, s>>>(g, indeg);
+    indegree_kernel<<<blocks_for(size_t(g.n) * g.k, 256), 256, 0, s>>>(g, indeg, gate);
 }
 
-void launch_reset_raw(const CandView& c, uint32_t n, cudaStream_t s) {
-    reset_raw_kernel<<<blocks_for(n, 256), 256, 0, s>>>(c, n);
+void launch_reset_raw(const CandView& c, uint32_t n, cudaStream_t s, const IterCounters* gate) {
+    reset_raw_kernel<<<blocks_for(n, 256), 256, 0, s>>>(c, n, gate);
 }
 
 void launch_sample(const GraphView& g, const CandView& c, const uint32_t* indeg, uint64_t seed,
-                   cudaStream_t s) {
+                   cudaStream_t s, const IterCounters* gate) {
     sample_kernel<<<blocks_for(size_t(g.n) * g.k, 256), 256, 0, s>>>(
-        g, c, indeg, uint32_t(seed), uint32_t(seed >> 32));
+        g, c, indeg, uint32_t(seed), uint32_t(seed >> 32), gate);
+}
+
+__global__ void iter_end_kernel(const IterCounters* cur, IterCounters* next, double threshold) {
+    next->halt = (cur->halt || cur->overflow || double(cur->changes) < threshold) ? 1u : 0u;
+}
+
+void launch_iter_end(const IterCounters* cur, IterCounters* next, double threshold,
+                     cudaStream_t s) {
+    iter_end_kernel<<<1, 1, 0, s>>>(cur, next, threshold);
+}
+
+// revcnt <- 0 unless the iteration is halted: a halted iteration must not
+// clear the reverse counts an overflowed earlier iteration's rerun still needs
+__global__ void zero_revcnt_kernel(uint32_t* revcnt, uint32_t n, const IterCounters* gate) {
+    const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u < n && !gate->halt) revcnt[u] = 0u;
 }
 
 void launch_finalize(const GraphView& g, const CandView& c, uint32_t* active,
                      IterCounters* ctr, cudaStream_t s, uint64_t seed) {
-    cudaMemsetAsync(c.revcnt, 0, sizeof(uint32_t) * g.n, s);
+    zero_revcnt_kernel<<<blocks_for(g.n, 256), 256, 0, s>>>(c.revcnt, g.n, ctr);
     if (g.hi <= g.lo) return;
     if (c.det) {
         finalize_det_kernel<<<blocks_for(g.hi - g.lo, kFinNodes), kFinWarps * 32, 0, s>>>(

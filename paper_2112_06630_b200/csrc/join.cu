@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(kThreads, KNNG_JOIN_MINBLOCKS) join_distances_
     DistShared& sh = *reinterpret_cast<DistShared*>(smem_raw);
     const uint32_t tid = threadIdx.x, group = tid >> 3, l8 = tid & 7u;
     const uint32_t stride = g.stride, cap = c.cap;
-    if (ctr->overflow) return;
+    if (ctr->overflow || ctr->halt) return;
     const uint32_t n_active = ctr->active;
     const uint32_t n_slabs = (stride + kSlab - 1) / kSlab;
     const bool resident = res_slots != 0;
@@ -913,7 +913,7 @@ __global__ void __launch_bounds__(kMergeWarps * 32, KNNG_MERGE_MINBLOCKS) join_m
     // uneven; finished warps leave at once): the last warp out flushes
     __shared__ unsigned long long s_changes;
     __shared__ uint32_t s_done;
-    if (ctr->overflow) return;
+    if (ctr->overflow || ctr->halt) return;
     if (threadIdx.x == 0) {
         s_changes = 0;
         s_done = 0;
@@ -970,7 +970,7 @@ __global__ void __launch_bounds__(kMergeWarps * 32) hub_merge_kernel(GraphView g
                                                                     const uint32_t* hubs) {
     __shared__ unsigned long long s_keys[kMergeWarps][32];
     __shared__ uint32_t s_fresh[kMergeWarps];
-    if (ctr->overflow) return;
+    if (ctr->overflow || ctr->halt) return;
     const uint32_t lane = lane_id(), w = threadIdx.x >> 5, k = g.k;
     const uint32_t nh = ctr->hubs;
     for (uint32_t h = blockIdx.x; h < nh; h += gridDim.x) {
@@ -1141,7 +1141,7 @@ template <bool kWrite>
 __global__ void __launch_bounds__(kMergeWarps * 32) export_remote_kernel(
     GraphView g, CandView c, IterCounters* ctr, uint32_t* counts, const uint64_t* offsets,
     uint32_t* records) {
-    if (ctr->overflow) return;
+    if (ctr->overflow || ctr->halt) return;
     const uint32_t lane = lane_id();
     const uint32_t t = blockIdx.x * kMergeWarps + (threadIdx.x >> 5);
     if (t >= g.n) return;

@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(kAThreads, 1) join_tc_kernel(GraphView g, Cand
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
-    if (ctr->overflow) return;  // the proposal blocks outgrew their buffer
+    if (ctr->overflow || ctr->halt) return;  // the proposal blocks outgrew their buffer
     const uint32_t n_active = ctr->active;
 
     if (tid >= kAGroups * kAGroupThreads) {

@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(kUWarps * 32, KNNG_U8_MINB) join_u8_kernel(Gra
     __shared__ U8Warp shw[kUWarps];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
     U8Warp& W = shw[warp];
-    if (ctr->overflow) return;
+    if (ctr->overflow || ctr->halt) return;
     const uint32_t n_active = ctr->active, cap = c.cap;
     for (;;) {
         uint32_t a = 0;
@@ -464,7 +464,7 @@ __global__ void __launch_bounds__(kSWarps * 32, 2)
     S.rid = rid;
     S.rmx = rmx;
     S.rowcnt = rowcnt;
-    if (ctr->overflow) return;
+    if (ctr->overflow || ctr->halt) return;
     const uint32_t n_active = ctr->active, lane = tid & 31u;
     const float inf = __int_as_float(0x7f800000);
     // work queue: warp 0 claims 32 active indices at a time and keeps the

@@ -68,6 +68,8 @@ struct IterCounters {
     uint32_t overflow;           // distance blocks exceed the buffer: join skipped
     uint32_t hubs;               // merge: targets left to the per-CTA hub merge
     uint32_t work2;              // second work counter (byte-valued join: staged nodes)
+    uint32_t halt;               // set by iter_end_kernel: an earlier iteration met the
+                                 // termination test (or overflowed); this one is a no-op
     unsigned long long screened;   // screened join: pairs bounded
     unsigned long long survivors;  // screened join: pairs evaluated exactly
 };
@@ -81,16 +83,24 @@ void launch_load_rows(const GraphView& g, const uint32_t* ids, const float* dist
                       const uint8_t* flags, cudaStream_t s);
 void launch_export_rows(const GraphView& g, uint32_t* ids, float* dists, uint8_t* flags,
                         cudaStream_t s);
-void launch_indegree(const GraphView& g, uint32_t* indeg, cudaStream_t s);
+// gate (optional): the iteration's counters; the kernel does nothing when
+// gate->halt is set (iterations enqueued past termination, see run_engine)
+void launch_indegree(const GraphView& g, uint32_t* indeg, cudaStream_t s,
+                     const IterCounters* gate = nullptr);
 void launch_sample(const GraphView& g, const CandView& c, const uint32_t* indeg, uint64_t seed,
-                   cudaStream_t s);
+                   cudaStream_t s, const IterCounters* gate = nullptr);
 // dedup + flag_consumed + join bookkeeping (active list, block sizes, reverse counts)
 void launch_finalize(const GraphView& g, const CandView& c, uint32_t* active,
                      IterCounters* ctr, cudaStream_t s, uint64_t seed = 0);
 // join bookkeeping only, for externally supplied candidate lists (fixed-state entries)
 void launch_bookkeeping(const GraphView& g, const CandView& c, uint32_t* active,
                         IterCounters* ctr, cudaStream_t s);
-void launch_reset_raw(const CandView& c, uint32_t n, cudaStream_t s);
+void launch_reset_raw(const CandView& c, uint32_t n, cudaStream_t s,
+                      const IterCounters* gate = nullptr);
+// next->halt = cur->halt | cur->overflow | (changes < threshold): the device-side
+// termination test (descent.hpp:242) that gates the iterations enqueued after cur
+void launch_iter_end(const IterCounters* cur, IterCounters* next, double threshold,
+                     cudaStream_t s);
 
 // --- join.cu ---------------------------------------------------------------
 // Exclusive scans dsz -> doff and revcnt -> roff (CUB); scratch sizing.

@@ -52,3 +52,30 @@ def test_recall_matches_reference(gpu, restated, kind, n, k, cap):
     assert np.all(np.diff(res.graph.dists, axis=1) >= 0)
     assert all(len(set(r)) == k for r in res.graph.ids.tolist())
     assert not np.any(res.graph.ids == np.arange(n)[:, None])
+
+
+@pytest.mark.parametrize("kind,n,k,cap", [("C1", 5000, 20, 20), ("C2", 3000, 20, 50)])
+def test_iteration_batching_is_invisible(gpu, monkeypatch, kind, n, k, cap):
+    """Iterations enqueued ahead of the host's termination test (run_engine,
+    KNNG_ITER_BATCH) and the overflow -> grow -> rerun path leave the build
+    exactly as one round trip per iteration does: same graph bits, same
+    per-iteration evaluations and changes, same stop iteration."""
+    data = make_data(kind, n, 5)
+    p = kg.RunParams(k=k, max_candidates=cap, seed=4, deterministic=True)
+    runs = {}
+    for tag, env in [("b1", {"KNNG_ITER_BATCH": "1"}), ("b4", {}), ("b3", {"KNNG_ITER_BATCH": "3"}),
+                     ("b32", {"KNNG_ITER_BATCH": "32"}),
+                     ("ovf", {"KNNG_ITER_BATCH": "4", "KNNG_TEST_DWORDS": "4096"})]:
+        for key in ("KNNG_ITER_BATCH", "KNNG_TEST_DWORDS"):
+            monkeypatch.delenv(key, raising=False)
+        for key, v in env.items():
+            monkeypatch.setenv(key, v)
+        runs[tag] = kg.run(data, p)
+    a = runs["b1"]
+    rows = [(it.iteration, it.dist_evals, it.changes) for it in a.metrics.iterations]
+    assert len(rows) > 3
+    for tag, r in runs.items():
+        assert np.array_equal(a.graph.ids, r.graph.ids), tag
+        assert np.array_equal(bits(a.graph.dists), bits(r.graph.dists)), tag
+        assert [(it.iteration, it.dist_evals, it.changes) for it in r.metrics.iterations] == rows, tag
+        assert r.metrics.total_dist_evals == a.metrics.total_dist_evals, tag
