@@ -427,6 +427,136 @@ __global__ void __launch_bounds__(kFinWarps * 32, 8) finalize_kernel(GraphView g
     flush_block_counters(acc, active, ctr);
 }
 
+// finalize with a per-warp open-addressing table instead of the O(cap^2)
+// shared-memory scans above (same rules, same outputs up to the order of the
+// compacted lists): every listed id is inserted once (old ids with bit 31
+// set; ids < 2^31), the lowest slot holding a key wins within a list
+// (atomicMin), an old id found among the new keys applies the forward-edge
+// rule, and flag_consumed probes the table.  KNNG_FIN_HASH=0 builds keep the
+// scan version for A/B.
+#ifndef KNNG_FIN_HASH
+#define KNNG_FIN_HASH 1
+#endif
+constexpr uint32_t kFinTab = 256;  // >= 4 kMaxCap keys at load <= 1/2
+constexpr uint32_t kFinEmpty = 0xffffffffu;
+constexpr uint32_t kFinDropped = 0x80000000u;  // s_first: the new copy lost to the old one
+
+__device__ __forceinline__ uint32_t fin_hash(uint32_t key) { return (key * 0x9E3779B1u) >> 24; }
+
+__global__ void __launch_bounds__(kFinWarps * 32, 8) finalize_hash_kernel(GraphView g, CandView c,
+                                                                       uint32_t* active,
+                                                                       IterCounters* ctr) {
+    __shared__ uint32_t s_key[kFinWarps][kFinTab];
+    __shared__ uint32_t s_first[kFinWarps][kFinTab];
+    __shared__ uint32_t s_hid[kFinWarps][kMaxK];
+    __shared__ BlockCounters acc;
+    if (ctr->halt) return;  // past termination: the graph is final
+    init_block_counters(acc);
+    const uint32_t w = threadIdx.x >> 5, lane = lane_id();
+    const uint32_t cap = c.cap, k = g.k;
+    uint32_t* const tkey = s_key[w];
+    uint32_t* const tfirst = s_first[w];
+    for (uint32_t it = 0; it < kFinNodesPerWarp; ++it) {
+        const uint32_t u = g.lo + (blockIdx.x * kFinNodesPerWarp + it) * kFinWarps + w;
+        if (u >= g.hi) break;
+        __syncwarp();  // the previous node's table is no longer read
+        for (uint32_t i = lane; i < kFinTab; i += 32) {
+            tkey[i] = kFinEmpty;
+            tfirst[i] = kFinEmpty;
+        }
+        const uint32_t nr = min(c.raw_new[u], cap), orr = min(c.raw_old[u], cap);
+        uint32_t* const list = c.ids + size_t(u) * 2 * cap;
+        // element e: 0 / 1 new slots lane / lane + 32, 2 / 3 old slots lane / lane + 32
+        uint32_t x[4], bkt[4];
+        bool keep[4];
+#pragma unroll
+        for (uint32_t e = 0; e < 4; ++e) {
+            const uint32_t p = lane + 32 * (e & 1u), cnt = e < 2 ? nr : orr;
+            keep[e] = p < cnt;
+            x[e] = keep[e] ? list[(e < 2 ? 0u : cap) + p] : 0u;
+            bkt[e] = 0;
+        }
+        const uint32_t hid = lane < k ? key_id(g.keys[size_t(u) * k + lane]) : kTomb;
+        s_hid[w][lane] = hid;
+        const uint32_t hflags = g.flags[u];
+        __syncwarp();
+#pragma unroll
+        for (uint32_t e = 0; e < 4; ++e) {
+            if (!keep[e]) continue;
+            const uint32_t key = x[e] | (e < 2 ? 0u : 0x80000000u);
+            uint32_t h = fin_hash(key);
+            for (;;) {
+                const uint32_t prev = atomicCAS(&tkey[h], kFinEmpty, key);
+                if (prev == kFinEmpty || prev == key) break;
+                h = (h + 1) & (kFinTab - 1);
+            }
+            bkt[e] = h;
+            atomicMin(&tfirst[h], lane + 32 * (e & 1u));
+        }
+        __syncwarp();
+        // within a list the first slot wins
+#pragma unroll
+        for (uint32_t e = 0; e < 4; ++e)
+            keep[e] = keep[e] && tfirst[bkt[e]] == lane + 32 * (e & 1u);
+        __syncwarp();
+        // across lists: the copy from the edge the reference visits first
+        // (forward edge u -> x iff u < x, selection.hpp:311-317)
+#pragma unroll
+        for (uint32_t e = 2; e < 4; ++e) {
+            if (!keep[e]) continue;
+            const uint32_t xv = x[e];
+            uint32_t h = fin_hash(xv);
+            uint32_t kk;
+            while ((kk = tkey[h]) != kFinEmpty && kk != xv) h = (h + 1) & (kFinTab - 1);
+            if (kk != xv) continue;
+            uint32_t f_fwd = 1u;
+            for (uint32_t i = 0; i < k; ++i)
+                if (s_hid[w][i] == xv) {
+                    f_fwd = (hflags >> i) & 1u;
+                    break;
+                }
+            const bool keep_new = (u < xv) ? (f_fwd != 0u) : (f_fwd == 0u);
+            if (keep_new)
+                keep[e] = false;
+            else
+                atomicOr(&tfirst[h], kFinDropped);
+        }
+        __syncwarp();
+#pragma unroll
+        for (uint32_t e = 0; e < 2; ++e)
+            keep[e] = keep[e] && !(tfirst[bkt[e]] & kFinDropped);
+        // compact both lists (slot order)
+        uint32_t nn = 0, no = 0;
+        const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+        for (uint32_t h = 0; h < 2; ++h) {
+            const uint32_t mn = __ballot_sync(0xffffffffu, keep[h]);
+            const uint32_t mo = __ballot_sync(0xffffffffu, keep[2 + h]);
+            if (keep[h]) list[nn + __popc(mn & lt)] = x[h];
+            if (keep[2 + h]) list[cap + no + __popc(mo & lt)] = x[2 + h];
+            nn += __popc(mn);
+            no += __popc(mo);
+        }
+        // flag_consumed: clear heap entries named by the final new list
+        bool named = false;
+        if (hid != kTomb) {
+            uint32_t h = fin_hash(hid);
+            uint32_t kk;
+            while ((kk = tkey[h]) != kFinEmpty && kk != hid) h = (h + 1) & (kFinTab - 1);
+            named = kk == hid && !(tfirst[h] & kFinDropped);
+        }
+        const uint32_t clear = __ballot_sync(0xffffffffu, named);
+        if (lane == 0) {
+            c.nc[u] = nn;
+            c.oc[u] = no;
+            g.flags[u] = hflags & ~clear;
+        }
+        __syncwarp();  // the compacted lists, read back by other lanes
+        join_bookkeeping(g, c, u, nn, no, acc);
+    }
+    flush_block_counters(acc, active, ctr);
+}
+
 // ---- deterministic mode ---------------------------------------------------
 
 // Bitonic sort of 32 E keys, E per lane (element E lane + r), ascending.
@@ -703,8 +833,13 @@ void launch_finalize(const GraphView& g, const CandView& c, uint32_t* active,
             g, c, active, ctr, uint32_t(seed), uint32_t(seed >> 32));
         return;
     }
+#if KNNG_FIN_HASH
+    finalize_hash_kernel<<<blocks_for(g.hi - g.lo, kFinNodes), kFinWarps * 32, 0, s>>>(g, c, active,
+                                                                                       ctr);
+#else
     finalize_kernel<<<blocks_for(g.hi - g.lo, kFinNodes), kFinWarps * 32, 0, s>>>(g, c, active,
                                                                                   ctr);
+#endif
 }
 
 void launch_bookkeeping(const GraphView& g, const CandView& c, uint32_t* active,

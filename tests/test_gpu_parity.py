@@ -193,9 +193,14 @@ def test_init_random_forced_complete_graph(gpu):
         assert sorted(g.ids[u].tolist()) == [v for v in range(3) if v != u]
 
 
-def test_select_soundness_and_flags(gpu, restated):
+@pytest.mark.parametrize("mixed", [False, True])
+def test_select_soundness_and_flags(gpu, restated, mixed):
     data = make_data("G24", 2000, 5)
     g0, _ = restated.init_random(data, 10, 99)
+    if mixed:
+        # half the entries old: both lists filled, ids offered to both lists
+        # exercise the cross-list rule
+        g0.flags[:] = (np.random.default_rng(3).random(g0.flags.shape) < 0.5).astype(g0.flags.dtype)
     cands, flags_after = kg.select_turbo(g0.ids, g0.dists, g0.flags, 25, 1234)
     n, k = g0.ids.shape
     nbr = [set() for _ in range(n)]
@@ -216,8 +221,11 @@ def test_select_soundness_and_flags(gpu, restated):
                 assert flags_after[u, i] == 0
             else:
                 assert flags_after[u, i] == g0.flags[u, i]
-    # initial graph: every edge is new, so old lists are empty
-    assert int(cands.old_counts.sum()) == 0
+    if mixed:
+        assert int(cands.old_counts.sum()) > 0 and int(cands.new_counts.sum()) > 0
+    else:
+        # initial graph: every edge is new, so old lists are empty
+        assert int(cands.old_counts.sum()) == 0
 
 
 def test_select_expectation(gpu, restated):
