@@ -38,6 +38,15 @@ __device__ __forceinline__ float group8_l2_scalar(const float* __restrict__ a,
     const uint32_t l8 = lane_id() & 7u;
     float acc = 0.0f;
     if (active) {
+#ifndef KNNG_INIT_UNROLL
+#define KNNG_INIT_UNROLL 8  // measured: C5 init 56 (1) / 40 (compiler) / 34.5 (8) / 41.6 (16) ms;
+                            // two pairs per group in one loop: 42.4 ms (not kept)
+#endif
+#if KNNG_INIT_UNROLL
+#define KNNG_PRAGMA_(x) _Pragma(#x)
+#define KNNG_PRAGMA(x) KNNG_PRAGMA_(x)
+        KNNG_PRAGMA(unroll KNNG_INIT_UNROLL)
+#endif
         for (uint32_t c = 0; c < stride; c += 8) {
             const float diff = __fsub_rn(__ldg(a + c + l8), __ldg(b + c + l8));
             acc = __fadd_rn(acc, __fmul_rn(diff, diff));
