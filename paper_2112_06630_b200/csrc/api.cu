@@ -239,6 +239,7 @@ struct Engine {
     DevBuf<uint64_t> dblocks;
     int filter = 1;  // join proposals prefiltered by the row maxima (0: keep all)
     bool det = false;            // deterministic mode (CandView::det)
+    bool indeg_inc = false;      // merges maintain indeg (CandView::indeg_inc)
     DevBuf<uint32_t> rawlist;    // its raw sampled lists, n x 4 cap
     size_t rev_cap = 0, d_cap = 0;
     DevBuf<IterCounters> ctr;    // slot 0, or one slot per iteration (ensure_slots)
@@ -341,7 +342,8 @@ struct Engine {
     CandView cv() const {
         return CandView{cap,   cand.p,   raw_new.p, raw_old.p, nc.p, oc.p, dsz.p,
                         doff.p, revcnt.p, roff.p,   rcur.p,    rev.p, dblocks.p, filter,
-                        cmax.p, arec.p, hubs.p, rawlist.p, det ? 1 : 0};
+                        cmax.p, arec.p, hubs.p, rawlist.p, det ? 1 : 0,
+                        indeg_inc ? indeg.p : nullptr};
     }
 
     void reserve_join(uint64_t rev_entries, uint64_t dwords) {
@@ -380,7 +382,10 @@ struct Engine {
         const GraphView g = gv();
         const CandView c = cv();
         int h = timer.begin(KNNG_CUDA_KERNEL_DEGREE);
-        launch_indegree(g, indeg.p, s, cur);
+        if (indeg_inc)
+            launch_indegree_gated(g, indeg.p, cur, s);  // recount only when cur->recount
+        else
+            launch_indegree(g, indeg.p, s, cur);
         launch_reset_raw(c, n, s, cur);
         timer.end(h);
         h = timer.begin(KNNG_CUDA_KERNEL_SAMPLE);
@@ -575,6 +580,13 @@ void metrics_push(knng_cuda_metrics* m, uint32_t iteration, double wall, uint64_
     m->total_changes += changes;
 }
 
+// Counter slot j's recount flag <- 1 (stream-ordered; pageable source is
+// copied before the call returns).
+void set_recount(Engine& e, uint32_t j) {
+    const uint32_t one = 1;
+    CK(cudaMemcpyAsync(&e.ctr.p[j].recount, &one, sizeof(uint32_t), cudaMemcpyHostToDevice, e.s));
+}
+
 // knng::run (descent.hpp:193-255) on one GPU; data already on the device or
 // on the host per data_on_device; outputs device pointers.
 void run_engine(Engine& e, const float* data, bool data_on_device, const knng_cuda_params& p,
@@ -614,10 +626,26 @@ void run_engine(Engine& e, const float* data, bool data_on_device, const knng_cu
     // halted too), the buffer grows, that iteration's join reruns, and
     // enqueueing resumes after it.  KNNG_ITER_BATCH=1 restores one round trip
     // per iteration.
+    // The merges keep indeg current while iterations change few rows; an
+    // iteration after one that changed more than 5% of the n·k entries
+    // recounts instead (KNNG_INDEG_INC=0: recount every iteration)
+    const char* iv = getenv("KNNG_INDEG_INC");
+    const char* fv = getenv("KNNG_INDEG_RECOUNT_FRAC");
+    const double frac = fv ? atof(fv) : 0.05;
+    const double recount_above = (iv && iv[0] == '0') ? -1.0 : frac * double(e.n) * double(e.k);
     const char* bv = getenv("KNNG_ITER_BATCH");
     const uint32_t batch = bv && atoi(bv) > 0 ? uint32_t(atoi(bv)) : 4u;
     const uint32_t T = p.max_iterations;
-    e.ensure_slots(T + 2);
+    e.ensure_slots(T + 3);
+    e.indeg_inc = true;
+    // iterations 1 and 2 recount (nothing counted yet / no change count to go by)
+    {
+        const uint32_t one = 1;
+        for (uint32_t j = 1; j <= 2; ++j)
+            CK(cudaMemcpyAsync(&e.ctr.p[j].recount, &one, sizeof(uint32_t),
+                               cudaMemcpyHostToDevice, e.s));
+        CK(cudaStreamSynchronize(e.s));
+    }
     std::vector<uint64_t> seeds(T + 1);
     for (uint32_t i = 1; i <= T; ++i) seeds[i] = master();  // the reference's order
     thread_local std::vector<cudaEvent_t> iev;
@@ -640,7 +668,7 @@ void run_engine(Engine& e, const float* data, bool data_on_device, const knng_cu
             CK(cudaEventRecord(iev[j], e.s));
             e.select(seeds[j], timer);
             e.join_enqueue(timer);
-            launch_iter_end(e.cur, e.cur + 1, threshold, e.s);
+            launch_iter_end(e.cur, e.cur + 1, threshold, recount_above, e.s);
         }
         CK(cudaEventRecord(iev[last + 1], e.s));
         CK(cudaMemcpyAsync(e.h_ctr + it, e.ctr.p + it, sizeof(IterCounters) * (last - it + 1),
@@ -667,9 +695,11 @@ void run_engine(Engine& e, const float* data, bool data_on_device, const knng_cu
                 e.join_stages(timer, false);
                 e.read_counters();
                 c = e.h_ctr[0];
-                // the later slots of this batch ran halted: reset them
-                CK(cudaMemsetAsync(e.ctr.p + j + 1, 0, sizeof(IterCounters) * (T + 1 - j), e.s));
-                launch_iter_end(e.cur, e.cur + 1, threshold, e.s);
+                // the later slots of this batch ran halted: reset them; the
+                // next iteration recounts the in-degree (always safe)
+                CK(cudaMemsetAsync(e.ctr.p + j + 1, 0, sizeof(IterCounters) * (T + 2 - j), e.s));
+                set_recount(e, j + 1);
+                launch_iter_end(e.cur, e.cur + 1, threshold, recount_above, e.s);
                 wall += now_s() - r0;
                 next = j + 1;
             }
@@ -687,6 +717,7 @@ void run_engine(Engine& e, const float* data, bool data_on_device, const knng_cu
                 e.reorder();
                 timer.end(h);
                 reordered = true;
+                set_recount(e, j + 1);  // ids renamed: recount
                 CK(cudaStreamSynchronize(e.s));
                 timer.flush();
                 if (m && m->iterations && m->n_rows > 0 && m->n_rows <= m->capacity)

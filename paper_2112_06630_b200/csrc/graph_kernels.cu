@@ -817,13 +817,32 @@ void launch_sample(const GraphView& g, const CandView& c, const uint32_t* indeg,
         g, c, indeg, uint32_t(seed), uint32_t(seed >> 32), gate);
 }
 
-__global__ void iter_end_kernel(const IterCounters* cur, IterCounters* next, double threshold) {
+__global__ void iter_end_kernel(const IterCounters* cur, IterCounters* next, double threshold,
+                                double recount_above) {
     next->halt = (cur->halt || cur->overflow || double(cur->changes) < threshold) ? 1u : 0u;
+    if (double(cur->changes) > recount_above) next[1].recount = 1u;
 }
 
 void launch_iter_end(const IterCounters* cur, IterCounters* next, double threshold,
-                     cudaStream_t s) {
-    iter_end_kernel<<<1, 1, 0, s>>>(cur, next, threshold);
+                     double recount_above, cudaStream_t s) {
+    iter_end_kernel<<<1, 1, 0, s>>>(cur, next, threshold, recount_above);
+}
+
+__global__ void indeg_zero_kernel(uint32_t* indeg, uint32_t n, const IterCounters* gate) {
+    const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u < n && gate->recount && !gate->halt) indeg[u] = 0u;
+}
+
+__global__ void indeg_count_kernel(GraphView g, uint32_t* indeg, const IterCounters* gate) {
+    const size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= size_t(g.n) * g.k || !gate->recount || gate->halt) return;
+    atomicAdd(indeg + key_id(g.keys[e]), 1u);
+}
+
+void launch_indegree_gated(const GraphView& g, uint32_t* indeg, const IterCounters* gate,
+                           cudaStream_t s) {
+    indeg_zero_kernel<<<blocks_for(g.n, 256), 256, 0, s>>>(indeg, g.n, gate);
+    indeg_count_kernel<<<blocks_for(size_t(g.n) * g.k, 256), 256, 0, s>>>(g, indeg, gate);
 }
 
 // revcnt <- 0 unless the iteration is halted: a halted iteration must not

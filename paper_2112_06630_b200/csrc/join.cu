@@ -895,6 +895,22 @@ __device__ __forceinline__ void merge_entries(const CandView& c, const uint64_t*
     }
 }
 
+// Incremental in-degree (CandView::indeg_inc): the ids that left row t
+// (initial row key0) lose one, the ids that came in (final row key) gain one.
+__device__ __forceinline__ void indeg_update(uint32_t* indeg, uint64_t key0, uint64_t key,
+                                             uint32_t k) {
+    const uint32_t lane = lane_id();
+    const uint32_t id0 = lane < k ? key_id(key0) : 0xffffffffu;
+    const uint32_t id1 = lane < k ? key_id(key) : 0xfffffffeu;
+    bool kept = false, had = false;
+    for (uint32_t j = 0; j < k; ++j) {
+        kept |= __shfl_sync(0xffffffffu, id1, j) == id0;
+        had |= __shfl_sync(0xffffffffu, id0, j) == id1;
+    }
+    if (lane < k && !kept) atomicSub(indeg + id0, 1u);
+    if (lane < k && !had) atomicAdd(indeg + id1, 1u);
+}
+
 // Targets named by more than kHubEntries reverse-index entries are left to
 // hub_merge_kernel (a whole CTA per target).
 #ifndef KNNG_MERGE_MINBLOCKS
@@ -936,8 +952,10 @@ __global__ void __launch_bounds__(kMergeWarps * 32, KNNG_MERGE_MINBLOCKS) join_m
         float cur_max = key_dist(__shfl_sync(0xffffffffu, key, k - 1));
         uint32_t inserted = 0;
         const uint32_t init_id = kDet ? key_id(key) : 0xffffffffu;
+        const uint64_t key0 = key;
         merge_entries<kDet>(c, c.rev + roff, cnt, k, key, flags, fresh, cur_max, inserted, init_id);
         if (inserted) {
+            if (c.indeg_inc && !ctr[1].recount) indeg_update(c.indeg_inc, key0, key, k);
             if (lane < k) g.keys[size_t(t) * k + lane] = key;
             if (lane == 0) {
                 g.flags[t] = flags;
@@ -984,6 +1002,7 @@ __global__ void __launch_bounds__(kHubWarps * 32) hub_merge_kernel(GraphView g, 
         const uint32_t b = uint32_t(uint64_t(cnt) * w / kHubWarps);
         const uint32_t e = uint32_t(uint64_t(cnt) * (w + 1) / kHubWarps);
         uint64_t key = lane < k ? g.keys[size_t(t) * k + lane] : kEmptyKey;
+        const uint64_t key0 = key;  // the initial row (incremental in-degree)
         uint32_t flags = g.flags[t], fresh = 0, inserted = 0;
         float cur_max = key_dist(__shfl_sync(0xffffffffu, key, k - 1));
         const uint32_t init_id = kDet ? key_id(key) : 0xffffffffu;
@@ -1009,6 +1028,7 @@ __global__ void __launch_bounds__(kHubWarps * 32) hub_merge_kernel(GraphView g, 
             const uint32_t kmask = k >= 32 ? 0xffffffffu : ((1u << k) - 1u);
             const uint32_t came = __popc(fresh & kmask);
             if (came || kDet) {
+                if (c.indeg_inc && !ctr[1].recount) indeg_update(c.indeg_inc, key0, key, k);
                 if (lane < k) g.keys[size_t(t) * k + lane] = key;
                 if (lane == 0) {
                     g.flags[t] = flags;

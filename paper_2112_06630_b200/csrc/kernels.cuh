@@ -54,6 +54,12 @@ struct CandView {
     // |final row \ initial row|
     uint32_t* raw;
     int det;
+    // in-degree kept up to date by the merges (single-GPU builds, counters
+    // in per-iteration slots): a merge that changes row t adds 1 for each id
+    // that came in and subtracts 1 for each id that left, unless the next
+    // iteration recounts (next slot's recount flag).  nullptr: recounted by
+    // indegree_kernel every iteration
+    uint32_t* indeg_inc;
 };
 
 // Device counters for one iteration.
@@ -70,6 +76,8 @@ struct IterCounters {
     uint32_t work2;              // second work counter (byte-valued join: staged nodes)
     uint32_t halt;               // set by iter_end_kernel: an earlier iteration met the
                                  // termination test (or overflowed); this one is a no-op
+    uint32_t recount;            // this iteration's selection recounts the in-degree; the
+                                 // previous iteration's merges then skip their updates
     unsigned long long screened;   // screened join: pairs bounded
     unsigned long long survivors;  // screened join: pairs evaluated exactly
 };
@@ -98,9 +106,15 @@ void launch_bookkeeping(const GraphView& g, const CandView& c, uint32_t* active,
 void launch_reset_raw(const CandView& c, uint32_t n, cudaStream_t s,
                       const IterCounters* gate = nullptr);
 // next->halt = cur->halt | cur->overflow | (changes < threshold): the device-side
-// termination test (descent.hpp:242) that gates the iterations enqueued after cur
+// termination test (descent.hpp:242) that gates the iterations enqueued after cur;
+// next[1].recount = cur->changes > recount_above (the iteration after next
+// recounts the in-degree when this one changed many rows: the incremental
+// updates would cost more atomics than the recount)
 void launch_iter_end(const IterCounters* cur, IterCounters* next, double threshold,
-                     cudaStream_t s);
+                     double recount_above, cudaStream_t s);
+// in-degree recount gated on gate->recount (and not halted)
+void launch_indegree_gated(const GraphView& g, uint32_t* indeg, const IterCounters* gate,
+                           cudaStream_t s);
 
 // --- join.cu ---------------------------------------------------------------
 // Exclusive scans dsz -> doff and revcnt -> roff (CUB); scratch sizing.

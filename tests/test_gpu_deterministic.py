@@ -54,19 +54,24 @@ def test_recall_matches_reference(gpu, restated, kind, n, k, cap):
     assert not np.any(res.graph.ids == np.arange(n)[:, None])
 
 
-@pytest.mark.parametrize("kind,n,k,cap", [("C1", 5000, 20, 20), ("C2", 3000, 20, 50)])
+@pytest.mark.parametrize("kind,n,k,cap", [("C1", 5000, 20, 20), ("C2", 3000, 20, 50),
+                                          ("C2", 8000, 20, 50), ("C3", 4000, 30, 50)])
 def test_iteration_batching_is_invisible(gpu, monkeypatch, kind, n, k, cap):
     """Iterations enqueued ahead of the host's termination test (run_engine,
-    KNNG_ITER_BATCH) and the overflow -> grow -> rerun path leave the build
+    KNNG_ITER_BATCH), the in-degree kept by the merges (KNNG_INDEG_INC) and
+    the overflow -> grow -> rerun path leave the build
     exactly as one round trip per iteration does: same graph bits, same
     per-iteration evaluations and changes, same stop iteration."""
     data = make_data(kind, n, 5)
     p = kg.RunParams(k=k, max_candidates=cap, seed=4, deterministic=True)
     runs = {}
-    for tag, env in [("b1", {"KNNG_ITER_BATCH": "1"}), ("b4", {}), ("b3", {"KNNG_ITER_BATCH": "3"}),
+    # b1: one round trip per iteration and the in-degree recounted every
+    # iteration (the most literal driver); the others keep it incrementally
+    for tag, env in [("b1", {"KNNG_ITER_BATCH": "1", "KNNG_INDEG_INC": "0"}), ("b4", {}),
+                     ("b3", {"KNNG_ITER_BATCH": "3"}), ("b4full", {"KNNG_INDEG_INC": "0"}),
                      ("b32", {"KNNG_ITER_BATCH": "32"}),
                      ("ovf", {"KNNG_ITER_BATCH": "4", "KNNG_TEST_DWORDS": "4096"})]:
-        for key in ("KNNG_ITER_BATCH", "KNNG_TEST_DWORDS"):
+        for key in ("KNNG_ITER_BATCH", "KNNG_TEST_DWORDS", "KNNG_INDEG_INC"):
             monkeypatch.delenv(key, raising=False)
         for key, v in env.items():
             monkeypatch.setenv(key, v)
