@@ -1231,7 +1231,13 @@ int knng_cuda_shard_create(const float* d_data, uint32_t n, uint32_t d,
             e.lo = std::min(n, rank * sh->chunk);
             e.hi = std::min(n, (rank + 1) * sh->chunk);
             e.upload(d_data, true);
-            e.u8_state = 0;  // the sharded path keeps the FP32 join kernel
+            // byte-valued data: check and pack once here (KNNG_SHARD_U8=0
+            // keeps the FP32 join on the shards)
+            const char* sv = getenv("KNNG_SHARD_U8");
+            if (sv && sv[0] == '0')
+                e.u8_state = 0;
+            else
+                e.use_u8_join();
             sh->exp_counts.alloc(n, e.pool, e.s);
             sh->exp_off.alloc(n, e.pool, e.s);
             sh->rcnt.alloc(n, e.pool, e.s);

@@ -71,16 +71,18 @@ def test_shard_step_exports_nothing_with_one_rank(gpu, nccl_world):
     eng.close()
 
 
-def test_shard_engine_two_ranks_one_process_exchange(gpu):
+@pytest.mark.parametrize("kind", ["C1", "C2"])
+def test_shard_engine_two_ranks_one_process_exchange(gpu, kind):
     """Two shard engines of a 2-rank split in ONE process (no collectives,
     sequential kernels — nothing waits on another rank): records exported by
     each rank are exactly for the other rank's rows, and merging them gives a
-    graph whose recall matches the single-GPU build."""
+    graph whose recall matches the single-GPU build.  C2-shaped byte data
+    (first 12k rows) runs the shards' joins through the byte-valued kernel."""
     import torch
     from paper_2112_06630_b200.shard import GpuShardEngine, seed_sequence
-    cfg = datasets.CONFIGS["C1"]
-    data = datasets.generate(cfg)
-    n, k = cfg.n, cfg.k
+    cfg = datasets.CONFIGS[kind]
+    data = datasets.generate(cfg)[:12000]
+    n, k = data.shape[0], cfg.k
     params = kg.RunParams(k=k, max_candidates=cfg.cap, seed=0)
     dd = torch.from_numpy(data).cuda()
     engs = [GpuShardEngine(dd, params, r, 2) for r in range(2)]
