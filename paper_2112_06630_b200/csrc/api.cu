@@ -1286,7 +1286,9 @@ int knng_cuda_shard_init(knng_cuda_shard* sh, uint64_t seed) {
     return guarded([&] {
         if (!sh) raise(KNNG_CUDA_INVALID_ARGUMENT, "null shard");
         DeviceGuard dg(sh->device);
-        launch_init_random(sh->e->gv(), seed, sh->s);
+        const bool u8 = sh->e->u8_state == 1;  // byte copy made at creation
+        launch_init_random(sh->e->gv(), seed, sh->s, u8 ? sh->e->packed.p : nullptr,
+                           u8 ? sh->e->lnorm.p : nullptr);
         CK(cudaGetLastError());
         CK(cudaStreamSynchronize(sh->s));
     });
