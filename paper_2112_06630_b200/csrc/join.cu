@@ -826,6 +826,7 @@ __device__ __forceinline__ void merge_entries(const CandView& c, const uint64_t*
         for (uint32_t q = 0; q < kMergeMeta; ++q) {
             const uint32_t e = g0 + 32 * q + lane;
             pes[q] = e < cnt ? uint32_t(c.D[mrows[q]]) : 0u;
+            JCHECK(pes[q] <= 2 * c.cap, "merge row count", e, pes[q]);
         }
 #pragma unroll
         for (uint32_t q = 0; q < kMergeMeta; ++q) {
@@ -1184,6 +1185,7 @@ __global__ void __launch_bounds__(kMergeWarps * 32) export_remote_kernel(
     for (uint32_t e = 0; e < cnt; ++e) {
         const uint64_t* row = c.D + rv[e];
         const uint32_t P = uint32_t(row[0]);  // proposals kept for t in this join
+        JCHECK(P <= 2 * c.cap, "export_remote row count", t, P);
         for (uint32_t q0 = 0; q0 < P; q0 += 32) {
             const uint32_t q = q0 + lane;
             const uint64_t kk = q < P ? row[1 + q] : kEmptyKey;
@@ -1213,7 +1215,10 @@ __global__ void __launch_bounds__(kMergeWarps * 32) export_remote_kernel(
 // target merges its records with try_insert semantics.
 __global__ void recv_count_kernel(const uint32_t* records, uint64_t count, uint32_t* cnt) {
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i < count) atomicAdd(cnt + records[3 * i], 1u);
+    if (i < count) {
+        JCHECK(records[3 * i] < 0x7fffffffu, "recv_count target", uint32_t(i), records[3 * i]);
+        atomicAdd(cnt + records[3 * i], 1u);
+    }
 }
 
 __global__ void recv_scatter_kernel(const uint32_t* records, uint64_t count, const uint32_t* off,
@@ -1221,6 +1226,7 @@ __global__ void recv_scatter_kernel(const uint32_t* records, uint64_t count, con
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= count) return;
     const uint32_t t = records[3 * i];
+    JCHECK(t < 0x7fffffffu, "recv_scatter target", uint32_t(i), t);
     const uint32_t slot = off[t] + atomicAdd(cur + t, 1u);
     grouped[slot] = pack_key(__uint_as_float(records[3 * i + 2]), records[3 * i + 1]);
 }
