@@ -8,38 +8,44 @@ import paper_2112_06630_b200 as kg
 from paper_2112_06630_b200 import datasets
 from paper_2112_06630_b200.shard import GpuShardEngine, seed_sequence
 
-cfg = datasets.CONFIGS["C2"]
-data = datasets.generate(cfg)[: int(sys.argv[1]) if len(sys.argv) > 1 else 12000]
-n, k = data.shape[0], cfg.k
-params = kg.RunParams(k=k, max_candidates=cfg.cap, seed=0)
-dd = torch.from_numpy(data).cuda()
-engs = [GpuShardEngine(dd, params, r, 2) for r in range(2)]
-seeds = seed_sequence(0, 31)
-for e in engs:
-    e.init(int(seeds[0]))
-chunk = engs[0].chunk
+def split(kind):
+  cfg = datasets.CONFIGS[kind]
+  data = datasets.generate(cfg)[:12000]
+  n, k = data.shape[0], cfg.k
+  params = kg.RunParams(k=k, max_candidates=cfg.cap, seed=0)
+  dd = torch.from_numpy(data).cuda()
+  engs = [GpuShardEngine(dd, params, r, 2) for r in range(2)]
+  seeds = seed_sequence(0, 31)
+  for e in engs:
+      e.init(int(seeds[0]))
+  chunk = engs[0].chunk
 
 
-def allgather():
-    for buf, w in (("keys", k), ("flags", 1), ("maxd", 1)):
-        for r in range(2):
-            src = getattr(engs[r], buf)[r * chunk * w:(r + 1) * chunk * w]
-            getattr(engs[1 - r], buf)[r * chunk * w:(r + 1) * chunk * w].copy_(src)
-    torch.cuda.synchronize()
+  def allgather():
+      for buf, w in (("keys", k), ("flags", 1), ("maxd", 1)):
+          for r in range(2):
+              src = getattr(engs[r], buf)[r * chunk * w:(r + 1) * chunk * w]
+              getattr(engs[1 - r], buf)[r * chunk * w:(r + 1) * chunk * w].copy_(src)
+      torch.cuda.synchronize()
 
 
-allgather()
-for it in range(1, 31):
-    steps = []
-    for r, e in enumerate(engs):
-        print("step", it, "rank", r, flush=True)
-        steps.append(e.step(int(seeds[it])))
-    ch = 0
-    for r in range(2):
-        print("merge", it, "rank", r, "records", steps[1 - r]["send"].numel() // 3, flush=True)
-        ch += engs[r].merge(steps[1 - r]["send"].clone())
-    allgather()
-    print("iteration", it, "changes", ch, flush=True)
-    if ch < params.termination_delta * n * k:
-        break
+  allgather()
+  for it in range(1, 31):
+      steps = []
+      for r, e in enumerate(engs):
+          print("step", it, "rank", r, flush=True)
+          steps.append(e.step(int(seeds[it])))
+      ch = 0
+      for r in range(2):
+          print("merge", it, "rank", r, "records", steps[1 - r]["send"].numel() // 3, flush=True)
+          ch += engs[r].merge(steps[1 - r]["send"].clone())
+      allgather()
+      print("iteration", it, "changes", ch, flush=True)
+      if ch < params.termination_delta * n * k:
+          break
+
+
+for kind in (sys.argv[1:] or ["C2"]):
+    print("split", kind, flush=True)
+    split(kind)
 print("done")
