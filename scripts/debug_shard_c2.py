@@ -45,7 +45,13 @@ def split(kind):
           break
 
 
-for kind in (sys.argv[1:] or ["C2"]):
+for kind in [a for a in sys.argv[1:] if not a.startswith("--")] or ["C2"]:
     print("split", kind, flush=True)
     split(kind)
+    if "--run" in sys.argv:  # what the pytest case does after its split
+        d = datasets.generate(datasets.CONFIGS[kind])[:12000]
+        kg.brute_force_knng(d, datasets.CONFIGS[kind].k)
+        kg.run(d, kg.RunParams(k=datasets.CONFIGS[kind].k,
+                               max_candidates=datasets.CONFIGS[kind].cap, seed=0))
+        print("single-GPU run done", flush=True)
 print("done")
