@@ -240,7 +240,7 @@ struct Engine {
     int filter = 1;  // join proposals prefiltered by the row maxima (0: keep all)
     bool det = false;            // deterministic mode (CandView::det)
     bool indeg_inc = false;      // merges maintain indeg (CandView::indeg_inc)
-    DevBuf<uint32_t> rawlist;    // its raw sampled lists, n x 4 cap
+    DevBuf<unsigned long long> rawlist;  // its raw sampled lists (keys), n x 4 cap
     size_t rev_cap = 0, d_cap = 0;
     DevBuf<IterCounters> ctr;    // slot 0, or one slot per iteration (ensure_slots)
     IterCounters* cur = nullptr;  // the slot the kernels of the current iteration use
@@ -286,6 +286,9 @@ struct Engine {
             active.alloc(n, pool, s);
             dsz.alloc(n, pool, s);
             doff.alloc(n, pool, s);
+            // pool memory is recycled: rows outside a shard's range are never
+            // written, so start from zero
+            CK(cudaMemsetAsync(dsz.p, 0, sizeof(uint64_t) * n, s));
             cmax.alloc(size_t(n) * 2 * cap, pool, s);
             arec.alloc(n, pool, s);
             hubs.alloc(n, pool, s);
@@ -305,19 +308,36 @@ struct Engine {
         h_ctr = pinned_slots(1);
         CK(cudaMemsetAsync(ctr.p, 0, sizeof(IterCounters), s));
     }
-    // pinned counter slots, cached per host thread (cudaMallocHost is slow)
-    static IterCounters* pinned_slots(size_t count) {
+    // pinned counter slots: each Engine holds its own buffer, recycled
+    // through a per-thread free list (cudaMallocHost is slow); a buffer is
+    // never freed while an Engine still points at it
+    struct Pinned {
+        IterCounters* p = nullptr;
+        size_t n = 0;
+    };
+    static std::vector<Pinned>& pinned_free() {
+        thread_local std::vector<Pinned> list;
+        return list;
+    }
+    Pinned pin;
+    IterCounters* pinned_slots(size_t count) {
         count = std::max<size_t>(count, 64);
-        thread_local IterCounters* pinned = nullptr;
-        thread_local size_t pinned_n = 0;
-        if (pinned_n < count) {
-            if (pinned) cudaFreeHost(pinned);
-            pinned = nullptr;
-            pinned_n = 0;
-            CK(cudaMallocHost(reinterpret_cast<void**>(&pinned), sizeof(IterCounters) * count));
-            pinned_n = count;
-        }
-        return pinned;
+        if (pin.n >= count) return pin.p;
+        release_pinned();
+        auto& fl = pinned_free();
+        for (size_t i = 0; i < fl.size(); ++i)
+            if (fl[i].n >= count) {
+                pin = fl[i];
+                fl.erase(fl.begin() + long(i));
+                return pin.p;
+            }
+        CK(cudaMallocHost(reinterpret_cast<void**>(&pin.p), sizeof(IterCounters) * count));
+        pin.n = count;
+        return pin.p;
+    }
+    void release_pinned() {
+        if (pin.p) pinned_free().push_back(pin);
+        pin = Pinned{};
     }
     // one zeroed counter slot per iteration (slot i = iteration i), so that
     // iterations can be enqueued ahead of the host's termination test
@@ -333,7 +353,8 @@ struct Engine {
         h_ctr = pinned_slots(count);
     }
     ~Engine() {
-        h_ctr = nullptr;  // the pinned slot is reused by the thread's next call
+        h_ctr = nullptr;
+        release_pinned();  // back to this thread's free list for the next Engine
     }
 
     GraphView gv() const {
@@ -389,7 +410,7 @@ struct Engine {
         launch_reset_raw(c, n, s, cur);
         timer.end(h);
         h = timer.begin(KNNG_CUDA_KERNEL_SAMPLE);
-        launch_sample(g, c, indeg.p, seed, s, cur);
+        launch_sample(g, c, indeg.p, seed, s, cur, seed);
         timer.end(h);
         h = timer.begin(KNNG_CUDA_KERNEL_FINALIZE);
         launch_finalize(g, c, active.p, cur, s, seed);
@@ -420,7 +441,7 @@ struct Engine {
     // the join's launches, no host round trip
     void join_enqueue(KernelTimer& timer, bool distances_only = false) {
         int h = timer.begin(KNNG_CUDA_KERNEL_INDEX);
-        launch_join_offsets(cv(), n, scan_tmp.p, scan_bytes, s);
+        launch_join_offsets(cv(), n, lo, hi, scan_tmp.p, scan_bytes, s);
         timer.end(h);
         join_stages(timer, distances_only);
     }
@@ -1211,6 +1232,7 @@ int knng_cuda_shard_create(const float* d_data, uint32_t n, uint32_t d,
     return guarded([&] {
         if (!d_data || !params || !out || !info) raise(KNNG_CUDA_INVALID_ARGUMENT, "null argument");
         if (nranks == 0 || rank >= nranks) raise(KNNG_CUDA_INVALID_ARGUMENT, "bad rank / nranks");
+        if (nranks > 1023) raise(KNNG_CUDA_INVALID_ARGUMENT, "this build supports at most 1023 shards");
         const knng_cuda_params p = *params;
         validate_params(n, d, p);
         if (p.reorder)
@@ -1313,7 +1335,7 @@ int knng_cuda_shard_step(knng_cuda_shard* sh, uint64_t seed, uint64_t* out_count
         size_t bytes = sh->scan_bytes;
         cub::DeviceScan::ExclusiveScan(sh->scan_tmp.p, bytes, sh->exp_counts.p, sh->exp_off.p,
                                        cub::Sum(), uint64_t(0), int(e.n), e.s);
-        shard_bounds_kernel<<<1, 64, 0, e.s>>>(sh->exp_off.p, sh->exp_counts.p, e.n, sh->chunk,
+        shard_bounds_kernel<<<1, sh->nranks + 1, 0, e.s>>>(sh->exp_off.p, sh->exp_counts.p, e.n, sh->chunk,
                                                sh->nranks, sh->bounds.p);
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(sh->h_bounds.data(), sh->bounds.p, sizeof(uint64_t) * (sh->nranks + 1),

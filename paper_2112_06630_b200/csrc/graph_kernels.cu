@@ -221,18 +221,41 @@ __global__ void indegree_kernel(GraphView g, uint32_t* indeg, const IterCounters
 // slot with reservoir probability cap/(seen) (the reference overwrites a
 // uniform slot unconditionally; both keep the list a random subset).
 // Duplicates are removed by finalize.
+// Pair weight of candidate x offered to u in list `kind` (order-free).
+__device__ __forceinline__ uint32_t det_weight(uint32_t u, uint32_t x, uint32_t kind,
+                                               uint32_t seed_lo, uint32_t seed_hi) {
+    return philox4x32_10(u, x, kind, kSaltDet, seed_lo, seed_hi).x;
+}
+
+__device__ __forceinline__ unsigned long long det_key(uint32_t target, uint32_t cand,
+                                                      uint32_t is_new, uint32_t seed_lo,
+                                                      uint32_t seed_hi) {
+    return (uint64_t(det_weight(target, cand, is_new ? 1u : 2u, seed_lo, seed_hi)) << 32) | cand;
+}
+
+// turbo acceptance (selection.hpp:297-298): min(1, cap / deg), deg = k + in-degree
+__device__ __forceinline__ bool accept_offer(const CandView& c, uint32_t k, const uint32_t* indeg,
+                                             uint32_t target, uint32_t r_accept) {
+    const uint32_t deg = k + __ldg(indeg + target);
+    return !(deg > c.cap && uint64_t(r_accept) * deg >= (uint64_t(c.cap) << 32));
+}
+
 __device__ __forceinline__ void offer(const CandView& c, uint32_t k, const uint32_t* indeg,
                                       uint32_t target, uint32_t cand, uint32_t is_new,
-                                      uint32_t r_accept, uint32_t r_slot) {
-    const uint32_t deg = k + __ldg(indeg + target);
-    if (deg > c.cap && uint64_t(r_accept) * deg >= (uint64_t(c.cap) << 32)) return;
+                                      uint32_t r_accept, uint32_t r_slot, uint32_t seed_lo,
+                                      uint32_t seed_hi, IterCounters* ctr) {
+    if (!accept_offer(c, k, indeg, target, r_accept)) return;
     uint32_t* counter = is_new ? c.raw_new : c.raw_old;
     const uint32_t slot = atomicAdd(counter + target, 1u);
     if (c.det) {
-        // every accepted offer (the expected count is <= cap; 2 cap slots),
-        // kept or cut by finalize on its pair weight, not on arrival order
+        // every accepted offer (the expected count is <= cap; 2 cap slots);
+        // which ones stay is decided on pair weights, not on arrival order:
+        // an overflowing list is rebuilt by det_fix_* after this kernel
         if (slot < 2 * c.cap)
-            c.raw[size_t(target) * 4 * c.cap + (is_new ? 0u : 2 * c.cap) + slot] = cand;
+            c.raw[size_t(target) * 4 * c.cap + (is_new ? 0u : 2 * c.cap) + slot] =
+                det_key(target, cand, is_new, seed_lo, seed_hi);
+        else if (slot == 2 * c.cap)
+            ctr->det_ovf = 1u;
         return;
     }
     uint32_t* list = c.ids + size_t(target) * 2 * c.cap + (is_new ? 0u : c.cap);
@@ -246,9 +269,10 @@ __device__ __forceinline__ void offer(const CandView& c, uint32_t k, const uint3
 
 __global__ void __launch_bounds__(256) sample_kernel(GraphView g, CandView c,
                                                      const uint32_t* indeg, uint32_t seed_lo,
-                                                     uint32_t seed_hi, const IterCounters* gate) {
+                                                     uint32_t seed_hi, IterCounters* gate,
+                                                     uint32_t det_lo, uint32_t det_hi) {
     const size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (e >= size_t(g.n) * g.k || (gate && gate->halt)) return;
+    if (e >= size_t(g.n) * g.k || gate->halt) return;
     const uint32_t u = uint32_t(e / g.k), i = uint32_t(e % g.k);
     const uint32_t v = key_id(g.keys[e]);
     const uint32_t is_new = (__ldg(g.flags + u) >> i) & 1u;
@@ -256,8 +280,67 @@ __global__ void __launch_bounds__(256) sample_kernel(GraphView g, CandView c,
                                     seed_hi);
     // only lists this device owns are built; the draws are per edge, so the
     // sampled lists do not depend on how the rows are sharded
-    if (u >= g.lo && u < g.hi) offer(c, g.k, indeg, u, v, is_new, r.x, r.y);  // v into u
-    if (v >= g.lo && v < g.hi) offer(c, g.k, indeg, v, u, is_new, r.z, r.w);  // u into v
+    if (u >= g.lo && u < g.hi)
+        offer(c, g.k, indeg, u, v, is_new, r.x, r.y, det_lo, det_hi, gate);  // v into u
+    if (v >= g.lo && v < g.hi)
+        offer(c, g.k, indeg, v, u, is_new, r.z, r.w, det_lo, det_hi, gate);  // u into v
+}
+
+// Deterministic sampling, lists that received more than 2cap offers: the
+// slots are reset, then every accepted offer into such a list is inserted
+// again into a lock-free bounded set of the 2cap smallest keys (a key only
+// replaces the current maximum; slot values only decrease, so a successful
+// CAS on the scanned maximum removes the true maximum).  The result is a
+// function of the set of offers, whatever the arrival order.
+__global__ void det_fix_reset_kernel(GraphView g, CandView c, const IterCounters* gate) {
+    const uint32_t u = g.lo + blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= g.hi || !gate->det_ovf || gate->halt) return;
+    const uint32_t cap2 = 2 * c.cap;
+    unsigned long long* raw = c.raw + size_t(u) * 4 * c.cap;
+    if (c.raw_new[u] > cap2)
+        for (uint32_t i = 0; i < cap2; ++i) raw[i] = ~0ull;
+    if (c.raw_old[u] > cap2)
+        for (uint32_t i = 0; i < cap2; ++i) raw[cap2 + i] = ~0ull;
+}
+
+__device__ __forceinline__ void det_fix_offer(const CandView& c, uint32_t k, const uint32_t* indeg,
+                                              uint32_t target, uint32_t cand, uint32_t is_new,
+                                              uint32_t r_accept, uint32_t seed_lo,
+                                              uint32_t seed_hi) {
+    const uint32_t cap2 = 2 * c.cap;
+    if ((is_new ? c.raw_new[target] : c.raw_old[target]) <= cap2) return;
+    if (!accept_offer(c, k, indeg, target, r_accept)) return;
+    const unsigned long long key = det_key(target, cand, is_new, seed_lo, seed_hi);
+    unsigned long long* set = c.raw + size_t(target) * 4 * c.cap + (is_new ? 0u : cap2);
+    for (;;) {
+        unsigned long long mx = 0;
+        uint32_t at = 0;
+        for (uint32_t i = 0; i < cap2; ++i) {
+            const unsigned long long v = *(volatile unsigned long long*)(set + i);
+            if (v >= mx) {
+                mx = v;
+                at = i;
+            }
+        }
+        if (key >= mx) return;  // not among the 2cap smallest (maxima only decrease)
+        if (atomicCAS(set + at, mx, key) == mx) return;
+    }
+}
+
+__global__ void __launch_bounds__(256) det_fix_sample_kernel(GraphView g, CandView c,
+                                                             const uint32_t* indeg,
+                                                             uint32_t seed_lo, uint32_t seed_hi,
+                                                             const IterCounters* gate,
+                                                             uint32_t det_lo, uint32_t det_hi) {
+    const size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= size_t(g.n) * g.k || !gate->det_ovf || gate->halt) return;
+    const uint32_t u = uint32_t(e / g.k), i = uint32_t(e % g.k);
+    const uint32_t v = key_id(g.keys[e]);
+    const uint32_t is_new = (__ldg(g.flags + u) >> i) & 1u;
+    const Philox4 r = philox4x32_10(uint32_t(e), uint32_t(e >> 32), kSaltSample, 0u, seed_lo,
+                                    seed_hi);
+    if (u >= g.lo && u < g.hi) det_fix_offer(c, g.k, indeg, u, v, is_new, r.x, det_lo, det_hi);
+    if (v >= g.lo && v < g.hi) det_fix_offer(c, g.k, indeg, v, u, is_new, r.z, det_lo, det_hi);
 }
 
 __global__ void reset_raw_kernel(CandView c, uint32_t n, const IterCounters* gate) {
@@ -602,12 +685,6 @@ __device__ __forceinline__ void warp_sort(T (&v)[E]) {
     }
 }
 
-// Pair weight of candidate x offered to u in list `kind` (order-free).
-__device__ __forceinline__ uint32_t det_weight(uint32_t u, uint32_t x, uint32_t kind,
-                                               uint32_t seed_lo, uint32_t seed_hi) {
-    return philox4x32_10(u, x, kind, kSaltDet, seed_lo, seed_hi).x;
-}
-
 // finalize for deterministic mode, one node: both raw lists sorted by id and
 // deduplicated; an id in both lists stays where the reference's first offer
 // would put it (forward edge u -> x iff u < x, selection.hpp:311-317); each
@@ -620,13 +697,13 @@ __device__ __forceinline__ void det_lists(const GraphView& g, const CandView& c,
                                           const uint32_t* s_hid, uint32_t seed_lo,
                                           uint32_t seed_hi, uint32_t& nn, uint32_t& no) {
     const uint32_t lane = lane_id(), cap = c.cap, k = g.k;
-    const uint32_t* raw = c.raw + size_t(u) * 4 * cap;
+    const unsigned long long* raw = c.raw + size_t(u) * 4 * cap;
     uint32_t vn[E], vo[E];
 #pragma unroll
     for (uint32_t r = 0; r < E; ++r) {
         const uint32_t i = E * lane + r;
-        vn[r] = i < nr ? raw[i] : kTomb;
-        vo[r] = i < orr ? raw[2 * cap + i] : kTomb;
+        vn[r] = i < nr ? uint32_t(raw[i]) : kTomb;
+        vo[r] = i < orr ? uint32_t(raw[2 * cap + i]) : kTomb;
     }
     warp_sort<E>(vn);
     warp_sort<E>(vo);
@@ -812,9 +889,16 @@ void launch_reset_raw(const CandView& c, uint32_t n, cudaStream_t s, const IterC
 }
 
 void launch_sample(const GraphView& g, const CandView& c, const uint32_t* indeg, uint64_t seed,
-                   cudaStream_t s, const IterCounters* gate) {
-    sample_kernel<<<blocks_for(size_t(g.n) * g.k, 256), 256, 0, s>>>(
-        g, c, indeg, uint32_t(seed), uint32_t(seed >> 32), gate);
+                   cudaStream_t s, IterCounters* gate, uint64_t det_seed) {
+    const uint32_t blocks = blocks_for(size_t(g.n) * g.k, 256);
+    sample_kernel<<<blocks, 256, 0, s>>>(g, c, indeg, uint32_t(seed), uint32_t(seed >> 32), gate,
+                                         uint32_t(det_seed), uint32_t(det_seed >> 32));
+    if (c.det && g.hi > g.lo) {
+        det_fix_reset_kernel<<<blocks_for(g.hi - g.lo, 256), 256, 0, s>>>(g, c, gate);
+        det_fix_sample_kernel<<<blocks, 256, 0, s>>>(g, c, indeg, uint32_t(seed),
+                                                     uint32_t(seed >> 32), gate,
+                                                     uint32_t(det_seed), uint32_t(det_seed >> 32));
+    }
 }
 
 __global__ void iter_end_kernel(const IterCounters* cur, IterCounters* next, double threshold,

@@ -981,8 +981,11 @@ __global__ void __launch_bounds__(kMergeWarps * 32, KNNG_MERGE_MINBLOCKS) join_m
 // A hub target per CTA: warp w merges a contiguous slice of the target's
 // entries into its own copy of the row; warp 0 then inserts the other warps'
 // incoming entries.  The result is the k smallest distinct candidates of the
-// row and all proposals, as in one warp (ties aside); the change count is the
-// number of entries that came in (the order-free count).
+// row and all proposals, as in one warp (ties aside).  The change count is,
+// like join_merge_kernel's, the number of successful inserts of the target's
+// proposals (each proposal counted at most once: the warps' slice inserts,
+// not warp 0's fold-in); deterministic mode counts the entries that came in
+// (the order-free count).
 #ifndef KNNG_HUB_WARPS
 #define KNNG_HUB_WARPS 16  // 16 measured: C2 merge 2.51 -> 2.23 ms with 256 entries
 #endif
@@ -994,6 +997,7 @@ __global__ void __launch_bounds__(kHubWarps * 32) hub_merge_kernel(GraphView g, 
                                                                     const uint32_t* hubs) {
     __shared__ unsigned long long s_keys[kHubWarps][32];
     __shared__ uint32_t s_fresh[kHubWarps];
+    __shared__ uint32_t s_ins[kHubWarps];
     if (ctr->overflow || ctr->halt) return;
     const uint32_t lane = lane_id(), w = threadIdx.x >> 5, k = g.k;
     const uint32_t nh = ctr->hubs;
@@ -1010,7 +1014,10 @@ __global__ void __launch_bounds__(kHubWarps * 32) hub_merge_kernel(GraphView g, 
         merge_entries<kDet>(c, c.rev + c.roff[t] + b, e - b, k, key, flags, fresh, cur_max, inserted,
                             init_id);
         s_keys[w][lane] = key;
-        if (lane == 0) s_fresh[w] = fresh;
+        if (lane == 0) {
+            s_fresh[w] = fresh;
+            s_ins[w] = inserted;
+        }
         __syncthreads();
         if (w == 0) {
             for (uint32_t o = 1; o < kHubWarps; ++o) {
@@ -1028,15 +1035,18 @@ __global__ void __launch_bounds__(kHubWarps * 32) hub_merge_kernel(GraphView g, 
             }
             const uint32_t kmask = k >= 32 ? 0xffffffffu : ((1u << k) - 1u);
             const uint32_t came = __popc(fresh & kmask);
+            uint32_t ins = 0;
+            for (uint32_t o = 0; o < kHubWarps; ++o) ins += s_ins[o];
+            const uint32_t ch = kDet ? came : ins;
             if (came || kDet) {
                 if (c.indeg_inc && !ctr[1].recount) indeg_update(c.indeg_inc, key0, key, k);
                 if (lane < k) g.keys[size_t(t) * k + lane] = key;
                 if (lane == 0) {
                     g.flags[t] = flags;
                     g.maxd[t] = cur_max;
-                    if (came) atomicAdd(&ctr->changes, (unsigned long long)came);
                 }
             }
+            if (lane == 0 && ch) atomicAdd(&ctr->changes, (unsigned long long)ch);
         }
         __syncthreads();
     }
@@ -1085,10 +1095,13 @@ size_t join_scan_scratch(uint32_t n) {
     return a > b ? a : b;
 }
 
-void launch_join_offsets(const CandView& c, uint32_t n, void* scratch, size_t scratch_bytes,
-                         cudaStream_t s) {
+void launch_join_offsets(const CandView& c, uint32_t n, uint32_t lo, uint32_t hi, void* scratch,
+                         size_t scratch_bytes, cudaStream_t s) {
+    // proposal blocks exist only for owned nodes (finalize writes dsz[u] for
+    // u in [lo, hi) only), so the block offsets are a scan of the owned range
     size_t bytes = scratch_bytes;
-    cub::DeviceScan::ExclusiveSum(scratch, bytes, c.dsz, c.doff, int(n), s);
+    if (hi > lo)
+        cub::DeviceScan::ExclusiveSum(scratch, bytes, c.dsz + lo, c.doff + lo, int(hi - lo), s);
     bytes = scratch_bytes;
     cub::DeviceScan::ExclusiveSum(scratch, bytes, c.revcnt, c.roff, int(n), s);
 }

@@ -48,11 +48,13 @@ struct CandView {
     uint4* arec;         // per active index: {u, nn | no << 16, doff lo, doff hi}
     uint32_t* hubs;      // n: targets with more than kHubEntries reverse entries
     // deterministic mode (knng_cuda_params.deterministic): sampling appends
-    // every accepted offer to n x 4cap raw lists (new 2cap, old 2cap; no
-    // reservoir), finalize keeps the cap offers of smallest pair weight, and
-    // the merges keep the smaller copy of a present id and count changes as
-    // |final row \ initial row|
-    uint32_t* raw;
+    // every accepted offer, as a key (pair weight << 32 | id), to n x 4cap
+    // raw lists (new 2cap, old 2cap; no reservoir); a list that received more
+    // than 2cap offers is rebuilt from all of them as the 2cap smallest keys
+    // (det_fix_*: order-free); finalize keeps the cap offers of smallest pair
+    // weight, and the merges keep the smaller copy of a present id and count
+    // changes as |final row \ initial row|
+    unsigned long long* raw;
     int det;
     // in-degree kept up to date by the merges (single-GPU builds, counters
     // in per-iteration slots): a merge that changes row t adds 1 for each id
@@ -80,6 +82,8 @@ struct IterCounters {
                                  // previous iteration's merges then skip their updates
     unsigned long long screened;   // screened join: pairs bounded
     unsigned long long survivors;  // screened join: pairs evaluated exactly
+    uint32_t det_ovf;              // deterministic sampling: some raw list overflowed 2cap
+    uint32_t pad_;
 };
 
 // --- graph_kernels.cu ------------------------------------------------------
@@ -95,8 +99,11 @@ void launch_export_rows(const GraphView& g, uint32_t* ids, float* dists, uint8_t
 // gate->halt is set (iterations enqueued past termination, see run_engine)
 void launch_indegree(const GraphView& g, uint32_t* indeg, cudaStream_t s,
                      const IterCounters* gate = nullptr);
+// gate: the iteration's counters (halt flag; det_ovf, set when a deterministic
+// raw list overflows).  det_seed keys the deterministic pair weights (the
+// iteration seed, the same value finalize_det gets).
 void launch_sample(const GraphView& g, const CandView& c, const uint32_t* indeg, uint64_t seed,
-                   cudaStream_t s, const IterCounters* gate = nullptr);
+                   cudaStream_t s, IterCounters* gate, uint64_t det_seed);
 // dedup + flag_consumed + join bookkeeping (active list, block sizes, reverse counts)
 void launch_finalize(const GraphView& g, const CandView& c, uint32_t* active,
                      IterCounters* ctr, cudaStream_t s, uint64_t seed = 0);
@@ -119,7 +126,8 @@ void launch_indegree_gated(const GraphView& g, uint32_t* indeg, const IterCounte
 // --- join.cu ---------------------------------------------------------------
 // Exclusive scans dsz -> doff and revcnt -> roff (CUB); scratch sizing.
 size_t join_scan_scratch(uint32_t n);
-void launch_join_offsets(const CandView& c, uint32_t n, void* scratch, size_t scratch_bytes,
+void launch_join_offsets(const CandView& c, uint32_t n, uint32_t lo, uint32_t hi, void* scratch,
+                         size_t scratch_bytes,
                          cudaStream_t s);
 // Sets ctr->overflow when the distance blocks need more than `capacity` floats
 // (the join stages then return at once; the host grows the buffer and

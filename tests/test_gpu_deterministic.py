@@ -40,6 +40,21 @@ def test_same_seed_same_graph(gpu, kind, n, k, cap):
     assert not np.array_equal(a.graph.ids, c.graph.ids)
 
 
+def test_overflowing_raw_lists_are_order_free(gpu):
+    """cap = k = 8: a list whose target has deg > cap accepts ~Poisson(cap)
+    offers, so some lists receive more than their 2 cap raw slots; the kept
+    offers are then the 2 cap smallest pair-weight keys, whatever order the
+    offers arrived in (det_fix_*), so builds still agree bit for bit."""
+    data = make_data("G24", 40000, 5)
+    p = kg.RunParams(k=8, max_candidates=8, seed=4, deterministic=True)
+    runs = [kg.run(data, p) for _ in range(3)]
+    for r in runs[1:]:
+        assert np.array_equal(runs[0].graph.ids, r.graph.ids)
+        assert np.array_equal(bits(runs[0].graph.dists), bits(r.graph.dists))
+        assert ([it.changes for it in runs[0].metrics.iterations]
+                == [it.changes for it in r.metrics.iterations])
+
+
 @pytest.mark.parametrize("kind,n,k,cap", [("C1", 10000, 20, 20), ("C3", 4000, 30, 50)])
 def test_recall_matches_reference(gpu, restated, kind, n, k, cap):
     data = make_data(kind, n, 0)

@@ -71,16 +71,18 @@ def test_shard_step_exports_nothing_with_one_rank(gpu, nccl_world):
     eng.close()
 
 
-@pytest.mark.parametrize("kind", [
-    "C1",
-    # Known bug: on C2-shaped data (hub targets) a 2-rank split
-    # hits an illegal address inside knng_cuda_shard_step — every time with the
-    # FP32 join on the shards (KNNG_SHARD_U8=0), 1 run in 4 with the byte
-    # join.  An illegal address poisons the process's CUDA context, so the
-    # case is skipped rather than xfailed until it is found.
-    pytest.param("C2", marks=pytest.mark.skip(reason="known sharded hub-path bug, DESIGN.md §7")),
+@pytest.mark.parametrize("kind,shard_u8", [
+    ("C1", "1"),
+    # C2-shaped data has hub targets; the FP32 join on the shards and the
+    # byte-valued one.  These ran into the stale proposal-block sizes of
+    # rows outside the shard (fixed: the offsets scan only the owned range)
+    # after earlier engines had left non-zero pool memory behind, so they run
+    # after the C1 case and its single-GPU build in the same process.
+    ("C2", "0"),
+    ("C2", "1"),
+    ("C4", "1"),
 ])
-def test_shard_engine_two_ranks_one_process_exchange(gpu, kind):
+def test_shard_engine_two_ranks_one_process_exchange(gpu, monkeypatch, kind, shard_u8):
     """Two shard engines of a 2-rank split in ONE process (no collectives,
     sequential kernels — nothing waits on another rank): records exported by
     each rank are exactly for the other rank's rows, and merging them gives a
@@ -88,8 +90,9 @@ def test_shard_engine_two_ranks_one_process_exchange(gpu, kind):
     (first 12k rows) runs the shards' joins through the byte-valued kernel."""
     import torch
     from paper_2112_06630_b200.shard import GpuShardEngine, seed_sequence
+    monkeypatch.setenv("KNNG_SHARD_U8", shard_u8)
     cfg = datasets.CONFIGS[kind]
-    data = datasets.generate(cfg)[:12000]
+    data = datasets.generate(cfg, n=12000) if kind == "C4" else datasets.generate(cfg)[:12000]
     n, k = data.shape[0], cfg.k
     params = kg.RunParams(k=k, max_candidates=cfg.cap, seed=0)
     dd = torch.from_numpy(data).cuda()
