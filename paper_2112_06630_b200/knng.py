@@ -361,3 +361,48 @@ def locality_permutation(ids, dists, device: int = 0):
     check(N.lib().knng_cuda_locality_permutation(n, k, ids, np.ascontiguousarray(dists, np.float32),
                                                  sigma, sigma_inv, device))
     return sigma, sigma_inv
+
+
+def scaling_exponent(sizes, evals) -> float:
+    """Least-squares slope of log(dist_evals) against log(n)
+    (oracle.hpp:147-171), with the reference's argument checks."""
+    sizes = [float(s) for s in sizes]
+    evals = [float(e) for e in evals]
+    if len(sizes) != len(evals) or len(sizes) < 3:
+        raise InvalidArgument("scaling_exponent: need at least 3 matched points")
+    for i, (s, e) in enumerate(zip(sizes, evals)):
+        if s <= 0 or e <= 0:
+            raise InvalidArgument("scaling_exponent: sizes and counts must be positive")
+        if i > 0 and s <= sizes[i - 1]:
+            raise InvalidArgument("scaling_exponent: sizes must be increasing")
+    x = np.log(np.asarray(sizes))
+    y = np.log(np.asarray(evals))
+    dx = x - x.mean()
+    return float((dx * (y - y.mean())).sum() / (dx * dx).sum())
+
+
+def window_cluster_fraction(labels, sigma, window: int = 2000):
+    """window_cluster_fraction (reorder.hpp:61-86) of a permutation sigma
+    (point i moved to position sigma[i]): for windows of `window` consecutive
+    positions, starts advancing by window / 4 with n - window always included,
+    the fraction of each cluster.  Returns (window_start, cluster, fraction)
+    rows in the reference's order."""
+    labels = np.asarray(labels, dtype=np.int64)
+    sigma = np.asarray(sigma, dtype=np.int64)
+    n = len(sigma)
+    if len(labels) != n:
+        raise InvalidArgument("window_cluster_fraction: labels/permutation size mismatch")
+    if window == 0 or n < window:
+        raise InvalidArgument("window_cluster_fraction: window larger than dataset")
+    inv = np.empty(n, np.int64)
+    inv[sigma] = np.arange(n)
+    c = int(labels.max()) + 1 if n else 0
+    step = max(1, window // 4)
+    out, p = [], 0
+    while True:
+        cnt = np.bincount(labels[inv[p:p + window]], minlength=c)
+        out.extend((p, cl, cnt[cl] / window) for cl in range(c))
+        if p == n - window:
+            break
+        p = min(p + step, n - window)
+    return out
