@@ -27,7 +27,58 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIBS = {
     "restated": (os.path.join(HERE, "lib", "libknng_oracle.so"), "oracle_"),
     "reference": (os.path.join(HERE, "_ref", "libknng_ref.so"), "ref_"),
+    "reference_native": (os.path.join(HERE, "_ref", "libknng_ref_native.so"), "ref_"),
 }
+
+# gcc -m<ext> option -> /proc/cpuinfo flag, for the extensions -march=native
+# may have enabled (the rest of the options are tuning, not ISA)
+_ISA_FLAG = {
+    "-mavx": "avx", "-mavx2": "avx2", "-mfma": "fma", "-mbmi": "bmi1", "-mbmi2": "bmi2",
+    "-mf16c": "f16c", "-mavx512f": "avx512f", "-mavx512bw": "avx512bw",
+    "-mavx512cd": "avx512cd", "-mavx512dq": "avx512dq", "-mavx512vl": "avx512vl",
+    "-mavx512vnni": "avx512_vnni", "-mavx512vbmi": "avx512vbmi", "-mavx512vbmi2": "avx512_vbmi2",
+    "-mavx512ifma": "avx512ifma", "-mavx512bitalg": "avx512_bitalg",
+    "-mavx512vpopcntdq": "avx512_vpopcntdq", "-mavx512bf16": "avx512_bf16",
+    "-mavx512fp16": "avx512_fp16", "-mamx-tile": "amx_tile", "-mamx-bf16": "amx_bf16",
+    "-mamx-int8": "amx_int8", "-mavxvnni": "avx_vnni", "-msse4.2": "sse4_2", "-mpopcnt": "popcnt",
+    "-mlzcnt": "abm", "-mmovbe": "movbe", "-madx": "adx", "-msha": "sha_ni", "-mvaes": "vaes",
+    "-mvpclmulqdq": "vpclmulqdq", "-mgfni": "gfni",
+}
+
+
+def native_compatible() -> tuple:
+    """(ok, missing): does this host have every ISA extension the
+    -march=native reference build enabled on the build machine?"""
+    isa = os.path.join(HERE, "_ref", "native_isa.txt")
+    if not (os.path.exists(LIBS["reference_native"][0]) and os.path.exists(isa)):
+        return False, ["native build absent"]
+    try:
+        flags = set()
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("flags"):
+                flags = set(line.split(":", 1)[1].split())
+                break
+    except OSError:
+        return False, ["no /proc/cpuinfo"]
+    need = [_ISA_FLAG[o] for o in open(isa).read().split() if o in _ISA_FLAG]
+    missing = [f for f in need if f not in flags]
+    return not missing, missing
+
+
+def reference_kind() -> str:
+    """The reference build to time: the -march=native one (the reference's own
+    CMake flags) when this host supports it, else the portable one."""
+    return "reference_native" if native_compatible()[0] else "reference"
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
 u64p = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
