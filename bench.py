@@ -431,8 +431,9 @@ def run_sharded_bench(args, rank, world, local):
                        "max_candidates": cap, "delta": cfg.delta, "seed": cfg.seed,
                        "step": "one complete K-NNG build sharded over all GPUs",
                        "l2": "inputs larger than L2 (data %.1f MB > 126 MB)" % (n * d * 4 / 1e6),
-                       "parallelism": f"{world} vertex-range shards, replicated data, NCCL "
-                                      "all-to-all of proposals + allgather of rows"},
+                       "parallelism": f"{world} vertex-range shards, replicated data; NCCL "
+                                      "all-reduce of in-degree, all-to-all of reverse offers "
+                                      "and of proposals, all-gather of row maxima"},
             "build_time_ms": round(ms / args.steps, 3),
             "iterations_per_s": round(iters / (ms * 1e-3), 2),
             "iterations_per_build": round(iters / args.steps, 2),
@@ -441,10 +442,12 @@ def run_sharded_bench(args, rank, world, local):
                     "h2d_bytes_per_step": n * d * 4,
                     "d2h_bytes_per_step": int(d2h / args.steps)},
             "exchange_bytes_per_step_rank0": int(sent / args.steps),
-            # per rank and build: init + export, and per iteration indegree,
-            # reset, sample, finalize, capacity check, reverse scatter,
-            # distances, merge, export count/write, received count/scatter/merge
-            "gpu_launches": int(2 * args.steps + 13 * iters),
+            # per rank and build: init + export, and per iteration partial
+            # in-degree, reset, sample, offers, finalize (2), offsets (2 scans),
+            # capacity check, reverse scatter, distances, merge (2), export
+            # count / scan / bounds / write, received count / scan / scatter /
+            # merge
+            "gpu_launches": int(2 * args.steps + 21 * iters),
             "roofline": None,
             "cpu_baseline": None,
             "clocks": clk,

@@ -126,7 +126,9 @@ int knng_cuda_device_count(void);
  * (descent.hpp:193-255) for squared L2.  HOST pointers.
  *   sample_rate rho -> max_candidates = lround(rho * k) (PAPER.md:88,
  *   SPEC.md:266,308); must be >= k.  out_ids/out_dists: n*k each, rows
- *   sorted by (distance, id).  out_metrics may be NULL.
+ *   sorted by (distance, id).  out_metrics may be NULL.  num_gpus > 1 runs
+ *   the vertex-sharded build over that many GPUs in this process
+ *   (knng_cuda_run_multi, shard r on device r % device count).
  */
 int knng_cuda_nndescent_l2(const float* data, uint32_t n, uint32_t d, uint32_t k,
                            double sample_rate, double delta, uint64_t seed,
@@ -216,31 +218,46 @@ int knng_cuda_locality_permutation(uint32_t n, uint32_t k, const uint32_t* ids,
                                    int device);
 
 /*
- * Multi-GPU shard — one process per GPU, vertex-range ownership with the data
- * and the graph replicated.  The library runs the per-device
- * kernels; the caller runs the collectives (NCCL), see
- * paper_2112_06630_b200/shard.py.  Per iteration:
- *   knng_cuda_shard_step   selection of the owned lists over the replicated
- *                          graph, local join of the owned active nodes,
- *                          merges into owned rows, and records
- *                          (target, id, dist bits) x u32 for targets owned by
- *                          other ranks, grouped by owner in rank order;
- *   caller                 all-to-all of the records;
- *   knng_cuda_shard_merge  merge of the received records into owned rows;
- *   caller                 allgather of the owned rows (keys/flags/maxd, in
- *                          place in the buffers below), allreduce of changes.
- * Device pointers; the library synchronises its stream before returning.
+ * Multi-GPU shards — vertex-range ownership with the data
+ * replicated.  Shard r owns rows [r*chunk, min(n, (r+1)*chunk)): their graph
+ * rows, candidate lists, joins and merges; only the row maxima (n floats, the
+ * join prefilter's bound) are replicated.  Replaces the reference loop
+ * descent.hpp:219-243 with, per iteration:
+ *   knng_cuda_shard_degree   partial in-degree of the owned rows' edges into
+ *                            info.indeg;           caller: all-reduce (sum, n u32)
+ *   knng_cuda_shard_sample   turbo sampling over the owned rows' edges (local
+ *                            offers applied; accepted reverse offers for rows
+ *                            owned elsewhere grouped by owner);
+ *                                                  caller: all-to-all (4 u32 each)
+ *   knng_cuda_shard_offers   received offers into the owned lists
+ *   knng_cuda_shard_step     finalize, local join of the owned active nodes,
+ *                            merges into owned rows, pre-reduced proposal
+ *                            records (target, id, dist bits) for rows owned
+ *                            elsewhere (<= k per target);
+ *                                                  caller: all-to-all (3 u32 each)
+ *   knng_cuda_shard_merge    received records into owned rows;
+ *                                                  caller: all-gather of the owned
+ *                                                  slices of info.maxd, all-reduce
+ *                                                  of changes (termination test)
+ * Work is stream-ordered on info.stream: the caller's stream when one is
+ * given (cudaStreamLegacy = (void*)1 for the default stream), else a stream
+ * of the shard's own; sample, step and merge return host counts and so
+ * synchronise it.
+ * knng_cuda_run_multi drives the same phases for N GPUs in one process.
  */
 typedef struct knng_cuda_shard knng_cuda_shard;
 
 typedef struct knng_cuda_shard_info {
-    uint64_t* keys;       /* rows_alloc x k: key = (dist bits << 32) | id, rows sorted */
+    uint64_t* keys;       /* rows_alloc x k (owned rows valid): (dist bits << 32) | id */
     uint32_t* flags;      /* rows_alloc: bit i = entry i is new */
-    float* maxd;          /* rows_alloc: row maximum */
+    float* maxd;          /* rows_alloc: row maximum, every row (replicated) */
+    uint32_t* indeg;      /* n: in-degree (partial after shard_degree; the sum after
+                             the caller's all-reduce) */
     uint32_t rows_alloc;  /* nranks * chunk (>= n), so every rank's slice is `chunk` rows */
     uint32_t chunk;
     uint32_t lo, hi;      /* owned rows */
-    void* stream;         /* the library stream (cudaStream_t) */
+    void* stream;         /* cudaStream_t of the shard's work */
+    uint64_t seg_cap;     /* offer records per destination segment of shard_sample */
 } knng_cuda_shard_info;
 
 int knng_cuda_shard_create(const float* d_data, uint32_t n, uint32_t d,
@@ -253,17 +270,35 @@ void knng_cuda_seed_sequence(uint64_t seed, uint32_t count, uint64_t* out);
 /* init_random (graph.hpp:34-67) of the owned rows; per-node Philox draws, so
  * the initial graph does not depend on the number of ranks. */
 int knng_cuda_shard_init(knng_cuda_shard* shard, uint64_t seed);
+int knng_cuda_shard_degree(knng_cuda_shard* shard);
+/* select_turbo (selection.hpp:282-320) over the owned edges with iteration
+ * seed `seed`.  send_counts: nranks offer counts; segment r of
+ * *send_records starts at record r * info.seg_cap (4 u32 per record). */
+int knng_cuda_shard_sample(knng_cuda_shard* shard, uint64_t seed, uint64_t* send_counts,
+                           const uint32_t** send_records);
+int knng_cuda_shard_offers(knng_cuda_shard* shard, const uint32_t* d_records, uint64_t count);
 /* counters: [0] distance evaluations, [1] candidates joined, [2] inserts into
  * owned rows so far, [3] active nodes.  send_counts: nranks record counts;
- * *send_records: device pointer to 3 * sum(send_counts) u32. */
-int knng_cuda_shard_step(knng_cuda_shard* shard, uint64_t seed, uint64_t* counters,
-                         uint64_t* send_counts, const uint32_t** send_records);
+ * *send_records: device pointer to 3 * sum(send_counts) u32, grouped by owner
+ * in rank order. */
+int knng_cuda_shard_step(knng_cuda_shard* shard, uint64_t* counters, uint64_t* send_counts,
+                         const uint32_t** send_records);
 /* d_records: count records (3 u32 each) for owned targets; *changes = all
  * inserts into owned rows this iteration (local + received). */
 int knng_cuda_shard_merge(knng_cuda_shard* shard, const uint32_t* d_records, uint64_t count,
                           uint64_t* changes);
 /* owned rows, sorted by (distance, id): (hi - lo) x k ids and distances. */
 int knng_cuda_shard_export(knng_cuda_shard* shard, uint32_t* d_ids, float* d_dists);
+
+/* knng::run (descent.hpp:193-255) over num_gpus shards in ONE process, shard r
+ * on device devices[r] (NULL: r % device count; several shards may share a
+ * device).  The exchanges are peer copies between the shards' streams
+ * (NVLink / NVSwitch between GPUs).  Host data in, host graph out (n x k,
+ * rows sorted by (distance, id)); metrics as knng_cuda_run.  params.reorder
+ * and params.deterministic are not supported here (KNNG_CUDA_NOT_IMPLEMENTED). */
+int knng_cuda_run_multi(const float* data, uint32_t n, uint32_t d, const knng_cuda_params* params,
+                        int num_gpus, const int* devices, uint32_t* out_ids, float* out_dists,
+                        knng_cuda_metrics* out_metrics);
 
 #ifdef __cplusplus
 }

@@ -8,5 +8,6 @@ from .knng import (  # noqa: F401
     CandidateSet, InvalidArgument, IterationMetrics, KnnGraph, KnngCudaError, RunMetrics,
     RunParams, RunResult, brute_force_knng, candidate_distances, compute_step, device_count,
     flop_count, init_random, locality_permutation, nndescent_l2, recall, run, run_device,
+    run_multi,
     scaling_exponent, select_turbo, window_cluster_fraction,
 )

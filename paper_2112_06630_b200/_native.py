@@ -44,9 +44,13 @@ EXPORTS = (
     "knng_cuda_shard_destroy",
     "knng_cuda_seed_sequence",
     "knng_cuda_shard_init",
+    "knng_cuda_shard_degree",
+    "knng_cuda_shard_sample",
+    "knng_cuda_shard_offers",
     "knng_cuda_shard_step",
     "knng_cuda_shard_merge",
     "knng_cuda_shard_export",
+    "knng_cuda_run_multi",
 )
 
 
@@ -55,11 +59,13 @@ class ShardInfo(C.Structure):
         ("keys", C.c_void_p),
         ("flags", C.c_void_p),
         ("maxd", C.c_void_p),
+        ("indeg", C.c_void_p),
         ("rows_alloc", C.c_uint32),
         ("chunk", C.c_uint32),
         ("lo", C.c_uint32),
         ("hi", C.c_uint32),
         ("stream", C.c_void_p),
+        ("seg_cap", C.c_uint64),
     ]
 
 
@@ -160,9 +166,14 @@ def lib() -> C.CDLL:
     fn("knng_cuda_shard_destroy", C.c_int, [vp])
     fn("knng_cuda_seed_sequence", None, [C.c_uint64, u32, u64p])
     fn("knng_cuda_shard_init", C.c_int, [vp, C.c_uint64])
-    fn("knng_cuda_shard_step", C.c_int, [vp, C.c_uint64, u64p, u64p, C.POINTER(vp)])
+    fn("knng_cuda_shard_degree", C.c_int, [vp])
+    fn("knng_cuda_shard_sample", C.c_int, [vp, C.c_uint64, u64p, C.POINTER(vp)])
+    fn("knng_cuda_shard_offers", C.c_int, [vp, vp, C.c_uint64])
+    fn("knng_cuda_shard_step", C.c_int, [vp, u64p, u64p, C.POINTER(vp)])
     fn("knng_cuda_shard_merge", C.c_int, [vp, vp, C.c_uint64, u64p])
     fn("knng_cuda_shard_export", C.c_int, [vp, vp, vp])
+    fn("knng_cuda_run_multi", C.c_int, [f32p, u32, u32, C.POINTER(Params), C.c_int, vp, u32p,
+                                        f32p, C.POINTER(Metrics)])
     _lib = L
     return L
 

@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <new>
 #include <random>
@@ -27,7 +28,29 @@
 
 using namespace knng_cuda;
 
+#include <csignal>
+#include <execinfo.h>
+#include <unistd.h>
+
 namespace {
+
+// KNNG_SEGV_TRACE=1: print a native backtrace on SIGSEGV (diagnostics; map
+// the addresses with addr2line -e libknng_cuda.so)
+void segv_trace(int sig) {
+    void* frames[64];
+    const int nf = backtrace(frames, 64);
+    const char msg[] = "knng_cuda: fatal signal, native backtrace:\n";
+    (void)!write(2, msg, sizeof(msg) - 1);
+    backtrace_symbols_fd(frames, nf, 2);
+    signal(sig, SIG_DFL);
+    raise(sig);
+}
+struct SegvTraceInstaller {
+    SegvTraceInstaller() {
+        const char* v = getenv("KNNG_SEGV_TRACE");
+        if (v && v[0] == '1') signal(SIGSEGV, segv_trace);
+    }
+} g_segv_trace_installer;
 
 thread_local std::string g_err;
 
@@ -258,6 +281,10 @@ struct Engine {
     DevBuf<int32_t> lnorm;
     DevBuf<uint32_t> u8_flag;
     int u8_state = -1;  // -1 unknown, 0 not eligible, 1 packed
+    // long rows (join_gl.cu): lane-major copy of the data, made on first use
+    // and after the data is permuted
+    DevBuf<float> dl;
+    bool dl_valid = false;
     uint32_t iteration = 0;  // the running iteration (1-based; 0 = fixed-state entry)
     uint64_t h2d = 0, d2h = 0;
 
@@ -454,6 +481,13 @@ struct Engine {
         h = timer.begin(KNNG_CUDA_KERNEL_JOIN);
         if (use_u8_join()) {
             launch_join_u8(gv(), cv(), cur, n, packed.p, lnorm.p, s);
+        } else if (use_gl_join()) {
+            if (!dl_valid) {
+                if (!dl.p) dl.alloc(size_t(n + 1) * gl_row_floats(stride), pool, s);
+                launch_gl_pack(data.p, n, stride, dl.p, s);
+                dl_valid = true;
+            }
+            launch_join_gl(cv(), dl.p, n, stride, cur, n, s);
         } else if (use_screened_join(distances_only)) {
             if (!norms_valid) {
                 if (!nrm2.p) {
@@ -495,6 +529,14 @@ struct Engine {
             }
         }
         return u8_state == 1;
+    }
+
+    // The register-staged join (join_gl.cu) is opt-in: KNNG_JOIN_GL=1.
+    // Measured 3x slower than the shared-memory tile kernel on C5 (DESIGN.md
+    // §3.5): loads straight into registers leave the L2 latency exposed.
+    bool use_gl_join() const {
+        const char* v = getenv("KNNG_JOIN_GL");
+        return v && v[0] == '1';
     }
 
     // The tensor-core screened join (join_tc.cu) is opt-in: KNNG_JOIN_TC=1
@@ -547,6 +589,7 @@ struct Engine {
         launch_permute_rows(data.p, data2.p, sigma.p, n, stride, s);
         std::swap(data.p, data2.p);
         norms_valid = false;
+        dl_valid = false;
         if (u8_state == 1) u8_state = -1;  // repack in the new row order
         remap_graph(sigma.p);
     }
@@ -896,9 +939,7 @@ int knng_cuda_nndescent_l2(const float* data, uint32_t n, uint32_t d, uint32_t k
     int rc = guarded([&] {
         if (!(sample_rate > 0.0) || !std::isfinite(sample_rate))
             raise(KNNG_CUDA_INVALID_ARGUMENT, "sample_rate must be positive");
-        if (num_gpus != 1)
-            raise(KNNG_CUDA_NOT_IMPLEMENTED, "this entry point drives one GPU per process; "
-                                             "shard across processes for more");
+        if (num_gpus < 1) raise(KNNG_CUDA_INVALID_ARGUMENT, "num_gpus must be at least 1");
     });
     if (rc) return rc;
     knng_cuda_params p;
@@ -909,6 +950,9 @@ int knng_cuda_nndescent_l2(const float* data, uint32_t n, uint32_t d, uint32_t k
     p.termination_delta = delta;
     p.seed = seed;
     p.max_iterations = max_iterations;
+    if (num_gpus > 1)  // shard r on device r % device count, in this process
+        return knng_cuda_run_multi(data, n, d, &p, num_gpus, nullptr, out_ids, out_dists,
+                                   out_metrics);
     return knng_cuda_run(data, n, d, &p, out_ids, out_dists, nullptr, nullptr, out_metrics);
 }
 
@@ -1187,42 +1231,259 @@ int knng_cuda_locality_permutation(uint32_t n, uint32_t k, const uint32_t* ids,
 }  // extern "C"
 
 // ---------------------------------------------------------------------------
-// Multi-GPU shard.  One process per GPU; the caller runs the
-// collectives (NCCL through torch.distributed in paper_2112_06630_b200/shard.py).
-// Each device owns rows [rank*chunk, min(n, (rank+1)*chunk)) and keeps the
-// whole graph replicated (allgathered by the caller into the buffers exposed
-// in knng_cuda_shard_info).  An iteration is: step (selection of the owned
-// lists over the replicated graph, local join of the owned active nodes,
-// merges for owned targets, export of proposals for remote targets grouped
-// by owner), the caller's all-to-all of those records, merge of the received
-// records, the caller's allgather of the owned rows and allreduce of changes.
+// Multi-GPU shards: vertex-range ownership with the data
+// replicated.  Shard r owns rows [r*chunk, min(n, (r+1)*chunk)): their graph
+// rows, their candidate lists, their joins and their merges.  Only the row
+// maxima (n floats, the join prefilter's bound) are replicated.  Per iteration
+// (reference loop descent.hpp:219-243):
+//   degree   partial in-degree of the owned rows' edges   -> all-reduce (n u32)
+//   sample   owned edges only; reverse offers for rows owned elsewhere,
+//            accepted with the global in-degree, grouped by owner -> all-to-all
+//   offers   received offers into the owned lists
+//   step     finalize, local join, merges into owned rows, pre-reduced
+//            proposal records for rows owned elsewhere    -> all-to-all
+//   merge    received records into owned rows            -> all-gather maxd,
+//                                                           all-reduce changes
+// Every phase is split into an enqueue part and a finish part (the host
+// reads the counts it needs), so the in-process driver (knng_cuda_run_multi)
+// keeps every GPU busy while it waits for one; the C-ABI phase functions run
+// both back to back for callers that exchange with NCCL (shard.py).
 // ---------------------------------------------------------------------------
 struct knng_cuda_shard {
+    // the stream a shard created for itself outlives every buffer freed on it
+    // (declared first, destroyed last)
+    struct OwnedStream {
+        cudaStream_t s = nullptr;
+        ~OwnedStream() {
+            if (s) cudaStreamDestroy(s);
+        }
+    } owned;
     int device = 0;
     knng_cuda_params p{};
     uint32_t rank = 0, nranks = 1, chunk = 0;
     cudaStream_t s = nullptr;
     Engine* e = nullptr;
+    KernelTimer* timer = nullptr;
+    knng_cuda_metrics kmetrics{};  // per-kernel times of the shard's stream (params.profile)
+    // reverse offers for rows owned elsewhere: nranks segments of seg_cap
+    // records {target, cand, is_new, slot draw}; their counts
+    DevBuf<uint4> osend;
+    DevBuf<uint32_t> ocnt;
+    uint64_t seg_cap = 0;
+    // proposal records for rows owned elsewhere
     DevBuf<uint32_t> exp_counts, rcnt, roff2, rcur2, send;
     DevBuf<uint64_t> exp_off, bounds, grouped;
     DevBuf<unsigned char> scan_tmp;
     size_t scan_bytes = 0, send_cap = 0, grouped_cap = 0;
-    std::vector<uint64_t> h_bounds;
-    ~knng_cuda_shard() { delete e; }
+    // pinned host mirror: [0, nranks) offer counts, [nranks, 2 nranks + 1) record bounds
+    uint64_t* h_pin = nullptr;
+    uint32_t* h_ocnt = nullptr;
+    IterCounters last{};  // counters of the last finished phase
+    ~knng_cuda_shard() {
+        delete timer;
+        delete e;
+        if (h_pin) cudaFreeHost(h_pin);
+        if (h_ocnt) cudaFreeHost(h_ocnt);
+    }
+
+    // ---- degree
+    void enq_degree() {
+        ++e->iteration;
+        CK(cudaMemsetAsync(e->ctr.p, 0, sizeof(IterCounters), s));
+        launch_indegree_owned(e->gv(), e->indeg.p, s);
+        CK(cudaGetLastError());
+    }
+    // ---- sample (the in-degree is global by now)
+    void enq_sample(uint64_t seed) {
+        const GraphView g = e->gv();
+        const CandView c = e->cv();
+        const int h = timer->begin(KNNG_CUDA_KERNEL_SAMPLE);
+        launch_reset_raw(c, e->n, s, e->ctr.p);
+        launch_sample_owned(g, c, e->indeg.p, seed, e->ctr.p, chunk, nranks, ocnt.p, osend.p,
+                            seg_cap, s);
+        timer->end(h);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(h_ocnt, ocnt.p, sizeof(uint32_t) * nranks, cudaMemcpyDeviceToHost, s));
+    }
+    void fin_sample(uint64_t* counts) {
+        CK(cudaStreamSynchronize(s));
+        for (uint32_t r = 0; r < nranks; ++r) counts[r] = h_ocnt[r];
+        e->d2h += sizeof(uint32_t) * nranks;
+    }
+    // ---- offers
+    void enq_offers(const uint4* recs, uint64_t count) {
+        launch_apply_offers(e->cv(), recs, count, e->ctr.p, s);
+        CK(cudaGetLastError());
+    }
+    // ---- step: finalize + join + merges of owned targets, then the export count
+    void enq_step_join() {
+        const int h = timer->begin(KNNG_CUDA_KERNEL_FINALIZE);
+        launch_finalize(e->gv(), e->cv(), e->active.p, e->ctr.p, s);
+        timer->end(h);
+        CK(cudaGetLastError());
+        e->cur = e->ctr.p;
+        e->join_enqueue(*timer);
+        CK(cudaMemcpyAsync(e->h_ctr, e->cur, sizeof(IterCounters), cudaMemcpyDeviceToHost, s));
+    }
+    void fin_step_join() {
+        CK(cudaStreamSynchronize(s));
+        e->d2h += sizeof(IterCounters);
+        if (e->h_ctr->overflow) {
+            e->reserve_join(e->h_ctr->rev, e->h_ctr->dwords);
+            CK(cudaMemsetAsync(&e->cur->overflow, 0, sizeof(uint32_t), s));
+            e->join_stages(*timer, false);
+            e->read_counters();
+        }
+        last = *e->h_ctr;
+        // records for targets owned elsewhere: count pass, offsets, bounds
+        const GraphView g = e->gv();
+        const int h = timer->begin(KNNG_CUDA_KERNEL_MERGE);
+        launch_export_remote(g, e->cv(), e->ctr.p, exp_counts.p, nullptr, nullptr, false, s);
+        size_t bytes = scan_bytes;
+        CK(cub::DeviceScan::ExclusiveScan(scan_tmp.p, bytes, exp_counts.p, exp_off.p, cub::Sum(),
+                                          uint64_t(0), int(e->n), s));
+        shard_bounds(s);
+        timer->end(h);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(h_pin + nranks, bounds.p, sizeof(uint64_t) * (nranks + 1),
+                           cudaMemcpyDeviceToHost, s));
+    }
+    void fin_step_export(uint64_t* send_counts) {
+        CK(cudaStreamSynchronize(s));
+        e->d2h += sizeof(uint64_t) * (nranks + 1);
+        const uint64_t* b = h_pin + nranks;
+        const uint64_t total = b[nranks];
+        if (3 * total > send_cap) {
+            send.~DevBuf();
+            new (&send) DevBuf<uint32_t>();
+            send_cap = 3 * (total + total / 4 + 1024);
+            send.alloc(send_cap, e->pool, s);
+        }
+        if (total)
+            launch_export_remote(e->gv(), e->cv(), e->ctr.p, exp_counts.p, exp_off.p, send.p, true,
+                                 s);
+        CK(cudaGetLastError());
+        for (uint32_t r = 0; r < nranks; ++r) send_counts[r] = b[r + 1] - b[r];
+    }
+    // ---- merge of received records
+    void enq_merge(const uint32_t* recs, uint64_t count) {
+        if (count > grouped_cap) {
+            grouped.~DevBuf();
+            new (&grouped) DevBuf<uint64_t>();
+            grouped_cap = count + count / 4 + 1024;
+            grouped.alloc(grouped_cap, e->pool, s);
+        }
+        const int h = timer->begin(KNNG_CUDA_KERNEL_MERGE);
+        launch_merge_received(e->gv(), recs, count, rcnt.p, roff2.p, rcur2.p, grouped.p,
+                              scan_tmp.p, scan_bytes, e->ctr.p, s);
+        timer->end(h);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(e->h_ctr, e->ctr.p, sizeof(IterCounters), cudaMemcpyDeviceToHost, s));
+    }
+    void fin_merge() {
+        CK(cudaStreamSynchronize(s));
+        e->d2h += sizeof(IterCounters);
+        last = *e->h_ctr;
+        timer->flush();
+    }
+    void shard_bounds(cudaStream_t st);
 };
 
 namespace {
 
 __global__ void shard_bounds_kernel(const uint64_t* off, const uint32_t* counts, uint32_t n,
                                     uint32_t chunk, uint32_t nranks, uint64_t* bounds) {
-    const uint32_t r = threadIdx.x;
-    if (r > nranks) return;
     const uint64_t total = n ? off[n - 1] + counts[n - 1] : 0;
-    const uint64_t start = uint64_t(r) * chunk;
-    bounds[r] = start >= n ? total : off[start];
+    for (uint32_t r = threadIdx.x; r <= nranks; r += blockDim.x) {
+        const uint64_t start = uint64_t(r) * chunk;
+        bounds[r] = start >= n ? total : off[start];
+    }
+}
+
+constexpr uint32_t kMaxShards = 1023;
+
+knng_cuda_shard* shard_new(const float* data, bool data_on_device, uint32_t n, uint32_t d,
+                           const knng_cuda_params& p, uint32_t rank, uint32_t nranks,
+                           cudaStream_t stream) {
+    if (nranks == 0 || rank >= nranks) raise(KNNG_CUDA_INVALID_ARGUMENT, "bad rank / nranks");
+    if (nranks > kMaxShards)
+        raise(KNNG_CUDA_INVALID_ARGUMENT, "this build supports at most 1023 shards");
+    validate_params(n, d, p);
+    if (p.reorder) raise(KNNG_CUDA_NOT_IMPLEMENTED, "reorder is not supported on the sharded path");
+    if (p.deterministic)
+        raise(KNNG_CUDA_NOT_IMPLEMENTED, "deterministic mode is not supported on the sharded path");
+    auto* sh = new knng_cuda_shard();
+    try {
+        sh->device = p.device;
+        sh->p = p;
+        sh->rank = rank;
+        sh->nranks = nranks;
+        sh->chunk = (n + nranks - 1) / nranks;
+        if (stream) {
+            sh->s = stream;
+        } else {
+            CK(cudaStreamCreateWithFlags(&sh->owned.s, cudaStreamNonBlocking));
+            sh->s = sh->owned.s;
+        }
+        sh->e = new Engine(p.device, n, d, p.k, p.max_candidates, sh->s, sh->chunk * nranks);
+        Engine& e = *sh->e;
+        e.lo = std::min(n, rank * sh->chunk);
+        e.hi = std::min(n, (rank + 1) * sh->chunk);
+        e.upload(data, data_on_device);
+        // byte-valued data: check and pack once here (KNNG_SHARD_U8=0 keeps
+        // the FP32 join on the shards)
+        const char* sv = getenv("KNNG_SHARD_U8");
+        if (sv && sv[0] == '0')
+            e.u8_state = 0;
+        else
+            e.use_u8_join();
+        const uint64_t owned_edges = uint64_t(e.hi - e.lo) * p.k;
+        sh->seg_cap = std::max<uint64_t>(owned_edges, 1);
+        sh->osend.alloc(sh->seg_cap * nranks, e.pool, e.s);
+        sh->ocnt.alloc(nranks, e.pool, e.s);
+        sh->exp_counts.alloc(n, e.pool, e.s);
+        sh->exp_off.alloc(n, e.pool, e.s);
+        sh->rcnt.alloc(n, e.pool, e.s);
+        sh->roff2.alloc(n, e.pool, e.s);
+        sh->rcur2.alloc(n, e.pool, e.s);
+        sh->bounds.alloc(nranks + 1, e.pool, e.s);
+        size_t a = 0, b = 0;
+        CK(cub::DeviceScan::ExclusiveScan(nullptr, a, sh->exp_counts.p, sh->exp_off.p, cub::Sum(),
+                                          uint64_t(0), int(n)));
+        CK(cub::DeviceScan::ExclusiveSum(nullptr, b, sh->rcnt.p, sh->roff2.p, int(n)));
+        sh->scan_bytes = std::max(a, b);
+        sh->scan_tmp.alloc(sh->scan_bytes, e.pool, e.s);
+        CK(cudaMallocHost(reinterpret_cast<void**>(&sh->h_pin), sizeof(uint64_t) * (2 * nranks + 2)));
+        CK(cudaMallocHost(reinterpret_cast<void**>(&sh->h_ocnt), sizeof(uint32_t) * nranks));
+        sh->timer = new KernelTimer(p.profile != 0, sh->s, &sh->kmetrics);
+        metrics_reset(&sh->kmetrics);
+        CK(cudaStreamSynchronize(e.s));
+    } catch (...) {
+        delete sh;
+        throw;
+    }
+    return sh;
+}
+
+void shard_fill_info(const knng_cuda_shard* sh, knng_cuda_shard_info* info) {
+    const Engine& e = *sh->e;
+    info->keys = e.keys.p;
+    info->flags = e.flags.p;
+    info->maxd = e.maxd.p;
+    info->indeg = e.indeg.p;
+    info->rows_alloc = e.rows_alloc;
+    info->chunk = sh->chunk;
+    info->lo = e.lo;
+    info->hi = e.hi;
+    info->stream = sh->s;
+    info->seg_cap = sh->seg_cap;
 }
 
 }  // namespace
+
+void knng_cuda_shard::shard_bounds(cudaStream_t st) {
+    shard_bounds_kernel<<<1, 256, 0, st>>>(exp_off.p, exp_counts.p, e->n, chunk, nranks, bounds.p);
+}
 
 extern "C" {
 
@@ -1231,61 +1492,10 @@ int knng_cuda_shard_create(const float* d_data, uint32_t n, uint32_t d,
                            void* stream, knng_cuda_shard** out, knng_cuda_shard_info* info) {
     return guarded([&] {
         if (!d_data || !params || !out || !info) raise(KNNG_CUDA_INVALID_ARGUMENT, "null argument");
-        if (nranks == 0 || rank >= nranks) raise(KNNG_CUDA_INVALID_ARGUMENT, "bad rank / nranks");
-        if (nranks > 1023) raise(KNNG_CUDA_INVALID_ARGUMENT, "this build supports at most 1023 shards");
-        const knng_cuda_params p = *params;
-        validate_params(n, d, p);
-        if (p.reorder)
-            raise(KNNG_CUDA_NOT_IMPLEMENTED, "reorder is not supported on the sharded path");
-        DeviceGuard dg(p.device);
-        auto* sh = new knng_cuda_shard();
-        try {
-            sh->device = p.device;
-            sh->p = p;
-            sh->rank = rank;
-            sh->nranks = nranks;
-            sh->chunk = (n + nranks - 1) / nranks;
-            StreamHolder hold(stream);
-            sh->s = hold.s;
-            sh->e = new Engine(p.device, n, d, p.k, p.max_candidates, sh->s,
-                               sh->chunk * nranks);
-            Engine& e = *sh->e;
-            e.lo = std::min(n, rank * sh->chunk);
-            e.hi = std::min(n, (rank + 1) * sh->chunk);
-            e.upload(d_data, true);
-            // byte-valued data: check and pack once here (KNNG_SHARD_U8=0
-            // keeps the FP32 join on the shards)
-            const char* sv = getenv("KNNG_SHARD_U8");
-            if (sv && sv[0] == '0')
-                e.u8_state = 0;
-            else
-                e.use_u8_join();
-            sh->exp_counts.alloc(n, e.pool, e.s);
-            sh->exp_off.alloc(n, e.pool, e.s);
-            sh->rcnt.alloc(n, e.pool, e.s);
-            sh->roff2.alloc(n, e.pool, e.s);
-            sh->rcur2.alloc(n, e.pool, e.s);
-            sh->bounds.alloc(nranks + 1, e.pool, e.s);
-            size_t a = 0, b = 0;
-            cub::DeviceScan::ExclusiveScan(nullptr, a, sh->exp_counts.p, sh->exp_off.p, cub::Sum(),
-                                           uint64_t(0), int(n));
-            cub::DeviceScan::ExclusiveSum(nullptr, b, sh->rcnt.p, sh->roff2.p, int(n));
-            sh->scan_bytes = std::max(a, b);
-            sh->scan_tmp.alloc(sh->scan_bytes, e.pool, e.s);
-            sh->h_bounds.resize(nranks + 1);
-            CK(cudaStreamSynchronize(e.s));
-            info->keys = e.keys.p;
-            info->flags = e.flags.p;
-            info->maxd = e.maxd.p;
-            info->rows_alloc = e.rows_alloc;
-            info->chunk = sh->chunk;
-            info->lo = e.lo;
-            info->hi = e.hi;
-            info->stream = sh->s;
-        } catch (...) {
-            delete sh;
-            throw;
-        }
+        DeviceGuard dg(params->device);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        knng_cuda_shard* sh = shard_new(d_data, true, n, d, *params, rank, nranks, st);
+        shard_fill_info(sh, info);
         *out = sh;
     });
 }
@@ -1316,70 +1526,59 @@ int knng_cuda_shard_init(knng_cuda_shard* sh, uint64_t seed) {
     });
 }
 
-int knng_cuda_shard_step(knng_cuda_shard* sh, uint64_t seed, uint64_t* out_counters,
-                         uint64_t* send_counts, const uint32_t** send_records) {
+int knng_cuda_shard_degree(knng_cuda_shard* sh) {
+    return guarded([&] {
+        if (!sh) raise(KNNG_CUDA_INVALID_ARGUMENT, "null shard");
+        DeviceGuard dg(sh->device);
+        sh->enq_degree();
+    });
+}
+
+int knng_cuda_shard_sample(knng_cuda_shard* sh, uint64_t seed, uint64_t* send_counts,
+                           const uint32_t** send_records) {
+    return guarded([&] {
+        if (!sh || !send_counts || !send_records) raise(KNNG_CUDA_INVALID_ARGUMENT, "null argument");
+        DeviceGuard dg(sh->device);
+        sh->enq_sample(seed);
+        sh->fin_sample(send_counts);
+        *send_records = reinterpret_cast<const uint32_t*>(sh->osend.p);
+    });
+}
+
+int knng_cuda_shard_offers(knng_cuda_shard* sh, const uint32_t* d_records, uint64_t count) {
+    return guarded([&] {
+        if (!sh || (count && !d_records)) raise(KNNG_CUDA_INVALID_ARGUMENT, "null argument");
+        DeviceGuard dg(sh->device);
+        sh->enq_offers(reinterpret_cast<const uint4*>(d_records), count);
+    });
+}
+
+int knng_cuda_shard_step(knng_cuda_shard* sh, uint64_t* out_counters, uint64_t* send_counts,
+                         const uint32_t** send_records) {
     return guarded([&] {
         if (!sh || !out_counters || !send_counts || !send_records)
             raise(KNNG_CUDA_INVALID_ARGUMENT, "null argument");
         DeviceGuard dg(sh->device);
-        Engine& e = *sh->e;
-        KernelTimer timer(false, e.s, nullptr);
-        ++e.iteration;
-        CK(cudaMemsetAsync(e.ctr.p, 0, sizeof(IterCounters), e.s));
-        e.select(seed, timer);
-        e.join(timer);  // local merges of the owned targets; ends with a counter read
-        const IterCounters c = *e.h_ctr;
-        // proposals for targets owned elsewhere
-        const GraphView g = e.gv();
-        launch_export_remote(g, e.cv(), e.ctr.p, sh->exp_counts.p, nullptr, nullptr, false, e.s);
-        size_t bytes = sh->scan_bytes;
-        cub::DeviceScan::ExclusiveScan(sh->scan_tmp.p, bytes, sh->exp_counts.p, sh->exp_off.p,
-                                       cub::Sum(), uint64_t(0), int(e.n), e.s);
-        shard_bounds_kernel<<<1, sh->nranks + 1, 0, e.s>>>(sh->exp_off.p, sh->exp_counts.p, e.n, sh->chunk,
-                                               sh->nranks, sh->bounds.p);
-        CK(cudaGetLastError());
-        CK(cudaMemcpyAsync(sh->h_bounds.data(), sh->bounds.p, sizeof(uint64_t) * (sh->nranks + 1),
-                           cudaMemcpyDeviceToHost, e.s));
-        CK(cudaStreamSynchronize(e.s));
-        const uint64_t total = sh->h_bounds[sh->nranks];
-        if (3 * total > sh->send_cap) {
-            sh->send.~DevBuf();
-            new (&sh->send) DevBuf<uint32_t>();
-            sh->send_cap = 3 * (total + total / 4 + 1024);
-            sh->send.alloc(sh->send_cap, e.pool, e.s);
-        }
-        if (total)
-            launch_export_remote(g, e.cv(), e.ctr.p, sh->exp_counts.p, sh->exp_off.p, sh->send.p,
-                                 true, e.s);
-        CK(cudaGetLastError());
-        CK(cudaStreamSynchronize(e.s));
-        for (uint32_t r = 0; r < sh->nranks; ++r)
-            send_counts[r] = sh->h_bounds[r + 1] - sh->h_bounds[r];
+        sh->enq_step_join();
+        sh->fin_step_join();
+        sh->fin_step_export(send_counts);
         *send_records = sh->send.p;
-        out_counters[0] = c.evals;
-        out_counters[1] = c.cands;
-        out_counters[2] = c.changes;
-        out_counters[3] = c.active;
+        out_counters[0] = sh->last.evals;
+        out_counters[1] = sh->last.cands;
+        out_counters[2] = sh->last.changes;
+        out_counters[3] = sh->last.active;
     });
 }
 
 int knng_cuda_shard_merge(knng_cuda_shard* sh, const uint32_t* d_records, uint64_t count,
                           uint64_t* changes) {
     return guarded([&] {
-        if (!sh || !changes) raise(KNNG_CUDA_INVALID_ARGUMENT, "null argument");
+        if (!sh || !changes || (count && !d_records))
+            raise(KNNG_CUDA_INVALID_ARGUMENT, "null argument");
         DeviceGuard dg(sh->device);
-        Engine& e = *sh->e;
-        if (count > sh->grouped_cap) {
-            sh->grouped.~DevBuf();
-            new (&sh->grouped) DevBuf<uint64_t>();
-            sh->grouped_cap = count + count / 4 + 1024;
-            sh->grouped.alloc(sh->grouped_cap, e.pool, e.s);
-        }
-        launch_merge_received(e.gv(), d_records, count, sh->rcnt.p, sh->roff2.p, sh->rcur2.p,
-                              sh->grouped.p, sh->scan_tmp.p, sh->scan_bytes, e.ctr.p, e.s);
-        CK(cudaGetLastError());
-        e.read_counters();
-        *changes = e.h_ctr->changes;  // local + received merges of this iteration
+        sh->enq_merge(d_records, count);
+        sh->fin_merge();
+        *changes = sh->last.changes;  // local + received merges of this iteration
     });
 }
 
@@ -1393,3 +1592,303 @@ int knng_cuda_shard_export(knng_cuda_shard* sh, uint32_t* d_ids, float* d_dists)
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// In-process multi-GPU driver: knng::run (descent.hpp:193-255) over P shards,
+// shard r on device devices[r] (default r % device count), one host thread,
+// one stream per shard.  The exchanges are peer copies (cudaMemcpyPeerAsync:
+// NVLink between B200s, a device copy when two shards share a GPU) ordered by
+// events between the shards' streams; the host reads only the counts an
+// exchange needs and the iteration's change counts.
+// ---------------------------------------------------------------------------
+namespace {
+
+struct MultiRun {
+    std::vector<knng_cuda_shard*> sh;
+    std::vector<int> dev;
+    std::vector<cudaEvent_t> ev;                  // one per shard, reused
+    std::unique_ptr<DevBuf<uint32_t>[]> ipart;    // per shard: P x n partial in-degrees
+    std::unique_ptr<DevBuf<uint4>[]> orecv;       // received offers
+    std::vector<size_t> orecv_cap;
+    std::unique_ptr<DevBuf<uint32_t>[]> rrecv;    // received proposal records
+    std::vector<size_t> rrecv_cap;
+    uint32_t P = 0, n = 0;
+    ~MultiRun() {
+        for (size_t r = 0; r < sh.size(); ++r) {
+            if (!sh[r]) continue;
+            cudaSetDevice(dev[r]);
+            cudaStreamSynchronize(sh[r]->s);
+            ipart[r].~DevBuf();
+            new (&ipart[r]) DevBuf<uint32_t>();
+            orecv[r].~DevBuf();
+            new (&orecv[r]) DevBuf<uint4>();
+            rrecv[r].~DevBuf();
+            new (&rrecv[r]) DevBuf<uint32_t>();
+            cudaStreamSynchronize(sh[r]->s);
+            delete sh[r];
+            if (ev[r]) cudaEventDestroy(ev[r]);
+        }
+    }
+    // every stream waits for every other stream's work so far (device-side)
+    void barrier() {
+        for (uint32_t r = 0; r < P; ++r) {
+            CK(cudaSetDevice(dev[r]));
+            CK(cudaEventRecord(ev[r], sh[r]->s));
+        }
+        for (uint32_t r = 0; r < P; ++r) {
+            CK(cudaSetDevice(dev[r]));
+            for (uint32_t q = 0; q < P; ++q)
+                if (q != r) CK(cudaStreamWaitEvent(sh[r]->s, ev[q], 0));
+        }
+    }
+    // the owned maxd slice of every shard into every other shard
+    void allgather_maxd() {
+        barrier();
+        const uint32_t chunk = sh[0]->chunk;
+        for (uint32_t r = 0; r < P; ++r) {
+            CK(cudaSetDevice(dev[r]));
+            for (uint32_t q = 0; q < P; ++q) {
+                if (q == r) continue;
+                const uint32_t lo = sh[q]->e->lo, hi = sh[q]->e->hi;
+                if (hi > lo)
+                    CK(cudaMemcpyPeerAsync(sh[r]->e->maxd.p + lo, dev[r], sh[q]->e->maxd.p + lo,
+                                           dev[q], sizeof(float) * (hi - lo), sh[r]->s));
+            }
+        }
+        (void)chunk;
+        barrier();
+    }
+};
+
+__global__ void sum_partials_kernel(uint32_t* out, const uint32_t* parts, uint32_t P,
+                                    uint32_t n) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint32_t s = 0;
+    for (uint32_t q = 0; q < P; ++q) s += parts[size_t(q) * n + i];
+    out[i] = s;
+}
+
+void run_multi(const float* data, uint32_t n, uint32_t d, const knng_cuda_params& p, int num_gpus,
+               const int* devices, uint32_t* out_ids, float* out_dists,
+               knng_cuda_metrics* m) {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        raise(KNNG_CUDA_CUDA_ERROR, "no CUDA device available (this library has no CPU path)");
+    }
+    if (num_gpus < 1 || uint32_t(num_gpus) > kMaxShards)
+        raise(KNNG_CUDA_INVALID_ARGUMENT, "num_gpus must be in [1, 1023]");
+    int prev = 0;
+    CK(cudaGetDevice(&prev));
+    struct Restore {
+        int d;
+        ~Restore() { cudaSetDevice(d); }
+    } restore{prev};
+    MultiRun R;
+    R.P = uint32_t(num_gpus);
+    R.n = n;
+    const uint32_t P = R.P;
+    R.sh.assign(P, nullptr);
+    R.dev.resize(P);
+    R.ev.assign(P, nullptr);
+    R.ipart.reset(new DevBuf<uint32_t>[P]);
+    R.orecv.reset(new DevBuf<uint4>[P]);
+    R.orecv_cap.assign(P, 0);
+    R.rrecv.reset(new DevBuf<uint32_t>[P]);
+    R.rrecv_cap.assign(P, 0);
+    for (uint32_t r = 0; r < P; ++r) {
+        R.dev[r] = devices ? devices[r] : int(r % uint32_t(ndev));
+        if (R.dev[r] < 0 || R.dev[r] >= ndev)
+            raise(KNNG_CUDA_INVALID_ARGUMENT, "device ordinal out of range");
+    }
+    // peer access where the hardware has it (NVLink / NVSwitch)
+    for (uint32_t r = 0; r < P; ++r)
+        for (uint32_t q = 0; q < P; ++q) {
+            if (R.dev[r] == R.dev[q]) continue;
+            int can = 0;
+            cudaDeviceCanAccessPeer(&can, R.dev[r], R.dev[q]);
+            if (can) {
+                cudaSetDevice(R.dev[r]);
+                const cudaError_t e = cudaDeviceEnablePeerAccess(R.dev[q], 0);
+                if (e != cudaSuccess) cudaGetLastError();  // already enabled
+            }
+        }
+    metrics_reset(m);
+    const double t_start = now_s();
+    for (uint32_t r = 0; r < P; ++r) {
+        CK(cudaSetDevice(R.dev[r]));
+        knng_cuda_params pr = p;
+        pr.device = R.dev[r];
+        R.sh[r] = shard_new(data, false, n, d, pr, r, P, nullptr);
+        CK(cudaEventCreateWithFlags(&R.ev[r], cudaEventDisableTiming));
+        R.ipart[r].alloc(size_t(P) * n, R.sh[r]->e->pool, R.sh[r]->s);
+    }
+    std::mt19937_64 master(p.seed);
+    const uint64_t init_seed = master();
+    for (uint32_t r = 0; r < P; ++r) {
+        CK(cudaSetDevice(R.dev[r]));
+        Engine& e = *R.sh[r]->e;
+        const bool u8 = e.u8_state == 1;
+        launch_init_random(e.gv(), init_seed, R.sh[r]->s, u8 ? e.packed.p : nullptr,
+                           u8 ? e.lnorm.p : nullptr);
+        CK(cudaGetLastError());
+    }
+    R.allgather_maxd();
+    for (uint32_t r = 0; r < P; ++r) {
+        CK(cudaSetDevice(R.dev[r]));
+        CK(cudaStreamSynchronize(R.sh[r]->s));
+    }
+    double t1 = now_s();
+    metrics_push(m, 0, t1 - t_start, uint64_t(n) * p.k, 0);
+    const double threshold = p.termination_delta * double(n) * double(p.k);
+    std::vector<uint64_t> counts(size_t(P) * P);
+    std::vector<uint64_t> seeds(p.max_iterations + 1);
+    for (uint32_t i = 1; i <= p.max_iterations; ++i) seeds[i] = master();  // reference order
+    for (uint32_t it = 1; it <= p.max_iterations; ++it) {
+        const double t0 = now_s();
+        // degree: partials, then every shard sums all of them
+        for (uint32_t r = 0; r < P; ++r) {
+            CK(cudaSetDevice(R.dev[r]));
+            R.sh[r]->enq_degree();
+        }
+        R.barrier();
+        for (uint32_t r = 0; r < P; ++r) {
+            CK(cudaSetDevice(R.dev[r]));
+            for (uint32_t q = 0; q < P; ++q)
+                CK(cudaMemcpyPeerAsync(R.ipart[r].p + size_t(q) * n, R.dev[r], R.sh[q]->e->indeg.p,
+                                       R.dev[q], sizeof(uint32_t) * n, R.sh[r]->s));
+        }
+        R.barrier();  // nobody overwrites its partial before every shard copied it
+        for (uint32_t r = 0; r < P; ++r) {
+            CK(cudaSetDevice(R.dev[r]));
+            sum_partials_kernel<<<(n + 255) / 256, 256, 0, R.sh[r]->s>>>(R.sh[r]->e->indeg.p,
+                                                                         R.ipart[r].p, P, n);
+            CK(cudaGetLastError());
+            R.sh[r]->enq_sample(seeds[it]);
+        }
+        for (uint32_t r = 0; r < P; ++r) {
+            CK(cudaSetDevice(R.dev[r]));
+            R.sh[r]->fin_sample(counts.data() + size_t(r) * P);
+        }
+        // offers: shard q's segment for r -> r
+        R.barrier();
+        for (uint32_t r = 0; r < P; ++r) {
+            CK(cudaSetDevice(R.dev[r]));
+            uint64_t total = 0;
+            for (uint32_t q = 0; q < P; ++q) total += counts[size_t(q) * P + r];
+            if (total > R.orecv_cap[r]) {
+                R.orecv[r].~DevBuf();
+                new (&R.orecv[r]) DevBuf<uint4>();
+                R.orecv_cap[r] = total + total / 4 + 1024;
+                R.orecv[r].alloc(R.orecv_cap[r], R.sh[r]->e->pool, R.sh[r]->s);
+            }
+            uint64_t at = 0;
+            for (uint32_t q = 0; q < P; ++q) {
+                const uint64_t c = counts[size_t(q) * P + r];
+                if (c)
+                    CK(cudaMemcpyPeerAsync(R.orecv[r].p + at, R.dev[r],
+                                           R.sh[q]->osend.p + size_t(r) * R.sh[q]->seg_cap,
+                                           R.dev[q], sizeof(uint4) * c, R.sh[r]->s));
+                at += c;
+            }
+            R.sh[r]->enq_offers(R.orecv[r].p, total);
+            R.sh[r]->enq_step_join();
+        }
+        for (uint32_t r = 0; r < P; ++r) {
+            CK(cudaSetDevice(R.dev[r]));
+            R.sh[r]->fin_step_join();
+        }
+        for (uint32_t r = 0; r < P; ++r) {
+            CK(cudaSetDevice(R.dev[r]));
+            R.sh[r]->fin_step_export(counts.data() + size_t(r) * P);
+        }
+        // proposal records: shard q's records for r -> r (q's records are
+        // grouped by target, hence by owner, in rank order)
+        R.barrier();
+        uint64_t evals = 0, cands = 0;
+        for (uint32_t r = 0; r < P; ++r) {
+            CK(cudaSetDevice(R.dev[r]));
+            uint64_t total = 0;
+            for (uint32_t q = 0; q < P; ++q) total += counts[size_t(q) * P + r];
+            if (3 * total > R.rrecv_cap[r]) {
+                R.rrecv[r].~DevBuf();
+                new (&R.rrecv[r]) DevBuf<uint32_t>();
+                R.rrecv_cap[r] = 3 * (total + total / 4 + 1024);
+                R.rrecv[r].alloc(R.rrecv_cap[r], R.sh[r]->e->pool, R.sh[r]->s);
+            }
+            uint64_t at = 0;
+            for (uint32_t q = 0; q < P; ++q) {
+                const uint64_t c = counts[size_t(q) * P + r];
+                uint64_t before = 0;
+                for (uint32_t t = 0; t < r; ++t) before += counts[size_t(q) * P + t];
+                if (c)
+                    CK(cudaMemcpyPeerAsync(R.rrecv[r].p + 3 * at, R.dev[r],
+                                           R.sh[q]->send.p + 3 * before, R.dev[q],
+                                           sizeof(uint32_t) * 3 * c, R.sh[r]->s));
+                at += c;
+            }
+            R.sh[r]->enq_merge(R.rrecv[r].p, total);
+            evals += R.sh[r]->last.evals;
+            cands += R.sh[r]->last.cands;
+        }
+        uint64_t changes = 0;
+        for (uint32_t r = 0; r < P; ++r) {
+            CK(cudaSetDevice(R.dev[r]));
+            R.sh[r]->fin_merge();
+            changes += R.sh[r]->last.changes;
+        }
+        R.allgather_maxd();
+        const double wall = now_s() - t0;
+        metrics_push(m, it, wall, evals, changes, cands, 0.0);
+        if (m) {
+            m->join_candidates += cands;
+            m->join_evals += evals;
+        }
+        if (double(changes) < threshold) break;
+    }
+    // owned rows -> host
+    for (uint32_t r = 0; r < P; ++r) {
+        CK(cudaSetDevice(R.dev[r]));
+        knng_cuda_shard* s = R.sh[r];
+        const uint32_t lo = s->e->lo, hi = s->e->hi;
+        if (hi <= lo) continue;
+        const size_t cnt = size_t(hi - lo) * p.k;
+        DevBuf<uint32_t> ids;
+        DevBuf<float> dd;
+        ids.alloc(cnt, s->e->pool, s->s);
+        dd.alloc(cnt, s->e->pool, s->s);
+        s->e->export_owned(ids.p, dd.p, nullptr);
+        CK(cudaMemcpyAsync(out_ids + size_t(lo) * p.k, ids.p, sizeof(uint32_t) * cnt,
+                           cudaMemcpyDeviceToHost, s->s));
+        CK(cudaMemcpyAsync(out_dists + size_t(lo) * p.k, dd.p, sizeof(float) * cnt,
+                           cudaMemcpyDeviceToHost, s->s));
+        CK(cudaStreamSynchronize(s->s));
+    }
+    if (m) {
+        uint64_t h2d = 0, d2h = 0;
+        for (uint32_t r = 0; r < P; ++r) {
+            h2d += R.sh[r]->e->h2d;
+            d2h += R.sh[r]->e->d2h + sizeof(float) * 2 * size_t(R.sh[r]->e->hi - R.sh[r]->e->lo) * p.k;
+            for (int kk = 0; kk < KNNG_CUDA_KERNEL_COUNT; ++kk) {
+                m->kernel_ms[kk] += R.sh[r]->kmetrics.kernel_ms[kk];
+                m->kernel_launches[kk] += R.sh[r]->kmetrics.kernel_launches[kk];
+            }
+        }
+        m->h2d_bytes = h2d;
+        m->d2h_bytes = d2h;
+    }
+}
+
+}  // namespace
+
+extern "C" int knng_cuda_run_multi(const float* data, uint32_t n, uint32_t d,
+                                   const knng_cuda_params* params, int num_gpus,
+                                   const int* devices, uint32_t* out_ids, float* out_dists,
+                                   knng_cuda_metrics* out_metrics) {
+    return guarded([&] {
+        if (!params || !data || !out_ids || !out_dists)
+            raise(KNNG_CUDA_INVALID_ARGUMENT, "null argument");
+        run_multi(data, n, d, *params, num_gpus, devices, out_ids, out_dists, out_metrics);
+    });
+}

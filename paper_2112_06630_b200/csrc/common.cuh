@@ -2,6 +2,9 @@
 #pragma once
 
 #include <cstdint>
+#include <stdexcept>
+#include <string>
+
 #include <cuda_runtime.h>
 
 namespace knng_cuda {
@@ -79,6 +82,38 @@ __device__ __forceinline__ uint64_t warp_sort_u64(uint64_t v) {
         }
     }
     return v;
+}
+
+// ---------------------------------------------------------------------------
+// Per-device launch facts.  One process may drive several GPUs (the in-process
+// multi-GPU driver), so kernel attributes, occupancy and SM counts are cached
+// per device ordinal, never once per process.
+// ---------------------------------------------------------------------------
+constexpr int kMaxDevices = 64;
+
+// A failed CUDA call inside a launch wrapper surfaces at once, as an exception
+// the C-ABI guard (api.cu) turns into KNNG_CUDA_CUDA_ERROR with this message,
+// instead of later under an unrelated call.
+inline void check_launch(cudaError_t e, const char* what = "CUDA call in a launch wrapper") {
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+    }
+}
+inline int current_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d & (kMaxDevices - 1);
+}
+inline uint32_t device_sm_count() {
+    static uint32_t cache[kMaxDevices] = {};
+    const int d = current_device();
+    if (!cache[d]) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d);
+        cache[d] = v > 0 ? uint32_t(v) : 148u;
+    }
+    return cache[d];
 }
 
 // Coherent (L2) loads/stores for data shared across SMs under locks.

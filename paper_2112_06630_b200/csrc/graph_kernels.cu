@@ -286,6 +286,72 @@ __global__ void __launch_bounds__(256) sample_kernel(GraphView g, CandView c,
         offer(c, g.k, indeg, v, u, is_new, r.z, r.w, det_lo, det_hi, gate);  // u into v
 }
 
+// Partitioned selection (multi-GPU): a shard walks only the edges
+// of the rows it owns.  The forward offer (v into u) is always local; the
+// reverse offer (u into v) is local when v is owned, else its acceptance is
+// drawn here (the all-reduced in-degree makes deg(v) global) and an accepted
+// offer becomes a record {v, u, is_new, slot draw} for owner(v) = v / chunk,
+// appended to that owner's segment of `send` (segments of seg_cap records,
+// counts in dst_cnt; warp-aggregated).  Edge e keeps its global index, so the
+// Philox draws — and the sampled lists — do not depend on the sharding.
+__global__ void __launch_bounds__(256) sample_owned_kernel(GraphView g, CandView c,
+                                                           const uint32_t* indeg, uint32_t seed_lo,
+                                                           uint32_t seed_hi, const IterCounters* gate,
+                                                           uint32_t chunk, uint32_t* dst_cnt,
+                                                           uint4* send, uint64_t seg_cap) {
+    const size_t e = size_t(g.lo) * g.k + size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const bool in = e < size_t(g.hi) * g.k && !gate->halt;
+    uint32_t dest = 0xffffffffu, v = 0, u = 0, is_new = 0;
+    Philox4 r{0, 0, 0, 0};
+    if (in) {
+        u = uint32_t(e / g.k);
+        const uint32_t i = uint32_t(e % g.k);
+        v = key_id(g.keys[e]);
+        is_new = (__ldg(g.flags + u) >> i) & 1u;
+        r = philox4x32_10(uint32_t(e), uint32_t(e >> 32), kSaltSample, 0u, seed_lo, seed_hi);
+        offer(c, g.k, indeg, u, v, is_new, r.x, r.y, 0u, 0u, nullptr);  // v into u
+        if (v >= g.lo && v < g.hi)
+            offer(c, g.k, indeg, v, u, is_new, r.z, r.w, 0u, 0u, nullptr);  // u into v
+        else if (accept_offer(c, g.k, indeg, v, r.z))
+            dest = v / chunk;
+    }
+    // one atomic per destination per warp
+    const uint32_t peers = __match_any_sync(0xffffffffu, dest);
+    const uint32_t leader = __ffs(peers) - 1u;
+    uint32_t base = 0;
+    if (dest != 0xffffffffu && lane_id() == leader) base = atomicAdd(dst_cnt + dest, __popc(peers));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (dest != 0xffffffffu) {
+        const uint32_t pos = base + __popc(peers & ((1u << lane_id()) - 1u));
+        send[size_t(dest) * seg_cap + pos] = make_uint4(v, u, is_new, r.w);
+    }
+}
+
+// Received reverse offers (accepted by the sender): the list insertion of
+// offer(), reservoir rule included.
+__global__ void apply_offers_kernel(CandView c, const uint4* recs, uint64_t count,
+                                    const IterCounters* gate) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= count || gate->halt) return;
+    const uint4 q = recs[i];
+    uint32_t* counter = q.z ? c.raw_new : c.raw_old;
+    const uint32_t slot = atomicAdd(counter + q.x, 1u);
+    uint32_t* list = c.ids + size_t(q.x) * 2 * c.cap + (q.z ? 0u : c.cap);
+    if (slot < c.cap) {
+        list[slot] = q.y;
+    } else {
+        const uint32_t j = bounded(q.w, slot + 1u);
+        if (j < c.cap) list[j] = q.y;
+    }
+}
+
+// Partial in-degree: the owned rows' edges only (the shards' partials sum to
+// the in-degree, all-reduced by the caller).
+__global__ void indeg_owned_kernel(GraphView g, uint32_t* indeg) {
+    const size_t e = size_t(g.lo) * g.k + size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e < size_t(g.hi) * g.k) atomicAdd(indeg + key_id(g.keys[e]), 1u);
+}
+
 // Deterministic sampling, lists that received more than 2cap offers: the
 // slots are reset, then every accepted offer into such a list is inserted
 // again into a lock-free bounded set of the 2cap smallest keys (a key only
@@ -880,12 +946,34 @@ void launch_export_rows(const GraphView& g, uint32_t* ids, float* dists, uint8_t
 
 void launch_indegree(const GraphView& g, uint32_t* indeg, cudaStream_t s,
                      const IterCounters* gate) {
-    cudaMemsetAsync(indeg, 0, sizeof(uint32_t) * g.n, s);
+    check_launch(cudaMemsetAsync(indeg, 0, sizeof(uint32_t) * g.n, s));
     indegree_kernel<<<blocks_for(size_t(g.n) * g.k, 256), 256, 0, s>>>(g, indeg, gate);
 }
 
 void launch_reset_raw(const CandView& c, uint32_t n, cudaStream_t s, const IterCounters* gate) {
     reset_raw_kernel<<<blocks_for(n, 256), 256, 0, s>>>(c, n, gate);
+}
+
+void launch_indegree_owned(const GraphView& g, uint32_t* indeg, cudaStream_t s) {
+    check_launch(cudaMemsetAsync(indeg, 0, sizeof(uint32_t) * g.n, s));
+    if (g.hi > g.lo)
+        indeg_owned_kernel<<<blocks_for(size_t(g.hi - g.lo) * g.k, 256), 256, 0, s>>>(g, indeg);
+}
+
+void launch_sample_owned(const GraphView& g, const CandView& c, const uint32_t* indeg,
+                         uint64_t seed, const IterCounters* gate, uint32_t chunk,
+                         uint32_t nranks, uint32_t* dst_cnt, uint4* send, uint64_t seg_cap,
+                         cudaStream_t s) {
+    check_launch(cudaMemsetAsync(dst_cnt, 0, sizeof(uint32_t) * nranks, s));
+    if (g.hi <= g.lo) return;
+    sample_owned_kernel<<<blocks_for(size_t(g.hi - g.lo) * g.k, 256), 256, 0, s>>>(
+        g, c, indeg, uint32_t(seed), uint32_t(seed >> 32), gate, chunk, dst_cnt, send, seg_cap);
+}
+
+void launch_apply_offers(const CandView& c, const uint4* recs, uint64_t count,
+                         const IterCounters* gate, cudaStream_t s) {
+    if (!count) return;
+    apply_offers_kernel<<<uint32_t((count + 255) / 256), 256, 0, s>>>(c, recs, count, gate);
 }
 
 void launch_sample(const GraphView& g, const CandView& c, const uint32_t* indeg, uint64_t seed,
@@ -956,7 +1044,7 @@ void launch_finalize(const GraphView& g, const CandView& c, uint32_t* active,
 
 void launch_bookkeeping(const GraphView& g, const CandView& c, uint32_t* active,
                         IterCounters* ctr, cudaStream_t s) {
-    cudaMemsetAsync(c.revcnt, 0, sizeof(uint32_t) * g.n, s);
+    check_launch(cudaMemsetAsync(c.revcnt, 0, sizeof(uint32_t) * g.n, s));
     if (g.hi <= g.lo) return;
     bookkeeping_kernel<<<blocks_for(g.hi - g.lo, kFinNodes), kFinWarps * 32, 0, s>>>(g, c, active,
                                                                                      ctr);

@@ -42,6 +42,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include "kernels.cuh"
+#include "tile_math.cuh"
 
 namespace knng_cuda {
 
@@ -151,13 +152,6 @@ __device__ __forceinline__ float* ring_base(DistShared& sh) {
     return reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(&sh) + kSlabOffset);
 }
 
-// Offset of candidate r's row in its node's proposal block (nn new, m = nn + no
-// candidates): word 0 = count, then up to m - 1 (new r) or nn (old r) keys
-// (distance bits << 32 | partner id).
-__device__ __forceinline__ size_t prow(uint32_t r, uint32_t nn, uint32_t m) {
-    return r < nn ? size_t(r) * m : size_t(nn) * m + size_t(r - nn) * (nn + 1);
-}
-
 // Float offset of row x of 8-block blk within a ring stage.
 __device__ __forceinline__ uint32_t ring_row(uint32_t blk, uint32_t x) {
     return blk * kBlkPitch + x * kSlab;
@@ -234,38 +228,6 @@ __device__ __forceinline__ void tile_slab(const float* __restrict__ slab, uint32
                 }
             }
         }
-    }
-}
-
-__device__ __forceinline__ float acc_at(const float2 (&acc)[32], uint32_t p) {
-    return (p & 1u) ? acc[p >> 1].y : acc[p >> 1].x;
-}
-
-// Reduce-scatter of the 64 per-lane partial sums over the group's 8 lanes in
-// the reference's tree order ((0+1)+(2+3))+((4+5)+(6+7)); lane
-// l8 = b0 + 2 b1 + 4 b2 ends with the 8 sums of tile row x = 4 b0 + 2 b1 + b2.
-__device__ __forceinline__ void group_reduce64(const float2 (&acc)[32], uint32_t l8,
-                                               float (&row)[8]) {
-    const bool b0 = l8 & 1u, b1 = (l8 >> 1) & 1u, b2 = (l8 >> 2) & 1u;
-    float r32[32];
-#pragma unroll
-    for (uint32_t j = 0; j < 32; ++j) {
-        const float send = b0 ? acc_at(acc, j) : acc_at(acc, 32 + j);
-        const float keep = b0 ? acc_at(acc, 32 + j) : acc_at(acc, j);
-        r32[j] = __fadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 1));
-    }
-    float r16[16];
-#pragma unroll
-    for (uint32_t j = 0; j < 16; ++j) {
-        const float send = b1 ? r32[j] : r32[16 + j];
-        const float keep = b1 ? r32[16 + j] : r32[j];
-        r16[j] = __fadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 2));
-    }
-#pragma unroll
-    for (uint32_t j = 0; j < 8; ++j) {
-        const float send = b2 ? r16[j] : r16[8 + j];
-        const float keep = b2 ? r16[8 + j] : r16[j];
-        row[j] = __fadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 4));
     }
 }
 
@@ -694,7 +656,7 @@ __global__ void __launch_bounds__(kThreads, KNNG_JOIN_MINBLOCKS) join_distances_
             }
             float row[8];
             group_reduce64(acc, l8, row);
-            const uint32_t x = 4u * (l8 & 1u) + 2u * ((l8 >> 1) & 1u) + ((l8 >> 2) & 1u);
+            const uint32_t x = reduced_row(l8);
             const uint32_t i = live ? sh.rowmap[v][rb * 8 + x] : kInvalid;
             if (i != kInvalid) {
                 // each pair is a proposal to both endpoints; kept (compacted
@@ -1074,18 +1036,6 @@ __global__ void check_capacity_kernel(IterCounters* ctr, unsigned long long capa
     ctr->overflow = ctr->dwords > capacity ? 1u : 0u;
 }
 
-uint32_t g_sm_count = 0;
-
-uint32_t sm_count() {
-    if (!g_sm_count) {
-        int dev = 0, v = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-        g_sm_count = v > 0 ? uint32_t(v) : 148u;
-    }
-    return g_sm_count;
-}
-
 }  // namespace
 
 size_t join_scan_scratch(uint32_t n) {
@@ -1101,9 +1051,9 @@ void launch_join_offsets(const CandView& c, uint32_t n, uint32_t lo, uint32_t hi
     // u in [lo, hi) only), so the block offsets are a scan of the owned range
     size_t bytes = scratch_bytes;
     if (hi > lo)
-        cub::DeviceScan::ExclusiveSum(scratch, bytes, c.dsz + lo, c.doff + lo, int(hi - lo), s);
+        check_launch(cub::DeviceScan::ExclusiveSum(scratch, bytes, c.dsz + lo, c.doff + lo, int(hi - lo), s));
     bytes = scratch_bytes;
-    cub::DeviceScan::ExclusiveSum(scratch, bytes, c.revcnt, c.roff, int(n), s);
+    check_launch(cub::DeviceScan::ExclusiveSum(scratch, bytes, c.revcnt, c.roff, int(n), s));
 }
 
 void launch_check_capacity(IterCounters* ctr, unsigned long long capacity, cudaStream_t s) {
@@ -1113,7 +1063,7 @@ void launch_check_capacity(IterCounters* ctr, unsigned long long capacity, cudaS
 void launch_scatter_rev(const CandView& c, const uint32_t* active, IterCounters* ctr,
                         uint32_t max_active, uint32_t n, cudaStream_t s) {
     if (!max_active) return;
-    cudaMemsetAsync(c.rcur, 0, sizeof(uint32_t) * n, s);
+    check_launch(cudaMemsetAsync(c.rcur, 0, sizeof(uint32_t) * n, s));
     scatter_rev_kernel<<<uint32_t((size_t(max_active) * 32 + 255) / 256), 256, 0, s>>>(c, active,
                                                                                        ctr);
 }
@@ -1132,18 +1082,20 @@ void launch_join_distances(const GraphView& g, const CandView& c, const uint32_t
         return !(v && v[0] == '0');
     }();
     if (res_slots < node_slots || !allow_resident) res_slots = 0;
-    static int per_sm = 0;  // occupancy is a property of the kernel: query once
+    static int occ[kMaxDevices] = {};  // per device: the attribute is per device
+    int& per_sm = occ[current_device()];
     if (!per_sm) {
-        cudaFuncSetAttribute(join_distances_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(kDistSmem));
+        check_launch(cudaFuncSetAttribute(join_distances_kernel,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(kDistSmem)));
         int v = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, join_distances_kernel, int(kThreads),
-                                                      kDistSmem);
+        check_launch(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, join_distances_kernel,
+                                                                   int(kThreads), kDistSmem));
         per_sm = v < 1 ? 1 : v;
     }
-    uint32_t grid = sm_count() * uint32_t(per_sm);
+    uint32_t grid = device_sm_count() * uint32_t(per_sm);
     if (grid > max_active) grid = max_active;
-    cudaMemsetAsync(&ctr->work, 0, sizeof(uint32_t), s);
+    check_launch(cudaMemsetAsync(&ctr->work, 0, sizeof(uint32_t), s));
     join_distances_kernel<<<grid, kThreads, kDistSmem, s>>>(g, c, active, ctr, res_slots, -0.0f);
 }
 
@@ -1152,7 +1104,7 @@ void launch_join_merge(const GraphView& g, const CandView& c, IterCounters* ctr,
     if (g.hi <= g.lo) return;
     const uint32_t blocks = (g.hi - g.lo + kMergeWarps - 1) / kMergeWarps;
     // the hubs it left: a CTA each, blocks looping over the device-side count
-    const uint32_t hub_blocks = std::min<uint32_t>(2 * sm_count(), (g.hi - g.lo + 1) / 2 + 1);
+    const uint32_t hub_blocks = std::min<uint32_t>(2 * device_sm_count(), (g.hi - g.lo + 1) / 2 + 1);
     if (c.det) {
         join_merge_kernel<true><<<blocks, kMergeWarps * 32, 0, s>>>(g, c, ctr, c.hubs);
         hub_merge_kernel<true><<<hub_blocks, kHubWarps * 32, 0, s>>>(g, c, ctr, c.hubs);
@@ -1168,10 +1120,10 @@ void launch_join_merge(const GraphView& g, const CandView& c, IterCounters* ctr,
 namespace {
 
 // Pass 1 (count) / pass 2 (write): one warp per non-owned target t named by
-// this device's lists.  The warp replays its merge on the replica of t's row
-// (iteration-start keys) and exports only the proposals that entered it, at
-// most k per target: a proposal outside the k best distinct ids of (t's row,
-// this device's proposals) cannot enter t's final row (SURVEY §8e
+// this device's lists.  The warp merges this device's proposals for t below
+// t's row maximum (replicated) into an empty row and exports the entries that
+// entered it, at most k per target: a proposal outside the k best distinct
+// ids of this device's proposals cannot enter t's final row (SURVEY §8e
 // pre-reduction; ties aside, as everywhere in the merge).  Both passes replay
 // the same entries in the same order, so they agree.  Records (t, id, dist
 // bits) are laid out in ascending t, hence grouped by owner device in rank
@@ -1191,9 +1143,13 @@ __global__ void __launch_bounds__(kMergeWarps * 32) export_remote_kernel(
         return;
     }
     const uint32_t k = g.k;
-    uint64_t key = lane < k ? g.keys[size_t(t) * k + lane] : kEmptyKey;
+    // the row replica is not kept (partitioned shards): start from k
+    // sentinels at t's row maximum (replicated) and keep the k best distinct
+    // proposals below it
+    const float mx = g.maxd[t];
+    uint64_t key = lane < k ? pack_key(mx, 0xffffffffu) : kEmptyKey;
     uint32_t fresh = 0;  // bit i: entry i entered from this device's proposals
-    float cur_max = key_dist(__shfl_sync(0xffffffffu, key, k - 1));
+    float cur_max = mx;
     const uint64_t* rv = c.rev + c.roff[t];
     for (uint32_t e = 0; e < cnt; ++e) {
         const uint64_t* row = c.D + rv[e];
@@ -1305,13 +1261,13 @@ void launch_merge_received(const GraphView& g, const uint32_t* records, uint64_t
                            uint32_t* cnt, uint32_t* off, uint32_t* cur, uint64_t* grouped,
                            void* scratch, size_t scratch_bytes, IterCounters* ctr,
                            cudaStream_t s) {
-    cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * g.n, s);
-    cudaMemsetAsync(cur, 0, sizeof(uint32_t) * g.n, s);
+    check_launch(cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * g.n, s));
+    check_launch(cudaMemsetAsync(cur, 0, sizeof(uint32_t) * g.n, s));
     if (count) {
         const uint32_t grid = uint32_t((count + 255) / 256);
         recv_count_kernel<<<grid, 256, 0, s>>>(records, count, cnt);
         size_t bytes = scratch_bytes;
-        cub::DeviceScan::ExclusiveSum(scratch, bytes, cnt, off, int(g.n), s);
+        check_launch(cub::DeviceScan::ExclusiveSum(scratch, bytes, cnt, off, int(g.n), s));
         recv_scatter_kernel<<<grid, 256, 0, s>>>(records, count, off, cur, grouped);
     }
     if (g.hi <= g.lo || !count) return;

@@ -551,17 +551,6 @@ __global__ void row_norms_kernel(const float* __restrict__ data, uint32_t n, uin
     }
 }
 
-uint32_t tc_sm_count() {
-    static uint32_t v = 0;
-    if (!v) {
-        int dev = 0, x = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&x, cudaDevAttrMultiProcessorCount, dev);
-        v = x > 0 ? uint32_t(x) : 148u;
-    }
-    return v;
-}
-
 }  // namespace
 
 void launch_row_norms(const float* data, uint32_t n, uint32_t stride, float* nrm2, float* nrmu,
@@ -574,10 +563,11 @@ void launch_join_tc(const GraphView& g, const CandView& c, IterCounters* ctr, ui
                     const float* nrm2, const float* nrmu, uint4* ovf, IterCounters* octr,
                     cudaStream_t s) {
     if (!max_active) return;
-    static bool attr = false;
+    static bool attrs[kMaxDevices] = {};
+    bool& attr = attrs[current_device()];
     if (!attr) {
-        cudaFuncSetAttribute(join_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(kASmemMax));
+        check_launch(cudaFuncSetAttribute(join_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(kASmemMax)));
         attr = true;
     }
     const uint32_t arena_floats = uint32_t((kASmemMax - kAArenaOffset) / sizeof(float));
@@ -586,9 +576,9 @@ void launch_join_tc(const GraphView& g, const CandView& c, IterCounters* ctr, ui
     // value (non-negative terms); the bound is scaled by 1 - 4x that
     const double gamma = (double(g.stride) / 8.0 + 3.0) * 5.9604644775390625e-08;
     const float lb_scale = float(1.0 - 4.0 * gamma);
-    cudaMemsetAsync(&ctr->work, 0, sizeof(uint32_t), s);
-    cudaMemsetAsync(octr, 0, sizeof(IterCounters), s);
-    uint32_t grid = tc_sm_count();
+    check_launch(cudaMemsetAsync(&ctr->work, 0, sizeof(uint32_t), s));
+    check_launch(cudaMemsetAsync(octr, 0, sizeof(IterCounters), s));
+    uint32_t grid = device_sm_count();
     if (grid > max_active) grid = max_active;
     join_tc_kernel<<<grid, kAThreads, kASmemMax, s>>>(g, c, ctr, nrm2, nrmu, ovf, octr,
                                                       arena_floats, lb_scale, -0.0f);
@@ -600,7 +590,7 @@ void launch_join_tc(const GraphView& g, const CandView& c, IterCounters* ctr, ui
     unsigned long long h[16];
     cudaMemcpyFromSymbolAsync(h, g_tc_prof, sizeof(h), 0, cudaMemcpyDeviceToHost, s);
     IterCounters ho;
-    cudaMemcpyAsync(&ho, octr, sizeof(ho), cudaMemcpyDeviceToHost, s);
+    check_launch(cudaMemcpyAsync(&ho, octr, sizeof(ho), cudaMemcpyDeviceToHost, s));
     cudaStreamSynchronize(s);
     const double G = grid;
     fprintf(stderr,

@@ -551,17 +551,6 @@ __global__ void __launch_bounds__(kSWarps * 32, 2)
     }
 }
 
-uint32_t u8_sm_count() {
-    static uint32_t v = 0;
-    if (!v) {
-        int dev = 0, x = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&x, cudaDevAttrMultiProcessorCount, dev);
-        v = x > 0 ? uint32_t(x) : 148u;
-    }
-    return v;
-}
-
 }  // namespace
 
 uint32_t u8_lane_bytes(uint32_t stride) { return (stride / 8 + 63) / 64 * 64; }
@@ -571,11 +560,11 @@ bool u8_eligible(const float* data, uint32_t n, uint32_t stride, uint32_t* d_fla
     // lane sums stay below 2^24: (stride / 8) * 255^2 < 2^24
     if (stride / 8 > 258) return false;
     const uint32_t one = 1;
-    cudaMemcpyAsync(d_flag, &one, sizeof(uint32_t), cudaMemcpyHostToDevice, s);
-    u8_check_kernel<<<4 * u8_sm_count(), 256, 0, s>>>(data, size_t(n) * stride, d_flag);
+    check_launch(cudaMemcpyAsync(d_flag, &one, sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+    u8_check_kernel<<<4 * device_sm_count(), 256, 0, s>>>(data, size_t(n) * stride, d_flag);
     uint32_t h = 0;
-    cudaMemcpyAsync(&h, d_flag, sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
-    cudaStreamSynchronize(s);
+    check_launch(cudaMemcpyAsync(&h, d_flag, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    check_launch(cudaStreamSynchronize(s), "byte-valued data check");
     return h == 1;
 }
 
@@ -600,9 +589,9 @@ void launch_join_u8(const GraphView& g, const CandView& c, IterCounters* ctr, ui
     if (staged_env && c2 <= 2 && 2 * (ssm + 1024) <= 233472) {
         const char* hv = getenv("KNNG_U8_HEAVY");
         heavy_nn = hv ? uint32_t(atoi(hv)) : 16u;
-        uint32_t grid = 2 * u8_sm_count();
+        uint32_t grid = 2 * device_sm_count();
         if (grid > max_active) grid = max_active;
-        cudaMemsetAsync(&ctr->work2, 0, sizeof(uint32_t), s);
+        check_launch(cudaMemsetAsync(&ctr->work2, 0, sizeof(uint32_t), s));
         if (c2 == 1) {
             cudaFuncSetAttribute(join_u8_staged_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(ssm));
@@ -618,16 +607,18 @@ void launch_join_u8(const GraphView& g, const CandView& c, IterCounters* ctr, ui
     // nodes with nn <= 8 take the swapped tile shape; KNNG_U8_SWAP=0 turns it off (A/B)
     const char* wenv = getenv("KNNG_U8_SWAP");
     const int no_swap = (wenv && wenv[0] == '0') ? 1 : 0;
-    static int per_sm = 0;
+    static int occ[kMaxDevices] = {};
+    int& per_sm = occ[current_device()];
     if (!per_sm) {
         int v = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, join_u8_kernel<2>, int(kUWarps * 32), 0);
+        check_launch(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, join_u8_kernel<2>,
+                                                                   int(kUWarps * 32), 0));
         per_sm = v < 1 ? 1 : v;
     }
-    uint32_t grid = u8_sm_count() * uint32_t(per_sm);
+    uint32_t grid = device_sm_count() * uint32_t(per_sm);
     const uint32_t need = (max_active + kUWarps - 1) / kUWarps;
     if (grid > need) grid = need;
-    cudaMemsetAsync(&ctr->work, 0, sizeof(uint32_t), s);
+    check_launch(cudaMemsetAsync(&ctr->work, 0, sizeof(uint32_t), s));
 #define KNNG_U8_CASE(CH)                                                                   \
     case CH:                                                                               \
         join_u8_kernel<CH><<<grid, kUWarps * 32, 0, s>>>(g, c, ctr, packed, lnorm, kl, heavy_nn, \

@@ -104,6 +104,18 @@ void launch_indegree(const GraphView& g, uint32_t* indeg, cudaStream_t s,
 // iteration seed, the same value finalize_det gets).
 void launch_sample(const GraphView& g, const CandView& c, const uint32_t* indeg, uint64_t seed,
                    cudaStream_t s, IterCounters* gate, uint64_t det_seed);
+// Partitioned selection (multi-GPU): the owned rows' edges only.  Partial
+// in-degree (the caller all-reduces it); sampling with local offers applied
+// and accepted remote reverse offers appended as {target, cand, is_new, slot
+// draw} to the owner's segment of send (nranks x seg_cap, counts in dst_cnt);
+// received offers inserted by launch_apply_offers.
+void launch_indegree_owned(const GraphView& g, uint32_t* indeg, cudaStream_t s);
+void launch_sample_owned(const GraphView& g, const CandView& c, const uint32_t* indeg,
+                         uint64_t seed, const IterCounters* gate, uint32_t chunk,
+                         uint32_t nranks, uint32_t* dst_cnt, uint4* send, uint64_t seg_cap,
+                         cudaStream_t s);
+void launch_apply_offers(const CandView& c, const uint4* recs, uint64_t count,
+                         const IterCounters* gate, cudaStream_t s);
 // dedup + flag_consumed + join bookkeeping (active list, block sizes, reverse counts)
 void launch_finalize(const GraphView& g, const CandView& c, uint32_t* active,
                      IterCounters* ctr, cudaStream_t s, uint64_t seed = 0);
@@ -139,6 +151,15 @@ void launch_scatter_rev(const CandView& c, const uint32_t* active, IterCounters*
 // Distance stage of the local join: every active node's distance block.
 void launch_join_distances(const GraphView& g, const CandView& c, const uint32_t* active,
                            IterCounters* ctr, uint32_t max_active, cudaStream_t s);
+// --- join_gl.cu --------------------------------------------------------------
+// Long rows: the distance stage with candidate rows loaded straight into
+// registers from a lane-major copy of the data (same proposal blocks,
+// bit-identical distances).  gl_row_floats: floats per row of that copy,
+// which holds n + 1 rows (row n all zero).
+uint32_t gl_row_floats(uint32_t stride);
+void launch_gl_pack(const float* data, uint32_t n, uint32_t stride, float* dl, cudaStream_t s);
+void launch_join_gl(const CandView& c, const float* dl, uint32_t n, uint32_t stride,
+                    IterCounters* ctr, uint32_t max_active, cudaStream_t s);
 // --- join_tc.cu --------------------------------------------------------------
 // ||x||^2 (rounded down) and ||x|| (rounded up) of every data row.
 void launch_row_norms(const float* data, uint32_t n, uint32_t stride, float* nrm2, float* nrmu,

@@ -184,14 +184,14 @@ void launch_locality_permutation(const GraphView& g, uint32_t* sigma, uint32_t* 
     init_comp_kernel<<<nblk(n, tb), tb, 0, s>>>(comp, n);
     uint32_t rounds = 0, h_merged = 1;
     while (rounds < kMaxRounds && h_merged) {
-        cudaMemsetAsync(merged, 0, 4, s);
+        check_launch(cudaMemsetAsync(merged, 0, 4, s));
         reset_best_kernel<<<nblk(n, tb), tb, 0, s>>>(best, n);
         min_edge_kernel<<<nblk(size_t(n) * g.k, tb), tb, 0, s>>>(g, comp, best);
         hook_kernel<<<nblk(n, tb), tb, 0, s>>>(comp, best, parent, n, merged);
         jump_kernel<<<nblk(n, tb), tb, 0, s>>>(comp, parent, n);
         relabel_kernel<<<nblk(n, tb), tb, 0, s>>>(comp, parent, labels + size_t(rounds) * n, n);
-        cudaMemcpyAsync(&h_merged, merged, 4, cudaMemcpyDeviceToHost, s);
-        cudaStreamSynchronize(s);
+        check_launch(cudaMemcpyAsync(&h_merged, merged, 4, cudaMemcpyDeviceToHost, s));
+        check_launch(cudaStreamSynchronize(s), "locality permutation (Boruvka round)");
         ++rounds;
     }
     // LSD: stable sorts by label_1 .. label_R (last = most significant)
@@ -199,8 +199,8 @@ void launch_locality_permutation(const GraphView& g, uint32_t* sigma, uint32_t* 
     for (uint32_t r = 0; r < rounds; ++r) {
         gather_keys_kernel<<<nblk(n, tb), tb, 0, s>>>(labels + size_t(r) * n, order_a, key_a, n);
         size_t tmp = cub_bytes;
-        cub::DeviceRadixSort::SortPairs(cub_tmp, tmp, key_a, key_b, order_a, order_b, int(n), 0,
-                                        32, s);
+        check_launch(cub::DeviceRadixSort::SortPairs(cub_tmp, tmp, key_a, key_b, order_a, order_b,
+                                                     int(n), 0, 32, s));
         std::swap(order_a, order_b);
     }
     invert_kernel<<<nblk(n, tb), tb, 0, s>>>(order_a, sigma, sigma_inv, n);

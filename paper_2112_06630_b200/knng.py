@@ -223,6 +223,28 @@ def run(data, params: RunParams = RunParams()) -> RunResult:
     return RunResult(KnnGraph(ids, dists, flags), RunMetrics._from_c(m, rows), sigma)
 
 
+def run_multi(data, params: RunParams = RunParams(), num_gpus: int = 2, devices=None):
+    """knng::run over num_gpus vertex shards in this process (C-ABI
+    knng_cuda_run_multi; shard r on devices[r], default r % device count).
+    Returns (ids, dists, metrics)."""
+    data = _as_data(data)
+    params.validate()
+    n, d = data.shape
+    if n <= params.k:
+        raise InvalidArgument("run: need n > k")
+    k = params.k
+    ids = np.zeros((n, k), np.uint32)
+    dists = np.zeros((n, k), np.float32)
+    m, rows = _metrics(params.max_iterations + 1)
+    p = params._c()
+    dev = None
+    if devices is not None:
+        dev = (C.c_int * num_gpus)(*devices)
+    check(N.lib().knng_cuda_run_multi(data, n, d, C.byref(p), num_gpus, dev, ids, dists,
+                                      C.byref(m)))
+    return ids, dists, RunMetrics._from_c(m, rows)
+
+
 def run_device(data_ptr: int, n: int, d: int, params: RunParams, out_ids_ptr: int,
                out_dists_ptr: int, stream: int = 0) -> RunMetrics:
     """knng::run on device-resident buffers (raw device pointers, e.g.

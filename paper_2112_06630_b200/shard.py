@@ -1,22 +1,30 @@
 """Multi-GPU NN-Descent: one process per GPU, vertex-range ownership.
 
-Every rank keeps the whole dataset and a replica of the whole graph; it owns
-the rows [rank * chunk, (rank + 1) * chunk).  Per iteration (reference loop
-descent.hpp:219-243):
+Every rank keeps the whole dataset; it owns the rows [rank * chunk,
+(rank + 1) * chunk): their graph rows, candidate lists, joins and merges.
+Only the row maxima (n floats, the join prefilter's bound) are replicated.
+Per iteration (reference loop descent.hpp:219-243):
 
-1. ``engine.step``: selection of the owned candidate lists over the replicated
-   graph (per-edge Philox draws, so the lists do not depend on the sharding),
-   local join of the owned active nodes, merges into owned rows, and records
-   (target, id, distance) for targets owned elsewhere, grouped by owner;
-2. ``all_to_all`` of the record counts, then of the records;
-3. ``engine.merge`` of the received records into owned rows;
-4. ``all_gather`` of the owned rows (keys, is_new flags, row maxima) into every
-   replica, ``all_reduce`` of changes / evaluations / candidates, and the
-   reference's termination test ``changes < delta * n * k``.
+1. ``engine.degree``: partial in-degree of the owned rows' edges,
+   ``all_reduce`` (sum) -> the global in-degree (turbo's deg = k + in-degree);
+2. ``engine.sample``: sampling over the owned rows' edges only; reverse offers
+   for rows owned elsewhere (accepted here) are grouped by owner,
+   ``all_to_all`` -> ``engine.offers`` inserts the received ones;
+3. ``engine.step``: finalize, local join of the owned active nodes, merges
+   into owned rows, and pre-reduced records (target, id, distance) for rows
+   owned elsewhere (<= k per target), ``all_to_all`` -> ``engine.merge``;
+4. ``all_gather`` of the owned row maxima, ``all_reduce`` of changes /
+   evaluations / candidates, and the reference's termination test
+   ``changes < delta * n * k``.
 
-The collectives go through ``torch.distributed`` (NCCL over NVLink on GPUs; the
-same runner drives a numpy engine over gloo in the CPU tests). The per-device
-work is the CUDA library (:class:`GpuShardEngine`, C-ABI knng_cuda_shard_*).
+Per-edge Philox draws keyed by the global edge index make the sampled lists
+independent of the sharding.  The collectives go through
+``torch.distributed`` (NCCL over NVLink on GPUs; the same runner drives a
+numpy engine over gloo in the CPU tests) on the library's stream (the shard
+is created on torch's current stream), so no host synchronisation orders
+them; the host reads only the counts each variable-size exchange needs and
+the iteration's counters.  One process driving N GPUs:
+``paper_2112_06630_b200.run_multi`` (C-ABI knng_cuda_run_multi, peer copies).
 """
 from __future__ import annotations
 
@@ -57,7 +65,7 @@ def seed_sequence(seed: int, count: int) -> np.ndarray:
 class GpuShardEngine:
     """This rank's share of a sharded build on its GPU (knng_cuda_shard_*)."""
 
-    def __init__(self, d_data, params: RunParams, rank: int, nranks: int):
+    def __init__(self, d_data, params: RunParams, rank: int, nranks: int, stream=None):
         import torch
         self.torch = torch
         n, d = d_data.shape
@@ -65,17 +73,21 @@ class GpuShardEngine:
         self.rank, self.nranks = rank, nranks
         self.device = d_data.device
         self._data = d_data.contiguous()
+        if stream is None:  # torch's current stream: the collectives order after our kernels
+            stream = torch.cuda.current_stream(self.device).cuda_stream
+            if stream == 0:
+                stream = 1  # cudaStreamLegacy: the default stream itself, not a library stream
         p = params._c()
         self._h = C.c_void_p()
         info = N.ShardInfo()
         check(N.lib().knng_cuda_shard_create(self._data.data_ptr(), self.n, self.d, C.byref(p),
-                                             rank, nranks, None, C.byref(self._h),
+                                             rank, nranks, stream or None, C.byref(self._h),
                                              C.byref(info)))
         self.chunk, self.lo, self.hi = int(info.chunk), int(info.lo), int(info.hi)
+        self.seg_cap = int(info.seg_cap)
         rows = int(info.rows_alloc)
-        self.keys = _device_view(info.keys, rows * self.k, "<i8", self.device)
-        self.flags = _device_view(info.flags, rows, "<i4", self.device)
         self.maxd = _device_view(info.maxd, rows, "<f4", self.device)
+        self.indeg = _device_view(info.indeg, self.n, "<i4", self.device)
 
     def seeds(self, seed: int, count: int) -> np.ndarray:
         return seed_sequence(seed, count)
@@ -83,11 +95,32 @@ class GpuShardEngine:
     def init(self, seed: int) -> None:
         check(N.lib().knng_cuda_shard_init(self._h, int(seed)))
 
-    def step(self, seed: int):
+    def degree(self):
+        """Partial in-degree of the owned rows' edges (int32 view, in place)."""
+        check(N.lib().knng_cuda_shard_degree(self._h))
+        return self.indeg
+
+    def sample(self, seed: int):
+        """(send_counts, segments): accepted reverse offers per owner rank, as
+        int32 views of 4 words per record."""
+        counts = np.zeros(self.nranks, np.uint64)
+        ptr = C.c_void_p()
+        check(N.lib().knng_cuda_shard_sample(self._h, int(seed), counts, C.byref(ptr)))
+        allrec = _device_view(ptr.value or 0, 4 * self.seg_cap * self.nranks, "<i4", self.device)
+        segs = [allrec[4 * r * self.seg_cap: 4 * (r * self.seg_cap + int(c))]
+                for r, c in enumerate(counts)]
+        return [int(c) for c in counts], segs
+
+    def offers(self, recv) -> None:
+        recv = recv.contiguous()
+        check(N.lib().knng_cuda_shard_offers(self._h, recv.data_ptr() if recv.numel() else None,
+                                             recv.numel() // 4))
+
+    def step(self):
         ctr = np.zeros(4, np.uint64)
         counts = np.zeros(self.nranks, np.uint64)
         ptr = C.c_void_p()
-        check(N.lib().knng_cuda_shard_step(self._h, int(seed), ctr, counts, C.byref(ptr)))
+        check(N.lib().knng_cuda_shard_step(self._h, ctr, counts, C.byref(ptr)))
         total = int(counts.sum())
         send = _device_view(ptr.value or 0, 3 * total, "<i4", self.device)
         return dict(evals=int(ctr[0]), cands=int(ctr[1]), active=int(ctr[3]),
@@ -133,12 +166,29 @@ class ShardedResult:
     bytes_exchanged: int = 0  # records sent by this rank (all iterations)
 
 
-def _allgather_rows(engine, group=None) -> None:
+def _exchange(segs: List, counts: List[int], width: int, dtype, dev, group=None):
+    """Variable-size all-to-all of per-destination segments (width words per
+    record); returns the concatenated received records."""
+    import torch
     import torch.distributed as dist
-    r, P, chunk, k = engine.rank, engine.nranks, engine.chunk, engine.k
-    for buf, width in ((engine.keys, k), (engine.flags, 1), (engine.maxd, 1)):
-        parts = [buf[i * chunk * width:(i + 1) * chunk * width] for i in range(P)]
-        dist.all_gather(parts, parts[r].clone(), group=group)
+    P = len(counts)
+    send_counts = torch.tensor(counts, dtype=torch.int64, device=dev)
+    recv_counts = torch.empty_like(send_counts)
+    dist.all_to_all_single(recv_counts, send_counts, group=group)
+    rc = recv_counts.tolist()  # the one host read this exchange needs
+    parts = [segs[r] for r in range(P) if counts[r]]
+    send = torch.cat(parts) if parts else torch.empty(0, dtype=dtype, device=dev)
+    recv = torch.empty(width * int(sum(rc)), dtype=dtype, device=dev)
+    dist.all_to_all_single(recv, send, output_split_sizes=[width * int(c) for c in rc],
+                           input_split_sizes=[width * int(c) for c in counts], group=group)
+    return recv
+
+
+def _allgather_maxd(engine, group=None) -> None:
+    import torch.distributed as dist
+    r, P, chunk = engine.rank, engine.nranks, engine.chunk
+    parts = [engine.maxd[i * chunk:(i + 1) * chunk] for i in range(P)]
+    dist.all_gather(parts, parts[r].clone(), group=group)
 
 
 def run_sharded(engine, params: RunParams, group=None) -> ShardedResult:
@@ -153,34 +203,34 @@ def run_sharded(engine, params: RunParams, group=None) -> ShardedResult:
     metrics = RunMetrics()
     t0 = time.perf_counter()
     engine.init(int(seeds[0]))
-    _allgather_rows(engine, group)
+    _allgather_maxd(engine, group)
     engine.sync()
     metrics.iterations.append(IterationMetrics(0, time.perf_counter() - t0, n * k, 0))
     threshold = params.termination_delta * n * k
     sent = 0
     for it in range(1, params.max_iterations + 1):
         t0 = time.perf_counter()
-        st = engine.step(int(seeds[it]))
-        send_counts = torch.tensor([3 * c for c in st["send_counts"]], dtype=torch.int64,
-                                   device=dev)
-        recv_counts = torch.empty_like(send_counts)
-        dist.all_to_all_single(recv_counts, send_counts, group=group)
-        rc = recv_counts.tolist()
-        recv = torch.empty(int(sum(rc)), dtype=torch.int32, device=dev)
-        dist.all_to_all_single(recv, st["send"], output_split_sizes=rc,
-                               input_split_sizes=send_counts.tolist(), group=group)
-        sent += 4 * int(sum(send_counts.tolist()))
-        engine.sync()
+        dist.all_reduce(engine.degree(), group=group)
+        counts, segs = engine.sample(int(seeds[it]))
+        recv = _exchange([s for s in segs], counts, 4, torch.int32, dev, group)
+        engine.offers(recv)
+        sent += 16 * sum(counts)
+        st = engine.step()
+        sc = st["send_counts"]
+        offs = np.concatenate([[0], np.cumsum(sc)]).astype(np.int64)
+        rsegs = [st["send"][3 * offs[r]: 3 * offs[r + 1]] for r in range(P)]
+        recv = _exchange(rsegs, sc, 3, torch.int32, dev, group)
+        sent += 12 * sum(sc)
         changes = engine.merge(recv)
-        _allgather_rows(engine, group)
+        _allgather_maxd(engine, group)
         tot = torch.tensor([changes, st["evals"], st["cands"]], dtype=torch.float64, device=dev)
         dist.all_reduce(tot, group=group)
-        engine.sync()
         changes_all, evals_all, cands_all = (int(x) for x in tot.tolist())
         metrics.iterations.append(IterationMetrics(it, time.perf_counter() - t0, evals_all,
                                                    changes_all, cands_all))
         if changes_all < threshold:
             break
+    engine.sync()
     for itm in metrics.iterations:
         metrics.total_wall_time_s += itm.wall_time_s
         metrics.total_dist_evals += itm.dist_evals

@@ -2,11 +2,12 @@
 the multi-process protocol of paper_2112_06630_b200/shard.py over gloo.
 
 Test infrastructure only.  It implements the same per-rank duties as the CUDA
-shard — owned-range init, selection of owned lists over the replicated graph,
-local join of owned active nodes, merges into owned rows, records for remote
-targets filtered by the replicated row maxima, merge of received records —
-with deterministic, order-independent rules (no random sampling), so a run
-over P ranks must equal the single-rank run exactly.
+shard — owned-range init, partial in-degree, selection over the owned rows'
+edges with reverse offers shipped to their owners, local join of owned active
+nodes, merges into owned rows, pre-reduced records for remote targets bounded
+by the replicated row maxima, merge of received records — with
+deterministic, order-independent rules (no random sampling), so a run over P
+ranks must equal the single-rank run exactly.
 """
 from __future__ import annotations
 
@@ -40,6 +41,7 @@ class NumpyShardEngine:
         self.keys = torch.zeros(rows * k, dtype=torch.int64)
         self.flags = torch.zeros(rows, dtype=torch.int32)
         self.maxd = torch.zeros(rows, dtype=torch.float32)
+        self.indeg = torch.zeros(self.n, dtype=torch.int32)
         self.sent_records = 0
 
     # ------------------------------------------------------------ helpers
@@ -89,33 +91,67 @@ class NumpyShardEngine:
             dists = np.array([self._d(u, v) for v in ids], np.float32)
             self._set_row(u, _keys(dists, ids), np.ones(self.k, np.int64))
 
-    def step(self, seed):
+    def _owned_ids(self):
+        k = self.k
+        keys = self.keys[self.lo * k:self.hi * k].numpy().reshape(-1, k)
+        return _ids(keys)
+
+    def degree(self):
+        """Partial in-degree of the owned rows' edges (the runner sums them)."""
+        self.indeg.zero_()
+        ids = self._owned_ids()
+        if ids.size:
+            self.indeg += torch.from_numpy(
+                np.bincount(ids.reshape(-1), minlength=self.n).astype(np.int32))
+        return self.indeg
+
+    def sample(self, seed):
+        """Owned rows' edges only: reverse edges (u -> v) to owned v stay
+        local, the others become offers {v, u, flag, 0} for owner(v)."""
+        ids = self._owned_ids()
+        flags = self.flags[self.lo:self.hi].numpy()
+        self._rev = {t: [] for t in range(self.lo, self.hi)}
+        out = [[] for _ in range(self.nranks)]
+        for r, u in enumerate(range(self.lo, self.hi)):
+            for i in range(self.k):
+                v, f = int(ids[r, i]), (int(flags[r]) >> i) & 1
+                if self.lo <= v < self.hi:
+                    self._rev[v].append((u, f))
+                else:
+                    out[min(self.nranks - 1, v // self.chunk)].append((v, u, f, 0))
+        counts = [len(o) for o in out]
+        segs = [torch.from_numpy(np.array(o, np.int64).reshape(-1).astype(np.int32))
+                for o in out]
+        self.seg_cap = max(counts + [1])
+        return counts, segs
+
+    def offers(self, recv):
+        rec = recv.numpy().reshape(-1, 4)
+        for v, u, f, _ in rec:
+            self._rev[int(v)].append((int(u), int(f)))
+
+    def step(self):
         n, k, cap = self.n, self.k, self.cap
-        keys = self.keys[: n * k].numpy().reshape(n, k)
-        flags = self.flags[:n].numpy()
+        ids = self._owned_ids()
+        flags = self.flags[self.lo:self.hi].numpy()
         maxd0 = self.maxd[:n].numpy().copy()
-        ids = _ids(keys)
-        # lists of the owned nodes: forward entries then reverse edges, first
-        # occurrence wins, each list the cap smallest ids
+        # lists of the owned nodes: forward entries, then reverse edges in
+        # source order, first occurrence wins, each list the cap smallest ids
         lists = {}
-        rev = [[] for _ in range(n)]
-        for u in range(n):
-            for i in range(k):
-                rev[ids[u, i]].append((u, (flags[u] >> i) & 1))
-        for t in range(self.lo, self.hi):
+        for r, t in enumerate(range(self.lo, self.hi)):
             seen = {}
             for i in range(k):
-                seen.setdefault(int(ids[t, i]), int((flags[t] >> i) & 1))
-            for x, f in rev[t]:
+                seen.setdefault(int(ids[r, i]), int((flags[r] >> i) & 1))
+            for x, f in sorted(self._rev[t]):
                 seen.setdefault(int(x), int(f))
             new = sorted(x for x, f in seen.items() if f)[:cap]
             old = sorted(x for x, f in seen.items() if not f)[:cap]
             lists[t] = (new, old)
         # flag_consumed on owned rows
-        for t, (new, _) in lists.items():
+        for r, (t, (new, _)) in enumerate(lists.items()):
             fl = int(self.flags[t])
             for i in range(k):
-                if int(ids[t, i]) in new:
+                if int(ids[r, i]) in new:
                     fl &= ~(1 << i)
             self.flags[t] = fl
         # local join of owned active nodes
@@ -138,20 +174,15 @@ class NumpyShardEngine:
             if self.lo <= t < self.hi:
                 changes += self._insert(t, plist)
             else:
-                # pre-reduced export: only the proposals that enter
-                # the k best distinct ids of (t's replicated row, these proposals)
-                row = self._row(t)
-                best = {int(i): float(dd) for i, dd in zip(_ids(row), _dist(row))}
+                # pre-reduced export: the k best distinct
+                # proposals below t's (replicated) row maximum
                 entered = {}
                 for pid, pd in plist:
-                    if pd >= maxd0[t] or pid == t or pid in best or pid in entered:
+                    if pd >= maxd0[t] or pid == t or pid in entered:
                         continue
                     entered[pid] = pd
-                pool = sorted([(d_, i, 0) for i, d_ in best.items()] +
-                              [(d_, i, 1) for i, d_ in entered.items()])[:k]
-                for d_, pid, fresh in pool:
-                    if fresh:
-                        records.append((t, pid, int(np.float32(d_).view(np.uint32))))
+                for d_, pid in sorted((d_, i) for i, d_ in entered.items())[:k]:
+                    records.append((t, pid, int(np.float32(d_).view(np.uint32))))
         self._local_changes = changes
         owner = [min(self.nranks - 1, t // self.chunk) for t, _, _ in records]
         order = np.argsort(owner, kind="stable") if records else []

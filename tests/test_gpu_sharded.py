@@ -64,56 +64,57 @@ def test_shard_step_exports_nothing_with_one_rank(gpu, nccl_world):
     params = kg.RunParams(k=8, max_candidates=16, seed=3)
     eng = GpuShardEngine(torch.from_numpy(data).cuda(), params, 0, 1)
     eng.init(1)
-    st = eng.step(2)
+    indeg = eng.degree()
+    torch.cuda.synchronize()
+    assert int(indeg.sum()) == 2000 * 8  # one rank owns every edge
+    counts, segs = eng.sample(2)
+    assert counts == [0] and segs[0].numel() == 0  # no reverse offers leave the rank
+    eng.offers(torch.empty(0, dtype=torch.int32, device="cuda"))
+    st = eng.step()
     assert st["send_counts"] == [0] and st["send"].numel() == 0
     assert st["evals"] > 0 and st["active"] > 0
     assert eng.merge(torch.empty(0, dtype=torch.int32, device="cuda")) >= 0
     eng.close()
 
 
-@pytest.mark.parametrize("kind,shard_u8", [
-    ("C1", "1"),
-    # C2-shaped data has hub targets; the FP32 join on the shards and the
-    # byte-valued one.  These ran into the stale proposal-block sizes of
-    # rows outside the shard (fixed: the offsets scan only the owned range)
-    # after earlier engines had left non-zero pool memory behind, so they run
-    # after the C1 case and its single-GPU build in the same process.
-    ("C2", "0"),
-    ("C2", "1"),
-    ("C4", "1"),
-])
-def test_shard_engine_two_ranks_one_process_exchange(gpu, monkeypatch, kind, shard_u8):
-    """Two shard engines of a 2-rank split in ONE process (no collectives,
-    sequential kernels — nothing waits on another rank): records exported by
-    each rank are exactly for the other rank's rows, and merging them gives a
-    graph whose recall matches the single-GPU build.  C2-shaped byte data
-    (first 12k rows) runs the shards' joins through the byte-valued kernel."""
+def _two_rank_build(data, params, k):
+    """Two shard engines of a 2-rank split in ONE process, sequential kernels
+    on one stream (nothing waits on another rank); the exchanges are done here
+    by hand.  Returns (graph ids, per-iteration record checks)."""
     import torch
     from paper_2112_06630_b200.shard import GpuShardEngine, seed_sequence
-    monkeypatch.setenv("KNNG_SHARD_U8", shard_u8)
-    cfg = datasets.CONFIGS[kind]
-    data = datasets.generate(cfg, n=12000) if kind == "C4" else datasets.generate(cfg)[:12000]
-    n, k = data.shape[0], cfg.k
-    params = kg.RunParams(k=k, max_candidates=cfg.cap, seed=0)
+    n = data.shape[0]
     dd = torch.from_numpy(data).cuda()
     engs = [GpuShardEngine(dd, params, r, 2) for r in range(2)]
-    seeds = seed_sequence(0, 31)
-    for e in engs:
-        e.init(int(seeds[0]))
+    seeds = seed_sequence(params.seed, 31)
     chunk = engs[0].chunk
 
-    def allgather():
-        for buf, w in (("keys", k), ("flags", 1), ("maxd", 1)):
-            for r in range(2):
-                src = getattr(engs[r], buf)[r * chunk * w:(r + 1) * chunk * w]
-                for q in range(2):
-                    if q != r:
-                        getattr(engs[q], buf)[r * chunk * w:(r + 1) * chunk * w].copy_(src)
-        torch.cuda.synchronize()
+    def allgather_maxd():
+        for r in range(2):
+            src = engs[r].maxd[r * chunk:(r + 1) * chunk]
+            engs[1 - r].maxd[r * chunk:(r + 1) * chunk].copy_(src)
 
-    allgather()
+    for e in engs:
+        e.init(int(seeds[0]))
+    allgather_maxd()
     for it in range(1, 31):
-        steps = [e.step(int(seeds[it])) for e in engs]
+        parts = [e.degree().clone() for e in engs]
+        total = parts[0] + parts[1]
+        assert int(total.sum()) == n * k  # every edge counted once
+        for e in engs:
+            e.indeg.copy_(total)
+        samples = [e.sample(int(seeds[it])) for e in engs]
+        for r in range(2):
+            counts, segs = samples[r]
+            assert counts[r] == 0  # local offers never leave the rank
+            recs = segs[1 - r].view(-1, 4)
+            if recs.numel():
+                tv = recs[:, 0].cpu().numpy()
+                other = engs[1 - r]
+                assert np.all((tv >= other.lo) & (tv < other.hi))
+        for r in range(2):
+            engs[r].offers(samples[1 - r][1][r].clone())
+        steps = [e.step() for e in engs]
         changes = 0
         for r in range(2):
             c = steps[r]["send_counts"]
@@ -126,14 +127,83 @@ def test_shard_engine_two_ranks_one_process_exchange(gpu, monkeypatch, kind, sha
             if len(t):
                 assert np.bincount(t).max() <= k
         for r in range(2):
-            other = 1 - r
-            changes += engs[r].merge(steps[other]["send"].clone())
-        allgather()
+            changes += engs[r].merge(steps[1 - r]["send"].clone())
+        allgather_maxd()
         if changes < params.termination_delta * n * k:
             break
     ids = torch.cat([e.export()[0] for e in engs]).cpu().numpy().astype(np.uint32)
-    ex, _ = kg.brute_force_knng(data, k)
-    single = kg.run(data, params)
-    assert kg.recall(ids, ex) >= kg.recall(single.graph.ids, ex) - 0.005
     for e in engs:
         e.close()
+    return ids
+
+
+@pytest.mark.parametrize("kind,shard_u8", [
+    ("C1", "1"),
+    # C2-shaped data has hub targets; the FP32 join on the shards and the
+    # byte-valued one, after earlier engines left non-zero pool memory behind
+    ("C2", "0"),
+    ("C2", "1"),
+    ("C4", "1"),
+])
+def test_shard_engine_two_ranks_one_process_exchange(gpu, monkeypatch, kind, shard_u8):
+    """A 2-rank split through the C-ABI phases (degree, sample, offers, step,
+    merge) with the exchanges done by hand: offers and records go only to the
+    owner, records are pre-reduced, and the graph's recall matches the
+    single-GPU build."""
+    monkeypatch.setenv("KNNG_SHARD_U8", shard_u8)
+    cfg = datasets.CONFIGS[kind]
+    data = datasets.generate(cfg, n=12000) if kind == "C4" else datasets.generate(cfg)[:12000]
+    k = cfg.k
+    params = kg.RunParams(k=k, max_candidates=cfg.cap, seed=0)
+    ids = _two_rank_build(data, params, k)
+    ex, _ = kg.brute_force_knng(data, k)
+    single = kg.run(data, params)
+    r_sh, r_single = kg.recall(ids, ex), kg.recall(single.graph.ids, ex)
+    assert abs(r_sh - r_single) <= 0.005, (r_sh, r_single)
+
+
+@pytest.mark.parametrize("kind,n,shards", [
+    ("C1", None, 2),
+    ("C1", None, 3),
+    ("C2", 12000, 2),
+    ("C3", 20000, 4),
+    ("C4", 20000, 2),
+    ("C4", 20000, 8),
+])
+def test_run_multi_matches_single_gpu(gpu, kind, n, shards):
+    """knng_cuda_run_multi: the vertex-sharded build driven from one process
+    (peer copies between the shards' streams; on one GPU every shard shares
+    the device).  Recall within 0.5 pp of the single-GPU build from the same
+    seed, the initial graph's evaluations counted once, rows sorted."""
+    cfg = datasets.CONFIGS[kind]
+    if n is None:
+        data = datasets.generate(cfg)
+    elif kind in ("C3", "C4"):
+        data = datasets.generate(cfg, n=n)
+    else:
+        data = datasets.generate(cfg)[:n]
+    params = kg.RunParams(k=cfg.k, max_candidates=cfg.cap, seed=0)
+    ids, dists, m = kg.run_multi(data, params, num_gpus=shards)
+    single = kg.run(data, params)
+    ex, _ = kg.brute_force_knng(data, cfg.k)
+    r_multi, r_single = kg.recall(ids, ex), kg.recall(single.graph.ids, ex)
+    assert abs(r_multi - r_single) <= 0.005, (r_multi, r_single)
+    assert m.iterations[0].dist_evals == data.shape[0] * cfg.k
+    assert abs(len(m.iterations) - len(single.metrics.iterations)) <= 2
+    assert np.all(np.diff(dists, axis=1) >= 0)
+    assert all(len(set(r)) == cfg.k for r in ids.tolist())
+    assert not np.any(ids == np.arange(data.shape[0])[:, None])
+    # the distances are the pairs' true distances (to FP32 rounding)
+    i = np.arange(0, data.shape[0], 97)
+    d64 = ((data[i, None, :].astype(np.float64) - data[ids[i]].astype(np.float64)) ** 2).sum(-1)
+    assert np.allclose(dists[i], d64, rtol=1e-4, atol=1e-4)
+
+
+def test_nndescent_l2_num_gpus(gpu):
+    """The north-star entry point with num_gpus > 1 runs the sharded build."""
+    cfg = datasets.CONFIGS["C1"]
+    data = datasets.generate(cfg)
+    ids, dists, m = kg.nndescent_l2(data, k=20, sample_rate=1.0, seed=0, num_gpus=2)
+    ex, _ = kg.brute_force_knng(data, 20)
+    single = kg.run(data, kg.RunParams(k=20, max_candidates=20, seed=0))
+    assert abs(kg.recall(ids, ex) - kg.recall(single.graph.ids, ex)) <= 0.005
