@@ -231,15 +231,61 @@ __device__ __forceinline__ void tile_slab(const float* __restrict__ slab, uint32
     }
 }
 
+// One 32-float slab of a U tile: the (at most 4) leftover new rows of a node
+// — rows 0..3 of A-block a_blk — against 16 columns, the rows of B-blocks
+// b_blk and b2_blk.  Leftover rows pair only through the reference's
+// flexible paths, so every pair is unfused.  acc[8 x + j] holds pairs
+// (x, 2j) and (x, 2j + 1), j < 4 in b_blk and j >= 4 in b2_blk; after
+// group_reduce64 the lane holding row X has pairs (X / 2, 8 (X % 2) + y),
+// i.e. one whole column block.  A node with nn = 4, no = 26 takes two U tiles
+// instead of four 8 x 8 tiles with half their rows empty.
+__device__ __forceinline__ void tile_slab_u(const float* __restrict__ slab, uint32_t a_blk,
+                                            uint32_t b_blk, uint32_t b2_blk, uint32_t l8,
+                                            uint32_t nseg, float2 minus_zero, float2 (&acc)[32]) {
+    const float2 minus_one = make_float2(-1.0f, -1.0f);
+#pragma unroll
+    for (uint32_t s = 0; s < kSlab / 8; ++s) {
+        if (s >= nseg) break;
+        const float* pa = slab + ring_row(a_blk, 0) + 8 * s + l8;
+        const float* pb = slab + ring_row(b_blk, 0) + 8 * s + l8;
+        const float* pc = slab + ring_row(b2_blk, 0) + 8 * s + l8;
+        float a[4];
+        float2 b[8];
+#pragma unroll
+        for (uint32_t x = 0; x < 4; ++x) a[x] = pa[x * kSlab];
+#pragma unroll
+        for (uint32_t j = 0; j < 4; ++j) {
+            b[j].x = pb[(2 * j) * kSlab];
+            b[j].y = pb[(2 * j + 1) * kSlab];
+            b[4 + j].x = pc[(2 * j) * kSlab];
+            b[4 + j].y = pc[(2 * j + 1) * kSlab];
+        }
+#pragma unroll
+        for (uint32_t x = 0; x < 4; ++x) {
+            const float2 ax = make_float2(a[x], a[x]);
+#pragma unroll
+            for (uint32_t j = 0; j < 8; ++j) {
+                const float2 diff = __ffma2_rn(b[j], minus_one, ax);
+                const float2 sq = __ffma2_rn(diff, diff, minus_zero);  // see tile_slab
+                acc[8 * x + j] = __fadd2_rn(acc[8 * x + j], sq);
+            }
+        }
+    }
+}
+
 // Per-node slot geometry (see the file comment): fullN/fullO, the padded
 // fused/unfused row and column extents, and the slot -> index maps.
-struct NodeGeom {
+// kContig (the U-tile kernel): with no fused rows (nn < 5) no pair is fused,
+// so the columns are laid out contiguously, [new | old], instead of fused ++
+// leftover blocks.
+template <bool kContig>
+struct NodeGeomT {
     uint32_t nn, no, fn, fo, rf, rs, cf, cs;
     __device__ __forceinline__ void set(uint32_t nn_, uint32_t no_) {
         nn = nn_;
         no = no_;
         fn = nn - nn % 5;
-        fo = no - no % 5;
+        fo = (fn || !kContig) ? no - no % 5 : 0u;
         rf = (fn + 7) & ~7u;
         rs = (nn - fn + 7) & ~7u;
         cf = (fn + fo + 7) & ~7u;
@@ -247,6 +293,9 @@ struct NodeGeom {
     }
     __device__ __forceinline__ uint32_t rbs() const { return (rf + rs) / 8; }
     __device__ __forceinline__ uint32_t cbs() const { return (cf + cs) / 8; }
+    // U tiles (4 x 16, see tile_slab_u): the leftover-row block rf / 8 against
+    // column-block pairs (2p, 2p + 1); only when there are leftover rows
+    __device__ __forceinline__ uint32_t uts() const { return rs ? (cbs() + 1) / 2 : 0u; }
     __device__ __forceinline__ uint32_t row(uint32_t sl) const {  // row slot -> new index
         if (sl < fn) return sl;
         if (sl >= rf && sl - rf < nn - fn) return fn + (sl - rf);
@@ -295,9 +344,14 @@ __device__ unsigned long long g_join_stats[8];
 // share one tile sweep, one set of barriers and one staging pass instead of
 // paying them per node.  res_slots > 0 selects resident mode with that slot
 // budget; 0 selects pass mode.
+// kU: U tiles (tile_slab_u) for nodes without fused rows — the long-row
+// instantiation; the other keeps 8x8 tiles only (see launch_join_distances).
+template <bool kU>
 __global__ void __launch_bounds__(kThreads, KNNG_JOIN_MINBLOCKS) join_distances_kernel(
     GraphView g, CandView c, const uint32_t* __restrict__ active, IterCounters* ctr,
     uint32_t res_slots, float minus_zero) {
+    using NodeGeom = NodeGeomT<kU>;
+    constexpr bool utiles = kU;
     const float2 mz2 = make_float2(minus_zero, minus_zero);  // -0.0f, opaque to ptxas
     extern __shared__ __align__(128) unsigned char smem_raw[];
     DistShared& sh = *reinterpret_cast<DistShared*>(smem_raw);
@@ -460,37 +514,60 @@ __global__ void __launch_bounds__(kThreads, KNNG_JOIN_MINBLOCKS) join_distances_
         // barriers while the other warps' row copies are in flight)
         if (tid < 32) {
             const uint32_t lane = tid;
-            uint32_t total = 0;
+            // phase 0: fused 8x8 tiles; 1: unfused 8x8 tiles (with U tiles on:
+            // all but the leftover-row block); 2: U tiles.  Each run is padded
+            // to whole warps so every warp runs one path.
+            // U tiles only for nodes without fused rows (nn < 5: late
+            // iterations); they lose to 8x8 tiles when they share a pass with
+            // a node's fused tiles (C5 iterations 1-4, measured)
+            auto count = [&](const NodeGeom& ng, uint32_t phase) -> uint32_t {
+                if (phase == 2) return utiles && ng.fn == 0 ? ng.uts() : 0u;
+                return ng.rbs() * ng.cbs();
+            };
+            uint32_t total01 = 0, total2 = 0;
             for (uint32_t v = 0; v < nv; ++v) {
                 NodeGeom ng;
                 ng.set(B.vnn[v], B.vno[v]);
-                total += ng.rbs() * ng.cbs();
+                total01 += count(ng, 0);
+                total2 += count(ng, 2);
             }
             uint32_t nt = 0;
-            for (uint32_t phase = 0; phase < 2; ++phase) {
+            for (uint32_t phase = 0; phase < (total2 ? 3u : 2u); ++phase) {
+                const uint32_t total = phase == 2 ? total2 : total01;
                 for (uint32_t t0 = 0; t0 < total; t0 += 32) {
                     uint32_t t = t0 + lane, v = 0, rb = 0, cb = 0;
                     bool live = false;
                     if (t < total) {
                         NodeGeom ng;
                         ng.set(B.vnn[0], B.vno[0]);
-                        while (t >= ng.rbs() * ng.cbs()) {
-                            t -= ng.rbs() * ng.cbs();
+                        while (t >= count(ng, phase)) {
+                            t -= count(ng, phase);
                             ++v;
                             ng.set(B.vnn[v], B.vno[v]);
                         }
-                        rb = t / ng.cbs();
-                        cb = t % ng.cbs();
-                        const bool fused_tile = rb * 8 < ng.rf && cb * 8 < ng.cf;
-                        if (fused_tile == (phase == 0)) {
-                            uint32_t imin = kInvalid;
-                            for (uint32_t x = 0; x < 8; ++x)
-                                imin = min(imin, uint32_t(sh.rowmap[v][rb * 8 + x]));
-                            if (imin != kInvalid)
-                                for (uint32_t y = 0; y < 8; ++y) {
-                                    const uint32_t col = sh.colmap[B.colbase[v] + cb * 8 + y];
-                                    live |= col != kInvalid && (col >= ng.nn || col > imin);
-                                }
+                        if (phase == 2) {
+                            // U tile t: leftover rows x column blocks 2t, 2t + 1
+                            rb = ng.rf / 8;
+                            cb = 0x80u | t;
+                            for (uint32_t y = 0; y < 16 && 16 * t + y < ng.cf + ng.cs; ++y) {
+                                const uint32_t col = sh.colmap[B.colbase[v] + 16 * t + y];
+                                live |= col != kInvalid && (col >= ng.nn || col > ng.fn);
+                            }
+                        } else {
+                            rb = t / ng.cbs();
+                            cb = t % ng.cbs();
+                            const bool fused_tile = rb * 8 < ng.rf && cb * 8 < ng.cf;
+                            const bool u_row = utiles && ng.fn == 0;  // all its tiles are U tiles
+                            if (fused_tile == (phase == 0) && !u_row) {
+                                uint32_t imin = kInvalid;
+                                for (uint32_t x = 0; x < 8; ++x)
+                                    imin = min(imin, uint32_t(sh.rowmap[v][rb * 8 + x]));
+                                if (imin != kInvalid)
+                                    for (uint32_t y = 0; y < 8; ++y) {
+                                        const uint32_t col = sh.colmap[B.colbase[v] + cb * 8 + y];
+                                        live |= col != kInvalid && (col >= ng.nn || col > imin);
+                                    }
+                            }
                         }
                     }
                     const uint32_t mask = __ballot_sync(0xffffffffu, live);
@@ -499,7 +576,7 @@ __global__ void __launch_bounds__(kThreads, KNNG_JOIN_MINBLOCKS) join_distances_
                             uint16_t((v << 13) | (rb << 8) | cb);
                     nt += __popc(mask);
                 }
-                if (phase == 0) {  // pad the fused run to whole warps with dead tiles
+                if (phase == 0 || (phase == 1 && total2)) {  // pad the run to whole warps
                     const uint32_t padded = (nt + 3u) & ~3u;
                     if (lane < padded - nt) sh.tiles[nt + lane] = kDeadTile;
                     nt = padded;
@@ -534,7 +611,13 @@ __global__ void __launch_bounds__(kThreads, KNNG_JOIN_MINBLOCKS) join_distances_
                             const uint32_t cb0 = B.colbase[v] / 8;
                             const uint32_t ab =
                                 cb0 + (rb * 8 < ng.rf ? rb : ng.cf / 8 + (rb - ng.rf / 8));
-                            m = (1ull << ab) | (1ull << (cb0 + cb));
+                            if (kU && (cb & 0x80u)) {  // U tile: column blocks 2t, 2t + 1
+                                const uint32_t c0 = 2 * (cb & 0x7fu);
+                                m = (1ull << ab) | (1ull << (cb0 + c0));
+                                if (c0 + 1 < ng.cbs()) m |= 1ull << (cb0 + c0 + 1);
+                            } else {
+                                m = (1ull << ab) | (1ull << (cb0 + cb));
+                            }
                         }
                     }
 #pragma unroll
@@ -577,15 +660,20 @@ __global__ void __launch_bounds__(kThreads, KNNG_JOIN_MINBLOCKS) join_distances_
             const uint32_t tile0 = group < pass_len && t < n_tiles ? sh.tiles[t] : kDeadTile;
             const bool live = tile0 != kDeadTile;
             const uint32_t tile = live ? tile0 : 0u;
-            const uint32_t v = tile >> 13, rb = (tile >> 8) & 31u, cb = tile & 0xffu;
+            const uint32_t v = tile >> 13, rb = (tile >> 8) & 31u;
+            const bool utile = kU && (tile & 0x80u) != 0u;
             NodeGeom ng;
             ng.set(B.vnn[v], B.vno[v]);
-            const bool fused = rb * 8 < ng.rf && cb * 8 < ng.cf;
+            // 8x8 tiles: column block cb; U tiles: blocks 2t and 2t + 1
+            const uint32_t cb = utile ? 2u * (tile & 0x7fu) : (tile & 0xffu);
+            const bool cb2_ok = utile && cb + 1 < ng.cbs();
+            const bool fused = !utile && rb * 8 < ng.rf && cb * 8 < ng.cf;
             // row slot block -> column slot block holding the same new
             // candidates, then into the batch's column-slot space
             const uint32_t cb0 = B.colbase[v] / 8;
             const uint32_t a_blk = cb0 + (rb * 8 < ng.rf ? rb : ng.cf / 8 + (rb - ng.rf / 8));
             const uint32_t b_blk = cb0 + cb;
+            const uint32_t b2_blk = cb2_ok ? b_blk + 1 : b_blk;  // past the node: ignored
             float2 acc[32];
 #pragma unroll
             for (uint32_t p = 0; p < 32; ++p) acc[p] = make_float2(0.0f, 0.0f);
@@ -594,7 +682,9 @@ __global__ void __launch_bounds__(kThreads, KNNG_JOIN_MINBLOCKS) join_distances_
                     for (uint32_t s = 0; s < n_slabs; ++s) {
                         const float* slab = ring_base(sh) + size_t(s) * (res_slots / 8) * kBlkPitch;
                         const uint32_t nseg = min(kSlab, stride - s * kSlab) / 8u;
-                        if (fused)
+                        if (utile)
+                            tile_slab_u(slab, a_blk, b_blk, b2_blk, l8, nseg, mz2, acc);
+                        else if (fused)
                             tile_slab<true>(slab, a_blk, b_blk, l8, nseg, mz2, acc);
                         else
                             tile_slab<false>(slab, a_blk, b_blk, l8, nseg, mz2, acc);
@@ -602,6 +692,7 @@ __global__ void __launch_bounds__(kThreads, KNNG_JOIN_MINBLOCKS) join_distances_
             } else {
                 const uint32_t a_pos = live ? sh.blkpos[a_blk] : 0u;
                 const uint32_t b_pos = live ? sh.blkpos[b_blk] : 0u;
+                const uint32_t b2_pos = live && cb2_ok ? sh.blkpos[b2_blk] : b_pos;
                 // kStages-deep cp.async ring, one barrier per slab.  Thread
                 // tid stages 16-byte chunk tid % kC4 of ring rows
                 // tid / kC4 + kSweep q; its data rows are read from the ring
@@ -646,7 +737,9 @@ __global__ void __launch_bounds__(kThreads, KNNG_JOIN_MINBLOCKS) join_distances_
                     const float* slab = ring_base(sh) + size_t(st) * kPassBlk * kBlkPitch;
                     const uint32_t nseg = min(kSlab, stride - sl * kSlab) / 8u;
                     if (live) {
-                        if (fused)
+                        if (utile)
+                            tile_slab_u(slab, a_pos, b_pos, b2_pos, l8, nseg, mz2, acc);
+                        else if (fused)
                             tile_slab<true>(slab, a_pos, b_pos, l8, nseg, mz2, acc);
                         else
                             tile_slab<false>(slab, a_pos, b_pos, l8, nseg, mz2, acc);
@@ -656,8 +749,12 @@ __global__ void __launch_bounds__(kThreads, KNNG_JOIN_MINBLOCKS) join_distances_
             }
             float row[8];
             group_reduce64(acc, l8, row);
-            const uint32_t x = reduced_row(l8);
-            const uint32_t i = live ? sh.rowmap[v][rb * 8 + x] : kInvalid;
+            const uint32_t X = reduced_row(l8);
+            // this lane's 8 pairs: row slot rb * 8 + x against column block cbx
+            const uint32_t x = utile ? X >> 1 : X;
+            const uint32_t cbx = utile ? cb + (X & 1u) : cb;
+            const bool col_ok = !utile || (X & 1u) == 0u || cb2_ok;
+            const uint32_t i = live && col_ok ? sh.rowmap[v][rb * 8 + x] : kInvalid;
             if (i != kInvalid) {
                 // each pair is a proposal to both endpoints; kept (compacted
                 // into the endpoint's row) only if it beats that candidate's
@@ -670,7 +767,7 @@ __global__ void __launch_bounds__(kThreads, KNNG_JOIN_MINBLOCKS) join_distances_
                 const float mx_i = sh.colmax[slot_i];
 #pragma unroll
                 for (uint32_t y = 0; y < 8; ++y) {
-                    const uint32_t slot_c = B.colbase[v] + cb * 8 + y;
+                    const uint32_t slot_c = B.colbase[v] + cbx * 8 + y;
                     const uint32_t col = sh.colmap[slot_c];
                     if (col == kInvalid || !(col >= nn || col > i)) continue;
                     // an id listed twice pairs with itself: try_insert ignores
@@ -1082,21 +1179,28 @@ void launch_join_distances(const GraphView& g, const CandView& c, const uint32_t
         return !(v && v[0] == '0');
     }();
     if (res_slots < node_slots || !allow_resident) res_slots = 0;
-    static int occ[kMaxDevices] = {};  // per device: the attribute is per device
-    int& per_sm = occ[current_device()];
+    // U tiles for long rows in pass mode: they cut the leftover-row padding of
+    // late iterations, which binds when each tile streams many slabs (C5:
+    // join 478 -> 451 ms); on short rows the extra tile phase costs more than
+    // it saves (C3: 24.9 -> 26.9 ms).  KNNG_JOIN_UTILES=0 / 1 forces them
+    // off / on (pass mode).
+    const char* uv = getenv("KNNG_JOIN_UTILES");
+    const bool utiles = res_slots == 0 && (uv ? uv[0] == '1' : g.stride >= 512);
+    auto kern = utiles ? join_distances_kernel<true> : join_distances_kernel<false>;
+    static int occ[kMaxDevices][2] = {};  // per device: the attribute is per device
+    int& per_sm = occ[current_device()][utiles ? 1 : 0];
     if (!per_sm) {
-        check_launch(cudaFuncSetAttribute(join_distances_kernel,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+        check_launch(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           int(kDistSmem)));
         int v = 0;
-        check_launch(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, join_distances_kernel,
-                                                                   int(kThreads), kDistSmem));
+        check_launch(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern, int(kThreads),
+                                                                   kDistSmem));
         per_sm = v < 1 ? 1 : v;
     }
     uint32_t grid = device_sm_count() * uint32_t(per_sm);
     if (grid > max_active) grid = max_active;
     check_launch(cudaMemsetAsync(&ctr->work, 0, sizeof(uint32_t), s));
-    join_distances_kernel<<<grid, kThreads, kDistSmem, s>>>(g, c, active, ctr, res_slots, -0.0f);
+    kern<<<grid, kThreads, kDistSmem, s>>>(g, c, active, ctr, res_slots, -0.0f);
 }
 
 void launch_join_merge(const GraphView& g, const CandView& c, IterCounters* ctr,

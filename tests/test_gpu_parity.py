@@ -164,6 +164,49 @@ def test_candidate_distances_bit_exact(gpu, restated, kind, n, k, cap, seed, t):
     assert checked > 0
 
 
+VARIANT_CASES = [("C1", 10000, 20, 20, 0, 5), ("C3", 4000, 30, 50, 2, 4),
+                 ("C5", 2000, 20, 50, 4, 2), ("C5", 2000, 20, 50, 4, 8),
+                 ("D100", 1500, 12, 20, 5, 2), ("G24", 600, 8, 15, 11, 3)]
+
+
+@pytest.mark.parametrize("env", ["KNNG_JOIN_UTILES=1", "KNNG_JOIN_UTILES=0", "KNNG_JOIN_GL=1"])
+@pytest.mark.parametrize("kind,n,k,cap,seed,t", VARIANT_CASES)
+def test_join_variants_match_oracle(gpu, restated, monkeypatch, env, kind, n, k, cap, seed, t):
+    """The distance-stage variants forced on — U tiles for the leftover rows
+    (join.cu tile_slab_u; default for long rows), 8x8 tiles only, and the
+    register-staged kernel (join_gl.cu, opt-in) — give the oracle's
+    accepted-update set and the reference's exact distance for every pair."""
+    name, val = env.split("=")
+    monkeypatch.setenv(name, val)
+    data = make_data(kind, n, seed)
+    gi, c, go, _, ev_ref = restated.capture_step(data, k, cap, seed, t)
+    cands = kg.CandidateSet(c.ids, c.new_counts, c.old_counts)
+    g, _, _, ev = kg.compute_step(data, gi.ids, gi.dists, gi.flags, cands)
+    assert ev == ev_ref
+    st = compare_step(gi, go, g, restated=restated, data=data)
+    assert st["mismatch"] == 0 and st["flag_mismatch"] == 0, st
+    assert st["bit_exact"] + st["other_path"] == st["common"], st
+    got = kg.candidate_distances(data, cands)
+    stride = (data.shape[1] + 7) // 8 * 8
+    pdata = np.zeros((n, stride), np.float32)
+    pdata[:, : data.shape[1]] = data
+    checked = 0
+    for u, D in list(got.items())[:: max(1, len(got) // 200)]:
+        nn, no = int(c.new_counts[u]), int(c.old_counts[u])
+        new = c.ids[u, :nn]
+        old = c.ids[u, cap: cap + no]
+        if nn >= 2:
+            mat, _ = restated.mutual_block(pdata[new])
+            iu = np.triu_indices(nn, 1)
+            assert np.array_equal(bits(D[:, :nn][iu]), bits(mat[iu])), u
+        for i0 in range(0, nn, 5):
+            for j0 in range(0, no, 5):
+                tile = restated.block_l2_sq(pdata[new[i0:i0 + 5]], pdata[old[j0:j0 + 5]])
+                assert np.array_equal(bits(D[i0:i0 + 5, nn + j0: nn + j0 + 5]), bits(tile)), u
+        checked += 1
+    assert checked > 0
+
+
 def test_init_random_properties(gpu, restated):
     data = make_data("C1", 3000)
     g, rev, ev = kg.init_random(data, 20, 77)
