@@ -365,6 +365,9 @@ def run_sharded_bench(args, rank, world, local):
     import paper_2112_06630_b200 as kg
     from paper_2112_06630_b200.shard import GpuShardEngine, gather_graph, run_sharded
     torch.cuda.set_device(local)
+    if "RANK" not in os.environ:  # --sharded on one GPU without torchrun
+        os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1",
+                          MASTER_PORT=str(29500 + os.getpid() % 1000))
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = datasets.CONFIGS[args.config]
     data = datasets.generate(cfg)  # same instance on every rank (replicated data)
