@@ -480,7 +480,10 @@ struct Engine {
         timer.end(h);
         h = timer.begin(KNNG_CUDA_KERNEL_JOIN);
         if (use_u8_join()) {
-            launch_join_u8(gv(), cv(), cur, n, packed.p, lnorm.p, s);
+            if (use_u8_tc())
+                launch_join_u8_tc(u8_map, cv(), cur, n, lnorm.p, s);
+            else
+                launch_join_u8(gv(), cv(), cur, n, packed.p, lnorm.p, s);
         } else if (use_gl_join()) {
             if (!dl_valid) {
                 if (!dl.p) dl.alloc(size_t(n + 1) * gl_row_floats(stride), pool, s);
@@ -529,6 +532,23 @@ struct Engine {
             }
         }
         return u8_state == 1;
+    }
+
+    // Byte-valued data on tcgen05 (join_u8_tc.cu) when its shapes are
+    // supported: KNNG_U8_TC=1 / 0 forces it on / off.  The tensor map of the
+    // byte copy is made once per packing.
+    alignas(64) unsigned char u8_map[128] = {};
+    const unsigned char* u8_map_for = nullptr;
+    bool use_u8_tc() {
+        const char* v = getenv("KNNG_U8_TC");
+        const bool want = v ? v[0] == '1' : false;
+        if (!want || !u8_tc_supported(stride, cap)) return false;
+        if (u8_map_for != packed.p) {
+            if (!u8_tc_make_map(packed.p, n, stride, u8_map))
+                raise(KNNG_CUDA_CUDA_ERROR, "cuTensorMapEncodeTiled failed for the byte copy");
+            u8_map_for = packed.p;
+        }
+        return true;
     }
 
     // The register-staged join (join_gl.cu) is opt-in: KNNG_JOIN_GL=1.

@@ -182,6 +182,14 @@ void launch_u8_pack(const float* data, uint32_t n, uint32_t stride, uint8_t* pac
                     int32_t* lnorm, cudaStream_t s);
 void launch_join_u8(const GraphView& g, const CandView& c, IterCounters* ctr, uint32_t max_active,
                     const uint8_t* packed, const int32_t* lnorm, cudaStream_t s);
+// --- join_u8_tc.cu -----------------------------------------------------------
+// The byte-valued join on tcgen05 (TMA gather4 -> SMEM -> kind::i8 MMA -> TMEM),
+// bit-identical to launch_join_u8.  Supported for Kl = 128 and cap <= 52; the
+// tensor map (CUtensorMap, 128 bytes) describes the lane-major byte copy.
+bool u8_tc_supported(uint32_t stride, uint32_t cap);
+bool u8_tc_make_map(const uint8_t* packed, uint32_t n, uint32_t stride, void* map_out);
+void launch_join_u8_tc(const void* map, const CandView& c, IterCounters* ctr,
+                       uint32_t max_active, const int32_t* lnorm, cudaStream_t s);
 // Update stage: one warp per target pulls and merges its proposals.
 void launch_join_merge(const GraphView& g, const CandView& c, IterCounters* ctr,
                        cudaStream_t s);

@@ -27,6 +27,7 @@ def u8_data(n, d, seed, sparse=True):
 @pytest.mark.parametrize("kind,n,k,cap,seed,t", [
     ("C2", 3000, 20, 50, 1, 1), ("C2", 3000, 20, 50, 1, 2), ("C2", 3000, 20, 50, 1, 6),
     ("U8_100", 2000, 12, 20, 3, 1), ("U8_128", 3000, 10, 50, 4, 2), ("U8_24", 1500, 8, 15, 5, 1),
+    ("U8_1000", 1500, 10, 40, 6, 1), ("U8_1000", 1500, 10, 40, 6, 3),
 ])
 def test_u8_step_equals_fp32_kernel_and_oracle(gpu, restated, monkeypatch, kind, n, k, cap, seed,
                                                t):
@@ -34,7 +35,7 @@ def test_u8_step_equals_fp32_kernel_and_oracle(gpu, restated, monkeypatch, kind,
     gi, c, go, _, ev_ref = restated.capture_step(data, k, cap, seed, t)
     cands = kg.CandidateSet(c.ids, c.new_counts, c.old_counts)
     out = {}
-    for mode in ("0", "1", "noswap", "mixed", "staged"):
+    for mode in ("0", "1", "noswap", "mixed", "staged", "tc"):
         # "1": the default (warp-per-node kernel); "mixed": nodes with more
         # than 16 new candidates through the opt-in staged kernel (CTA per
         # node, rows in shared memory) where it fits, the rest through the
@@ -44,10 +45,13 @@ def test_u8_step_equals_fp32_kernel_and_oracle(gpu, restated, monkeypatch, kind,
         monkeypatch.setenv("KNNG_U8_HEAVY", "0" if mode == "staged" else "16")
         # "noswap": nodes with nn <= 8 keep the 16 (new) x 8 tile shape
         monkeypatch.setenv("KNNG_U8_SWAP", "0" if mode == "noswap" else "1")
+        # "tc": the tcgen05 kernel (join_u8_tc.cu) where its shapes are
+        # supported (Kl = 128: C2, U8_1000), the warp kernel otherwise
+        monkeypatch.setenv("KNNG_U8_TC", "1" if mode == "tc" else "0")
         out[mode] = kg.compute_step(data, gi.ids, gi.dists, gi.flags, cands)
     g8 = out["1"][0]
     assert out["1"][3] == ev_ref
-    for mode in ("noswap", "mixed", "staged"):
+    for mode in ("noswap", "mixed", "staged", "tc"):
         assert out[mode][3] == ev_ref
         st3 = compare_step(gi, out[mode][0], g8)
         assert st3["mismatch"] == 0 and st3["bit_exact"] == st3["common"], (mode, st3)
