@@ -166,8 +166,8 @@ def u8_roofline(mets, n, d, k, imma_tops, fp32_tflops, config):
     F = Q = t = t_star = t_int = t_hbm = E = 0.0
     launches = 0
     for m in mets:
-        for it in m.iterations[1:]:
-            if it.join_ms <= 0:
+        for it in m.iterations:
+            if it.iteration == 0 or it.join_ms <= 0:
                 continue
             f = it.dist_evals * 2.0 * d
             q = it.join_candidates * (8 * kl + 32 + 8) + 12.0 * n * k
@@ -245,8 +245,8 @@ def join_roofline(mets, n, d, k, peak_tflops, config):
     F = Q = t = t_star = t_fp = t_hbm = 0.0
     launches = 0
     for m in mets:
-        for it in m.iterations[1:]:
-            if it.join_ms <= 0:
+        for it in m.iterations:
+            if it.iteration == 0 or it.join_ms <= 0:
                 continue
             f = it.dist_evals * (3 * d - 1)
             q = it.join_candidates * (4 * stride + 8) + 12 * n * k
@@ -374,11 +374,15 @@ def run_sharded_bench(args, rank, world, local):
     n, d = data.shape
     k, cap = cfg.k, cfg.cap
     params = kg.RunParams(k=k, max_candidates=cap, termination_delta=cfg.delta, seed=cfg.seed,
-                          device=local)
+                          device=local, profile=True)
     d_data = torch.from_numpy(data).to(f"cuda:{local}")
     eng = GpuShardEngine(d_data, params, rank, world)
+    peak = ffma_peak_tflops(local)
+    u8 = byte_valued(data)
+    ipeak = imma_peak_tops(local) if u8 else None
     for _ in range(args.warmup):
         run_sharded(eng, params)
+    rows_before = len(eng.metrics().iterations)
     torch.cuda.synchronize()
     dist.barrier()
     clocks = Clocks(local)
@@ -393,6 +397,14 @@ def run_sharded_bench(args, rank, world, local):
     dist.barrier()
     clk = clocks.stop()
     ms = e0.elapsed_time(e1)
+    # this rank's join-kernel roofline over the timed builds (its own share of
+    # evaluations, candidates and owned rows)
+    shard_m = eng.metrics()
+    shard_m.iterations = shard_m.iterations[rows_before:]
+    owned = eng.hi - eng.lo
+    roof = (u8_roofline([shard_m], owned, d, k, ipeak, peak, args.config) if u8 else
+            join_roofline([shard_m], owned, d, k, peak, args.config))
+    roof["scope"] = f"rank {rank} of {world}: its join launches and its share of the work"
     evals = sum(r.metrics.total_dist_evals for r in results)  # already summed over ranks
     iters = sum(len(r.metrics.iterations) - 1 for r in results)
     sent = sum(r.bytes_exchanged for r in results)
@@ -451,7 +463,7 @@ def run_sharded_bench(args, rank, world, local):
             # count / scan / bounds / write, received count / scan / scatter /
             # merge
             "gpu_launches": int(2 * args.steps + 21 * iters),
-            "roofline": None,
+            "roofline": roof,
             "cpu_baseline": None,
             "clocks": clk,
         }

@@ -289,6 +289,10 @@ int knng_cuda_shard_merge(knng_cuda_shard* shard, const uint32_t* d_records, uin
                           uint64_t* changes);
 /* owned rows, sorted by (distance, id): (hi - lo) x k ids and distances. */
 int knng_cuda_shard_export(knng_cuda_shard* shard, uint32_t* d_ids, float* d_dists);
+/* This shard's share so far: per-kernel device times (params.profile at
+ * creation) and one row per iteration (its evaluations, candidates, inserts
+ * into owned rows and join-kernel time). */
+int knng_cuda_shard_metrics(knng_cuda_shard* shard, knng_cuda_metrics* out);
 
 /* knng::run (descent.hpp:193-255) over num_gpus shards in ONE process, shard r
  * on device devices[r] (NULL: r % device count; several shards may share a

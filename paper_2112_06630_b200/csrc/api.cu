@@ -1299,6 +1299,8 @@ struct knng_cuda_shard {
     uint64_t* h_pin = nullptr;
     uint32_t* h_ocnt = nullptr;
     IterCounters last{};  // counters of the last finished phase
+    IterCounters joined{};  // this iteration's join counters (evaluations, candidates)
+    std::vector<knng_cuda_iteration> rows;  // per iteration: this shard's share
     ~knng_cuda_shard() {
         delete timer;
         delete e;
@@ -1309,6 +1311,7 @@ struct knng_cuda_shard {
     // ---- degree
     void enq_degree() {
         ++e->iteration;
+        timer->tag = e->iteration;
         CK(cudaMemsetAsync(e->ctr.p, 0, sizeof(IterCounters), s));
         launch_indegree_owned(e->gv(), e->indeg.p, s);
         CK(cudaGetLastError());
@@ -1355,6 +1358,7 @@ struct knng_cuda_shard {
             e->read_counters();
         }
         last = *e->h_ctr;
+        joined = last;
         // records for targets owned elsewhere: count pass, offsets, bounds
         const GraphView g = e->gv();
         const int h = timer->begin(KNNG_CUDA_KERNEL_MERGE);
@@ -1405,6 +1409,8 @@ struct knng_cuda_shard {
         e->d2h += sizeof(IterCounters);
         last = *e->h_ctr;
         timer->flush();
+        rows.push_back(knng_cuda_iteration{e->iteration, 0.0, joined.evals, last.changes,
+                                           joined.cands, timer->join_ms_of(e->iteration)});
     }
     void shard_bounds(cudaStream_t st);
 };
@@ -1599,6 +1605,28 @@ int knng_cuda_shard_merge(knng_cuda_shard* sh, const uint32_t* d_records, uint64
         sh->enq_merge(d_records, count);
         sh->fin_merge();
         *changes = sh->last.changes;  // local + received merges of this iteration
+    });
+}
+
+int knng_cuda_shard_metrics(knng_cuda_shard* sh, knng_cuda_metrics* out) {
+    return guarded([&] {
+        if (!sh || !out) raise(KNNG_CUDA_INVALID_ARGUMENT, "null argument");
+        DeviceGuard dg(sh->device);
+        CK(cudaStreamSynchronize(sh->s));
+        sh->timer->flush();
+        metrics_reset(out);
+        for (int kk = 0; kk < KNNG_CUDA_KERNEL_COUNT; ++kk) {
+            out->kernel_ms[kk] = sh->kmetrics.kernel_ms[kk];
+            out->kernel_launches[kk] = sh->kmetrics.kernel_launches[kk];
+        }
+        for (const knng_cuda_iteration& r : sh->rows) {
+            if (out->iterations && out->n_rows < out->capacity) out->iterations[out->n_rows] = r;
+            ++out->n_rows;
+            out->total_dist_evals += r.dist_evals;
+            out->total_changes += r.changes;
+            out->join_candidates += r.join_candidates;
+            out->join_evals += r.dist_evals;
+        }
     });
 }
 

@@ -136,6 +136,14 @@ class GpuShardEngine:
     def sync(self) -> None:
         self.torch.cuda.current_stream(self.device).synchronize()
 
+    def metrics(self, capacity: int = 256) -> RunMetrics:
+        """This shard's share: per-kernel times and one row per iteration
+        (evaluations, candidates, inserts into owned rows, join-kernel ms)."""
+        from .knng import _metrics
+        m, rows = _metrics(capacity)
+        check(N.lib().knng_cuda_shard_metrics(self._h, C.byref(m)))
+        return RunMetrics._from_c(m, rows)
+
     def export(self):
         rows = self.hi - self.lo
         ids = self.torch.empty((rows, self.k), dtype=self.torch.int32, device=self.device)
