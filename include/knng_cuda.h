@@ -55,6 +55,16 @@ extern "C" {
 /* knng::RunParams (descent.hpp:18-36).  strategy is always turbo and the
  * join always blocked (the reference defaults); naive/fused/flat are the
  * reference's benchmark baselines and are not part of this path. */
+/* Per-iteration observer: knng::IterationObserver (descent.hpp:184, called at
+ * :241) sees the graph after each iteration in the run's current internal
+ * labeling (permuted ids after a reorder).  Called on the calling thread with
+ * HOST arrays of n * k ids, squared distances and is_new flags, rows sorted by
+ * (distance, id); setting it makes the run read the graph back every
+ * iteration. */
+typedef void (*knng_cuda_observer_fn)(uint32_t iteration, uint32_t n, uint32_t k,
+                                      const uint32_t* ids, const float* dists,
+                                      const uint8_t* flags, void* user);
+
 typedef struct knng_cuda_params {
     uint32_t k;                        /* default 20 */
     uint32_t max_candidates;           /* default 50 (selection.hpp:15) */
@@ -67,6 +77,8 @@ typedef struct knng_cuda_params {
     int32_t profile;                   /* 1: time each kernel with CUDA events */
     int32_t deterministic;             /* 1: seed-deterministic build (order-independent
                                           sampling and merges; default 0) */
+    knng_cuda_observer_fn observer;    /* NULL (default): none */
+    void* observer_user;               /* passed back to observer */
 } knng_cuda_params;
 
 /* knng::IterationMetrics (descent.hpp:38-43).  `changes` counts successful

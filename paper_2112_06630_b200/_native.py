@@ -82,7 +82,14 @@ class Params(C.Structure):
         ("device", C.c_int32),
         ("profile", C.c_int32),
         ("deterministic", C.c_int32),
+        ("observer", C.c_void_p),
+        ("observer_user", C.c_void_p),
     ]
+
+
+# knng_cuda_observer_fn
+OBSERVER = C.CFUNCTYPE(None, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(C.c_uint32),
+                       C.POINTER(C.c_float), C.POINTER(C.c_uint8), C.c_void_p)
 
 
 class Iteration(C.Structure):

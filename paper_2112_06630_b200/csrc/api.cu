@@ -718,7 +718,36 @@ void run_engine(Engine& e, const float* data, bool data_on_device, const knng_cu
     const double frac = fv ? atof(fv) : 0.05;
     const double recount_above = (iv && iv[0] == '0') ? -1.0 : frac * double(e.n) * double(e.k);
     const char* bv = getenv("KNNG_ITER_BATCH");
-    const uint32_t batch = bv && atoi(bv) > 0 ? uint32_t(atoi(bv)) : 4u;
+    // an observer sees every iteration's graph: one iteration per round trip
+    const uint32_t batch = p.observer ? 1u : bv && atoi(bv) > 0 ? uint32_t(atoi(bv)) : 4u;
+    DevBuf<uint32_t> obs_ids;
+    DevBuf<float> obs_dists;
+    DevBuf<uint8_t> obs_flags;
+    std::vector<uint32_t> h_obs_ids;
+    std::vector<float> h_obs_dists;
+    std::vector<uint8_t> h_obs_flags;
+    auto observe = [&](uint32_t j) {
+        if (!p.observer) return;
+        const size_t nk = size_t(e.n) * e.k;
+        if (!obs_ids.p) {
+            obs_ids.alloc(nk, e.pool, e.s);
+            obs_dists.alloc(nk, e.pool, e.s);
+            obs_flags.alloc(nk, e.pool, e.s);
+            h_obs_ids.resize(nk);
+            h_obs_dists.resize(nk);
+            h_obs_flags.resize(nk);
+        }
+        e.export_rows(obs_ids.p, obs_dists.p, obs_flags.p);
+        CK(cudaMemcpyAsync(h_obs_ids.data(), obs_ids.p, sizeof(uint32_t) * nk,
+                           cudaMemcpyDeviceToHost, e.s));
+        CK(cudaMemcpyAsync(h_obs_dists.data(), obs_dists.p, sizeof(float) * nk,
+                           cudaMemcpyDeviceToHost, e.s));
+        CK(cudaMemcpyAsync(h_obs_flags.data(), obs_flags.p, nk, cudaMemcpyDeviceToHost, e.s));
+        CK(cudaStreamSynchronize(e.s));
+        e.d2h += 9 * nk;
+        p.observer(j, e.n, e.k, h_obs_ids.data(), h_obs_dists.data(), h_obs_flags.data(),
+                   p.observer_user);
+    };
     const uint32_t T = p.max_iterations;
     e.ensure_slots(T + 3);
     e.indeg_inc = true;
@@ -808,6 +837,7 @@ void run_engine(Engine& e, const float* data, bool data_on_device, const knng_cu
                     m->iterations[m->n_rows - 1].wall_time_s += now_s() - r0;
                 if (m) m->total_wall_time_s += now_s() - r0;
             }
+            observe(j);  // descent.hpp:241, after the reorder of this iteration
             if (double(c.changes) < threshold) {
                 done = true;
                 break;
@@ -884,6 +914,8 @@ void knng_cuda_params_default(knng_cuda_params* p) {
     p->device = 0;
     p->profile = 0;
     p->deterministic = 0;
+    p->observer = nullptr;
+    p->observer_user = nullptr;
 }
 
 const char* knng_cuda_last_error(void) { return g_err.c_str(); }

@@ -203,8 +203,12 @@ def _as_data(data) -> np.ndarray:
     return data
 
 
-def run(data, params: RunParams = RunParams()) -> RunResult:
-    """knng::run (descent.hpp:193-255) on the GPU; host arrays in and out."""
+def run(data, params: RunParams = RunParams(), observer=None) -> RunResult:
+    """knng::run (descent.hpp:193-255) on the GPU; host arrays in and out.
+
+    observer(iteration, KnnGraph): the reference's IterationObserver
+    (descent.hpp:184, called at :241), after each iteration in the run's
+    current labeling (permuted ids after a reorder)."""
     data = _as_data(data)
     params.validate()
     n, d = data.shape
@@ -217,9 +221,20 @@ def run(data, params: RunParams = RunParams()) -> RunResult:
     sigma = np.zeros(n, np.uint32) if params.reorder else None
     m, rows = _metrics(params.max_iterations + 1)
     p = params._c()
+    cb = None
+    if observer is not None:
+        def _obs(it, nn, kk, pi, pd, pf, _user):
+            cnt = nn * kk
+            g = KnnGraph(np.ctypeslib.as_array(pi, (cnt,)).reshape(nn, kk).copy(),
+                         np.ctypeslib.as_array(pd, (cnt,)).reshape(nn, kk).copy(),
+                         np.ctypeslib.as_array(pf, (cnt,)).reshape(nn, kk).copy())
+            observer(int(it), g)
+        cb = N.OBSERVER(_obs)
+        p.observer = C.cast(cb, C.c_void_p)
     check(N.lib().knng_cuda_run(data.ctypes.data, n, d, C.byref(p), ids.ctypes.data,
                                 dists.ctypes.data, flags.ctypes.data,
                                 sigma.ctypes.data if sigma is not None else None, C.byref(m)))
+    del cb
     return RunResult(KnnGraph(ids, dists, flags), RunMetrics._from_c(m, rows), sigma)
 
 

@@ -46,8 +46,8 @@ inline std::vector<float> unpadded(const Dataset& data) {
 
 // knng::run on the GPU.  RunParams::strategy must be turbo and
 // blocked_compute true (the reference defaults; naive/fused/flat are its
-// benchmark baselines).  The per-iteration observer is not supported (the
-// graph stays on the device between iterations).  The returned graph is in
+// benchmark baselines).  An observer makes the run read the graph back after
+// every iteration (it stays on the device otherwise).  The returned graph is in
 // original ids; its heap rows are rebuilt with KnnGraph::from_rows.
 inline RunResult run(const Dataset& data, const RunParams& params,
                      const IterationObserver& observer = {}, int device = 0) {
@@ -56,8 +56,6 @@ inline RunResult run(const Dataset& data, const RunParams& params,
     if (params.strategy != SelectionStrategy::turbo || !params.blocked_compute)
         throw std::invalid_argument("knng::cuda::run: the GPU path implements turbo selection "
                                     "with the blocked join");
-    if (observer)
-        throw std::invalid_argument("knng::cuda::run: iteration observers are not supported");
 
     knng_cuda_params p;
     knng_cuda_params_default(&p);
@@ -69,6 +67,26 @@ inline RunResult run(const Dataset& data, const RunParams& params,
     p.reorder_after_iteration = params.reorder_after_iteration;
     p.seed = params.seed;
     p.device = device;
+    // the observer sees a KnnGraph rebuilt from the device rows after every
+    // iteration (descent.hpp:241), in the run's current labeling
+    struct ObserverCtx {
+        const IterationObserver* fn;
+    } octx{&observer};
+    if (observer) {
+        p.observer = [](std::uint32_t it, std::uint32_t n_, std::uint32_t k_,
+                        const std::uint32_t* ids_, const float* dists_, const std::uint8_t* fl_,
+                        void* user) {
+            std::vector<std::vector<NeighborEntry>> rows(n_, std::vector<NeighborEntry>(k_));
+            for (std::uint32_t u = 0; u < n_; ++u)
+                for (std::uint32_t i = 0; i < k_; ++i) {
+                    const std::size_t q = std::size_t(u) * k_ + i;
+                    rows[u][i] = NeighborEntry{ids_[q], dists_[q], fl_[q] != 0};
+                }
+            const KnnGraph g = KnnGraph::from_rows(k_, rows);
+            (*static_cast<ObserverCtx*>(user)->fn)(it, g);
+        };
+        p.observer_user = &octx;
+    }
 
     const std::uint32_t n = data.n(), k = params.k;
     const std::vector<float> rows = detail::unpadded(data);

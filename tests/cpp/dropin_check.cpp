@@ -26,14 +26,26 @@ int main() {
     params.k = 20;
     params.seed = 13;
     try {
-        const RunResult gpu = cuda::run(data, params);
-        const RunResult cpu = run(data, params);
+        // the reference's IterationObserver (descent.hpp:184,241): one call per
+        // iteration, in order, with the graph as it stands after it
+        std::uint32_t calls = 0, last_it = 0;
+        double last_recall = -1.0;
         const ExactGraph exact = brute_force_knng(data, 20);
+        const RunResult gpu = cuda::run(data, params, [&](std::uint32_t it, const KnnGraph& g) {
+            ++calls;
+            last_it = it;
+            last_recall = recall(g, exact);
+        });
+        const RunResult cpu = run(data, params);
         const double rg = recall(gpu.graph, exact), rc = recall(cpu.graph, exact);
-        std::printf("dropin %s recall gpu %.4f cpu %.4f iterations gpu %zu cpu %zu\n",
-                    rg >= rc - 0.005 ? "OK" : "FAIL", rg, rc, gpu.metrics.iterations.size() - 1,
-                    cpu.metrics.iterations.size() - 1);
-        return rg >= rc - 0.005 ? 0 : 1;
+        const bool obs_ok = calls == gpu.metrics.iterations.size() - 1 &&
+                            last_it == calls && last_recall == rg;
+        const bool ok = rg >= rc - 0.005 && obs_ok;
+        std::printf("dropin %s recall gpu %.4f cpu %.4f iterations gpu %zu cpu %zu observer "
+                    "calls %u last recall %.4f\n",
+                    ok ? "OK" : "FAIL", rg, rc, gpu.metrics.iterations.size() - 1,
+                    cpu.metrics.iterations.size() - 1, calls, last_recall);
+        return ok ? 0 : 1;
     } catch (const std::runtime_error& e) {
         std::printf("dropin NODEVICE %s\n", e.what());
         return 3;

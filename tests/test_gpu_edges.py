@@ -78,3 +78,30 @@ def test_all_points_equal(gpu):
     res = kg.run(data, kg.RunParams(k=6, max_candidates=12))
     _rows_valid(res.graph.ids, res.graph.dists, 500, 6)
     assert np.all(res.graph.dists == 0)
+
+
+def test_iteration_observer(gpu):
+    """The reference's IterationObserver (descent.hpp:184, called at :241):
+    one call per iteration, in order, each with a sorted graph; without a
+    reorder the last one is the returned graph."""
+    import paper_2112_06630_b200 as kg
+    data = np.random.default_rng(5).standard_normal((3000, 16)).astype(np.float32)
+    seen = []
+
+    def obs(it, g):
+        assert np.all(np.diff(g.dists, axis=1) >= 0)
+        seen.append((it, g.ids.copy(), g.dists.copy()))
+
+    res = kg.run(data, kg.RunParams(k=10, max_candidates=20, seed=3), observer=obs)
+    iters = len(res.metrics.iterations) - 1
+    assert [s[0] for s in seen] == list(range(1, iters + 1))
+    assert np.array_equal(seen[-1][1], res.graph.ids)
+    assert np.array_equal(seen[-1][2].view(np.uint32), res.graph.dists.view(np.uint32))
+    # with a reorder the observer sees the permuted labeling from that
+    # iteration on; the returned graph is in original ids
+    seen.clear()
+    res2 = kg.run(data, kg.RunParams(k=10, max_candidates=20, seed=3, reorder=True,
+                                     reorder_after_iteration=1), observer=obs)
+    assert len(seen) == len(res2.metrics.iterations) - 1
+    sig = res2.permutation
+    assert np.array_equal(np.sort(seen[-1][1][sig], axis=1), np.sort(sig[res2.graph.ids], axis=1))
