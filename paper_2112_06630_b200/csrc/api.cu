@@ -597,13 +597,26 @@ struct Engine {
 
     // sigma from the current graph, rows gathered, graph relabelled
     void reorder() {
-        sigma.alloc(n, pool, s);
-        sigma_inv.alloc(n, pool, s);
+        compute_sigma();
+        apply_sigma();
+    }
+    void compute_sigma() {
+        if (!sigma.p) {
+            sigma.alloc(n, pool, s);
+            sigma_inv.alloc(n, pool, s);
+        }
         const size_t scratch_bytes = locality_permutation_scratch(n);
         DevBuf<unsigned char> scratch;
         scratch.alloc(scratch_bytes, pool, s);
-        launch_locality_permutation(gv(), sigma.p, sigma_inv.p, scratch.p, scratch_bytes, s);
+        GraphView g = gv();
+        g.lo = 0;
+        g.hi = n;
+        launch_locality_permutation(g, sigma.p, sigma_inv.p, scratch.p, scratch_bytes, s);
         CK(cudaGetLastError());
+    }
+    // the data rows and every graph row (ids renamed) into the order sigma
+    // (sigma / sigma_inv already in place)
+    void apply_sigma() {
         DevBuf<float> data2;
         data2.alloc(size_t(n) * stride, pool, s);
         launch_permute_rows(data.p, data2.p, sigma.p, n, stride, s);
@@ -612,6 +625,15 @@ struct Engine {
         dl_valid = false;
         if (u8_state == 1) u8_state = -1;  // repack in the new row order
         remap_graph(sigma.p);
+    }
+    // remap_graph over every row, whatever the owned range (multi-GPU)
+    void remap_all(const uint32_t* perm) {
+        const uint32_t lo0 = lo, hi0 = hi;
+        lo = 0;
+        hi = n;
+        remap_graph(perm);
+        lo = lo0;
+        hi = hi0;
     }
 
     void export_rows(uint32_t* ids, float* dists, uint8_t* fl) {
@@ -1462,12 +1484,14 @@ constexpr uint32_t kMaxShards = 1023;
 
 knng_cuda_shard* shard_new(const float* data, bool data_on_device, uint32_t n, uint32_t d,
                            const knng_cuda_params& p, uint32_t rank, uint32_t nranks,
-                           cudaStream_t stream) {
+                           cudaStream_t stream, bool allow_reorder = false) {
     if (nranks == 0 || rank >= nranks) raise(KNNG_CUDA_INVALID_ARGUMENT, "bad rank / nranks");
     if (nranks > kMaxShards)
         raise(KNNG_CUDA_INVALID_ARGUMENT, "this build supports at most 1023 shards");
     validate_params(n, d, p);
-    if (p.reorder) raise(KNNG_CUDA_NOT_IMPLEMENTED, "reorder is not supported on the sharded path");
+    if (p.reorder && !allow_reorder)
+        raise(KNNG_CUDA_NOT_IMPLEMENTED,
+              "reorder on shards is supported by knng_cuda_run_multi, not by the phase API");
     if (p.deterministic)
         raise(KNNG_CUDA_NOT_IMPLEMENTED, "deterministic mode is not supported on the sharded path");
     auto* sh = new knng_cuda_shard();
@@ -1721,6 +1745,30 @@ struct MultiRun {
                 if (q != r) CK(cudaStreamWaitEvent(sh[r]->s, ev[q], 0));
         }
     }
+    // the owned graph rows (keys, flags, maxd) of every shard into shard
+    // `only` (or every shard when only == ~0)
+    void gather_rows(uint32_t only = ~0u) {
+        barrier();
+        const uint32_t k = sh[0]->e->k;
+        for (uint32_t r = 0; r < P; ++r) {
+            if (only != ~0u && r != only) continue;
+            CK(cudaSetDevice(dev[r]));
+            Engine& er = *sh[r]->e;
+            for (uint32_t q = 0; q < P; ++q) {
+                if (q == r) continue;
+                const Engine& eq = *sh[q]->e;
+                const uint32_t lo = eq.lo, hi = eq.hi;
+                if (hi <= lo) continue;
+                CK(cudaMemcpyPeerAsync(er.keys.p + size_t(lo) * k, dev[r], eq.keys.p + size_t(lo) * k,
+                                       dev[q], sizeof(uint64_t) * size_t(hi - lo) * k, sh[r]->s));
+                CK(cudaMemcpyPeerAsync(er.flags.p + lo, dev[r], eq.flags.p + lo, dev[q],
+                                       sizeof(uint32_t) * (hi - lo), sh[r]->s));
+                CK(cudaMemcpyPeerAsync(er.maxd.p + lo, dev[r], eq.maxd.p + lo, dev[q],
+                                       sizeof(float) * (hi - lo), sh[r]->s));
+            }
+        }
+        barrier();
+    }
     // the owned maxd slice of every shard into every other shard
     void allgather_maxd() {
         barrier();
@@ -1800,7 +1848,7 @@ void run_multi(const float* data, uint32_t n, uint32_t d, const knng_cuda_params
         CK(cudaSetDevice(R.dev[r]));
         knng_cuda_params pr = p;
         pr.device = R.dev[r];
-        R.sh[r] = shard_new(data, false, n, d, pr, r, P, nullptr);
+        R.sh[r] = shard_new(data, false, n, d, pr, r, P, nullptr, true);
         CK(cudaEventCreateWithFlags(&R.ev[r], cudaEventDisableTiming));
         R.ipart[r].alloc(size_t(P) * n, R.sh[r]->e->pool, R.sh[r]->s);
     }
@@ -1823,6 +1871,7 @@ void run_multi(const float* data, uint32_t n, uint32_t d, const knng_cuda_params
     metrics_push(m, 0, t1 - t_start, uint64_t(n) * p.k, 0);
     const double threshold = p.termination_delta * double(n) * double(p.k);
     std::vector<uint64_t> counts(size_t(P) * P);
+    bool reordered = false;
     std::vector<uint64_t> seeds(p.max_iterations + 1);
     for (uint32_t i = 1; i <= p.max_iterations; ++i) seeds[i] = master();  // reference order
     for (uint32_t it = 1; it <= p.max_iterations; ++it) {
@@ -1919,6 +1968,43 @@ void run_multi(const float* data, uint32_t n, uint32_t d, const knng_cuda_params
             changes += R.sh[r]->last.changes;
         }
         R.allgather_maxd();
+        // the locality reorder (descent.hpp:230-235): sigma from the whole
+        // graph on shard 0, the data and the graph of every shard permuted;
+        // the shards then own contiguous ranges of sigma, so graph
+        // neighbours mostly share a shard
+        if (p.reorder && !reordered && it == p.reorder_after_iteration) {
+            R.gather_rows();
+            CK(cudaSetDevice(R.dev[0]));
+            R.sh[0]->e->compute_sigma();
+            R.barrier();
+            for (uint32_t r = 0; r < P; ++r) {
+                CK(cudaSetDevice(R.dev[r]));
+                Engine& er = *R.sh[r]->e;
+                if (r && !er.sigma.p) {
+                    er.sigma.alloc(n, er.pool, er.s);
+                    er.sigma_inv.alloc(n, er.pool, er.s);
+                }
+                if (r) {
+                    CK(cudaMemcpyPeerAsync(er.sigma.p, R.dev[r], R.sh[0]->e->sigma.p, R.dev[0],
+                                           sizeof(uint32_t) * n, R.sh[r]->s));
+                    CK(cudaMemcpyPeerAsync(er.sigma_inv.p, R.dev[r], R.sh[0]->e->sigma_inv.p,
+                                           R.dev[0], sizeof(uint32_t) * n, R.sh[r]->s));
+                }
+            }
+            R.barrier();
+            for (uint32_t r = 0; r < P; ++r) {
+                CK(cudaSetDevice(R.dev[r]));
+                Engine& er = *R.sh[r]->e;
+                const uint32_t lo0 = er.lo, hi0 = er.hi;
+                er.lo = 0;
+                er.hi = n;
+                er.apply_sigma();  // data rows and every graph row
+                er.lo = lo0;
+                er.hi = hi0;
+            }
+            R.barrier();
+            reordered = true;
+        }
         const double wall = now_s() - t0;
         metrics_push(m, it, wall, evals, changes, cands, 0.0);
         if (m) {
@@ -1927,8 +2013,25 @@ void run_multi(const float* data, uint32_t n, uint32_t d, const knng_cuda_params
         }
         if (double(changes) < threshold) break;
     }
+    if (reordered) {
+        // back to the caller's ids (descent.hpp:245): every row on shard 0,
+        // relabelled by sigma_inv, exported from there
+        R.gather_rows(0);
+        CK(cudaSetDevice(R.dev[0]));
+        Engine& e0 = *R.sh[0]->e;
+        e0.remap_all(e0.sigma_inv.p);
+        const size_t cnt = size_t(n) * p.k;
+        DevBuf<uint32_t> ids;
+        DevBuf<float> dd;
+        ids.alloc(cnt, e0.pool, e0.s);
+        dd.alloc(cnt, e0.pool, e0.s);
+        e0.export_rows(ids.p, dd.p, nullptr);
+        CK(cudaMemcpyAsync(out_ids, ids.p, sizeof(uint32_t) * cnt, cudaMemcpyDeviceToHost, e0.s));
+        CK(cudaMemcpyAsync(out_dists, dd.p, sizeof(float) * cnt, cudaMemcpyDeviceToHost, e0.s));
+        CK(cudaStreamSynchronize(e0.s));
+    }
     // owned rows -> host
-    for (uint32_t r = 0; r < P; ++r) {
+    for (uint32_t r = 0; r < P && !reordered; ++r) {
         CK(cudaSetDevice(R.dev[r]));
         knng_cuda_shard* s = R.sh[r];
         const uint32_t lo = s->e->lo, hi = s->e->hi;

@@ -94,10 +94,15 @@ constexpr int kMaxDevices = 64;
 // A failed CUDA call inside a launch wrapper surfaces at once, as an exception
 // the C-ABI guard (api.cu) turns into KNNG_CUDA_CUDA_ERROR with this message,
 // instead of later under an unrelated call.
-inline void check_launch(cudaError_t e, const char* what = "CUDA call in a launch wrapper") {
+inline void check_launch(cudaError_t e, const char* what = "CUDA call in a launch wrapper",
+                         const char* file = __builtin_FILE(), int line = __builtin_LINE()) {
     if (e != cudaSuccess) {
         cudaGetLastError();
-        throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+        const char* base = file;
+        for (const char* q = file; *q; ++q)
+            if (*q == '/') base = q + 1;
+        throw std::runtime_error(std::string(what) + " (" + base + ":" + std::to_string(line) +
+                                 "): " + cudaGetErrorString(e));
     }
 }
 inline int current_device() {

@@ -156,7 +156,10 @@ size_t locality_permutation_scratch(uint32_t n) {
     cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, (const uint32_t*)nullptr,
                                     (uint32_t*)nullptr, (const uint32_t*)nullptr,
                                     (uint32_t*)nullptr, int(n));
-    return size_t(n) * 4 * (6 + kMaxRounds) + size_t(n) * 8 + 256 + cub_bytes + 1024;
+    // the same 256-byte rounding as launch_locality_permutation's carving
+    auto r256 = [](size_t b) { return (b + 255) & ~size_t(255); };
+    return 6 * r256(size_t(n) * 4) + r256(size_t(n) * 4 * kMaxRounds) + r256(size_t(n) * 8) + 256 +
+           cub_bytes + 1024;
 }
 
 void launch_locality_permutation(const GraphView& g, uint32_t* sigma, uint32_t* sigma_inv,

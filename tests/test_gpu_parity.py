@@ -438,3 +438,14 @@ def test_hub_target_merge_matches_oracle(gpu, restated):
     st = compare_step(g0, go, g, restated=restated, data=data)
     assert st["mismatch"] == 0 and st["flag_mismatch"] == 0, st
     assert st["bit_exact"] + st["other_path"] == st["common"], st
+
+
+@pytest.mark.parametrize("n", [10000, 12345, 4099])
+def test_locality_permutation_scratch_sizes(gpu, n):
+    """The permutation's scratch carving rounds every array to 256 bytes; the
+    scratch size must include that rounding for every n (n = 10000 once left
+    the radix sort's temporary storage short)."""
+    data = np.random.default_rng(n).standard_normal((n, 8)).astype(np.float32)
+    res = kg.run(data, kg.RunParams(k=10, max_candidates=20, seed=1, reorder=True,
+                                    reorder_after_iteration=1, max_iterations=3))
+    assert np.array_equal(np.sort(res.permutation), np.arange(n))

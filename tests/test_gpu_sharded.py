@@ -207,3 +207,30 @@ def test_nndescent_l2_num_gpus(gpu):
     ex, _ = kg.brute_force_knng(data, 20)
     single = kg.run(data, kg.RunParams(k=20, max_candidates=20, seed=0))
     assert abs(kg.recall(ids, ex) - kg.recall(single.graph.ids, ex)) <= 0.005
+
+
+@pytest.mark.parametrize("kind,n,shards", [("C1", None, 2), ("C4", 20000, 4), ("C3", 20000, 3)])
+def test_run_multi_reorder(gpu, kind, n, shards):
+    """The locality reorder on shards (descent.hpp:230-235, 245): sigma from
+    the whole graph, every shard's data and graph permuted, the shards then
+    owning contiguous ranges of sigma; the returned graph is in the caller's
+    ids.  Recall within 0.01 of the build without reorder
+    (test_descent.cpp:211-224) and within 0.5 pp of the single-GPU reordered
+    build."""
+    cfg = datasets.CONFIGS[kind]
+    data = datasets.generate(cfg) if n is None else datasets.generate(cfg, n=n)
+    base = kg.RunParams(k=cfg.k, max_candidates=cfg.cap, seed=0)
+    reo = kg.RunParams(k=cfg.k, max_candidates=cfg.cap, seed=0, reorder=True,
+                       reorder_after_iteration=1)
+    ids, dists, m = kg.run_multi(data, reo, num_gpus=shards)
+    ex, _ = kg.brute_force_knng(data, cfg.k)
+    r_multi = kg.recall(ids, ex)
+    r_plain = kg.recall(kg.run(data, base).graph.ids, ex)
+    r_single_reo = kg.recall(kg.run(data, reo).graph.ids, ex)
+    assert r_multi >= r_plain - 0.01, (r_multi, r_plain)
+    assert abs(r_multi - r_single_reo) <= 0.005, (r_multi, r_single_reo)
+    assert np.all(np.diff(dists, axis=1) >= 0)
+    assert not np.any(ids == np.arange(data.shape[0])[:, None])
+    i = np.arange(0, data.shape[0], 101)
+    d64 = ((data[i, None, :].astype(np.float64) - data[ids[i]].astype(np.float64)) ** 2).sum(-1)
+    assert np.allclose(dists[i], d64, rtol=1e-4, atol=1e-4)
