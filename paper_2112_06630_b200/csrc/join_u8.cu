@@ -64,14 +64,31 @@ __device__ __forceinline__ size_t u8_prow(uint32_t r, uint32_t nn, uint32_t m) {
 // not depend on the order of terms (u8_pack_kernel writes it).
 
 // All coordinates integral in [0, 255]?  flag starts at 1; any miss clears it.
+// Grid-stride in chunks of 32 elements per thread; every warp re-reads the
+// flag between chunks and stops once any warp has cleared it, so float data
+// (the usual case: C1 / C3 / C4 / C5) is rejected after the first chunk
+// instead of after a full pass over the data (C5: 2.9 -> ~0.01 ms).
 __global__ void u8_check_kernel(const float* __restrict__ data, size_t count, uint32_t* flag) {
-    bool ok = true;
-    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
-         i += size_t(gridDim.x) * blockDim.x) {
-        const float x = data[i];
-        ok &= x >= 0.0f && x <= 255.0f && x == rintf(x);
+    constexpr uint32_t kPer = 32;
+    const size_t span = size_t(gridDim.x) * blockDim.x;
+    const size_t t = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const size_t lane0 = t - (threadIdx.x & 31u);  // warp-uniform loop bound
+    for (size_t w0 = lane0, base = t; w0 < count; w0 += span * kPer, base += span * kPer) {
+        bool ok = true;
+#pragma unroll 4
+        for (uint32_t j = 0; j < kPer; ++j) {
+            const size_t i = base + size_t(j) * span;
+            if (i < count) {
+                const float x = data[i];
+                ok &= x >= 0.0f && x <= 255.0f && x == rintf(x);
+            }
+        }
+        if (!__all_sync(0xffffffffu, ok)) {
+            if ((threadIdx.x & 31u) == 0) atomicAnd(flag, 0u);
+            return;
+        }
+        if (__shfl_sync(0xffffffffu, *(volatile uint32_t*)flag, 0) == 0u) return;
     }
-    if (!__all_sync(0xffffffffu, ok) && (threadIdx.x & 31u) == 0) atomicAnd(flag, 0u);
 }
 
 // Lane-major byte copy and per-lane squared norms (exact integers).  One warp
