@@ -364,11 +364,19 @@ def run_sharded_bench(args, rank, world, local):
 
     import paper_2112_06630_b200 as kg
     from paper_2112_06630_b200.shard import GpuShardEngine, gather_graph, run_sharded
+    # KNNG_DIST_BACKEND=gloo: the collectives through host memory, so several
+    # ranks can share one GPU (a functional check of this path on a one-GPU
+    # box; NCCL, the default, needs a GPU per rank)
+    backend = os.environ.get("KNNG_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if "RANK" not in os.environ:  # --sharded on one GPU without torchrun
         os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1",
                           MASTER_PORT=str(29500 + os.getpid() % 1000))
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group(backend)
     cfg = datasets.CONFIGS[args.config]
     data = datasets.generate(cfg)  # same instance on every rank (replicated data)
     n, d = data.shape
@@ -427,7 +435,8 @@ def run_sharded_bench(args, rank, world, local):
         e2e_evals += r.metrics.total_dist_evals
         e.close()
     e2e_s = time.perf_counter() - t0
-    t = torch.tensor([ms, e2e_s], dtype=torch.float64, device=f"cuda:{local}")
+    t = torch.tensor([ms, e2e_s], dtype=torch.float64,
+                     device=f"cuda:{local}" if backend == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms, e2e_s = float(t[0]), float(t[1])
     out = None

@@ -174,6 +174,46 @@ class ShardedResult:
     bytes_exchanged: int = 0  # records sent by this rank (all iterations)
 
 
+def _staged(t, group=None) -> bool:
+    """Device tensors over a host-only backend (gloo) go through host memory;
+    NCCL takes them in place."""
+    import torch.distributed as dist
+    return t.device.type == "cuda" and dist.get_backend(group) == "gloo"
+
+
+def _all_reduce(t, group=None) -> None:
+    import torch.distributed as dist
+    if _staged(t, group):
+        h = t.cpu()
+        dist.all_reduce(h, group=group)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, group=group)
+
+
+def _all_to_all_single(out, inp, out_splits=None, in_splits=None, group=None) -> None:
+    import torch.distributed as dist
+    if _staged(out, group):
+        h = out.new_empty(out.shape, device="cpu")
+        dist.all_to_all_single(h, inp.cpu(), output_split_sizes=out_splits,
+                               input_split_sizes=in_splits, group=group)
+        out.copy_(h)
+    else:
+        dist.all_to_all_single(out, inp, output_split_sizes=out_splits,
+                               input_split_sizes=in_splits, group=group)
+
+
+def _all_gather(parts, mine, group=None) -> None:
+    import torch.distributed as dist
+    if _staged(mine, group):
+        hp = [p.new_empty(p.shape, device="cpu") for p in parts]
+        dist.all_gather(hp, mine.cpu(), group=group)
+        for p, h in zip(parts, hp):
+            p.copy_(h)
+    else:
+        dist.all_gather(parts, mine, group=group)
+
+
 def _exchange(segs: List, counts: List[int], width: int, dtype, dev, group=None):
     """Variable-size all-to-all of per-destination segments (width words per
     record); returns the concatenated received records."""
@@ -182,13 +222,13 @@ def _exchange(segs: List, counts: List[int], width: int, dtype, dev, group=None)
     P = len(counts)
     send_counts = torch.tensor(counts, dtype=torch.int64, device=dev)
     recv_counts = torch.empty_like(send_counts)
-    dist.all_to_all_single(recv_counts, send_counts, group=group)
+    _all_to_all_single(recv_counts, send_counts, group=group)
     rc = recv_counts.tolist()  # the one host read this exchange needs
     parts = [segs[r] for r in range(P) if counts[r]]
     send = torch.cat(parts) if parts else torch.empty(0, dtype=dtype, device=dev)
     recv = torch.empty(width * int(sum(rc)), dtype=dtype, device=dev)
-    dist.all_to_all_single(recv, send, output_split_sizes=[width * int(c) for c in rc],
-                           input_split_sizes=[width * int(c) for c in counts], group=group)
+    _all_to_all_single(recv, send, [width * int(c) for c in rc],
+                       [width * int(c) for c in counts], group=group)
     return recv
 
 
@@ -196,7 +236,7 @@ def _allgather_maxd(engine, group=None) -> None:
     import torch.distributed as dist
     r, P, chunk = engine.rank, engine.nranks, engine.chunk
     parts = [engine.maxd[i * chunk:(i + 1) * chunk] for i in range(P)]
-    dist.all_gather(parts, parts[r].clone(), group=group)
+    _all_gather(parts, parts[r].clone(), group=group)
 
 
 def run_sharded(engine, params: RunParams, group=None) -> ShardedResult:
@@ -218,7 +258,7 @@ def run_sharded(engine, params: RunParams, group=None) -> ShardedResult:
     sent = 0
     for it in range(1, params.max_iterations + 1):
         t0 = time.perf_counter()
-        dist.all_reduce(engine.degree(), group=group)
+        _all_reduce(engine.degree(), group=group)
         counts, segs = engine.sample(int(seeds[it]))
         recv = _exchange([s for s in segs], counts, 4, torch.int32, dev, group)
         engine.offers(recv)
@@ -232,7 +272,7 @@ def run_sharded(engine, params: RunParams, group=None) -> ShardedResult:
         changes = engine.merge(recv)
         _allgather_maxd(engine, group)
         tot = torch.tensor([changes, st["evals"], st["cands"]], dtype=torch.float64, device=dev)
-        dist.all_reduce(tot, group=group)
+        _all_reduce(tot, group=group)
         changes_all, evals_all, cands_all = (int(x) for x in tot.tolist())
         metrics.iterations.append(IterationMetrics(it, time.perf_counter() - t0, evals_all,
                                                    changes_all, cands_all))
@@ -258,6 +298,6 @@ def gather_graph(res: ShardedResult, n: int, k: int, group=None):
     dd = torch.nn.functional.pad(res.dists, (0, 0, 0, pad)) if pad else res.dists
     outs_i = [torch.empty_like(ids) for _ in range(P)]
     outs_d = [torch.empty_like(dd) for _ in range(P)]
-    dist.all_gather(outs_i, ids.contiguous(), group=group)
-    dist.all_gather(outs_d, dd.contiguous(), group=group)
+    _all_gather(outs_i, ids.contiguous(), group=group)
+    _all_gather(outs_d, dd.contiguous(), group=group)
     return torch.cat(outs_i)[:n], torch.cat(outs_d)[:n]

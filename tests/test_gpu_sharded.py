@@ -234,3 +234,58 @@ def test_run_multi_reorder(gpu, kind, n, shards):
     i = np.arange(0, data.shape[0], 101)
     d64 = ((data[i, None, :].astype(np.float64) - data[ids[i]].astype(np.float64)) ** 2).sum(-1)
     assert np.allclose(dists[i], d64, rtol=1e-4, atol=1e-4)
+
+
+def _mp_worker(rank, world, port, out_path, kind, n):
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    import paper_2112_06630_b200 as kg2
+    from paper_2112_06630_b200 import datasets as ds
+    from paper_2112_06630_b200.shard import GpuShardEngine, gather_graph, run_sharded
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    cfg = ds.CONFIGS[kind]
+    data = ds.generate(cfg, n=n) if kind in ("C3", "C4") else ds.generate(cfg)[:n]
+    params = kg2.RunParams(k=cfg.k, max_candidates=cfg.cap, seed=0)
+    eng = GpuShardEngine(torch.from_numpy(data).cuda(), params, rank, world)
+    res = run_sharded(eng, params)
+    ids, dists = gather_graph(res, data.shape[0], cfg.k)
+    if rank == 0:
+        np.savez(out_path, ids=ids.cpu().numpy().astype(np.uint32), dists=dists.cpu().numpy(),
+                 iters=len(res.metrics.iterations) - 1,
+                 evals=np.array([it.dist_evals for it in res.metrics.iterations]))
+    eng.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("kind,n,world", [("C1", 10000, 2), ("C4", 20000, 3), ("C2", 12000, 2)])
+def test_run_sharded_multiprocess(gpu, kind, n, world):
+    """shard.py's run_sharded in separate processes (the torchrun path of
+    bench.py --gpus N), each rank a real CUDA shard engine; the GPU is shared,
+    so the collectives go over gloo through host memory (NCCL does not
+    allow two ranks on one GPU).  Recall within 0.5 pp of the single-GPU
+    build; the initial graph's evaluations counted once."""
+    import tempfile
+
+    import torch.multiprocessing as mp
+    out = tempfile.mktemp(suffix=".npz")
+    mp.spawn(_mp_worker, args=(world, _port(), out, kind, n), nprocs=world, join=True)
+    r = np.load(out)
+    os.unlink(out)
+    cfg = datasets.CONFIGS[kind]
+    data = datasets.generate(cfg, n=n) if kind in ("C3", "C4") else datasets.generate(cfg)[:n]
+    params = kg.RunParams(k=cfg.k, max_candidates=cfg.cap, seed=0)
+    single = kg.run(data, params)
+    ex, _ = kg.brute_force_knng(data, cfg.k)
+    r_mp, r_single = kg.recall(r["ids"], ex), kg.recall(single.graph.ids, ex)
+    assert abs(r_mp - r_single) <= 0.005, (r_mp, r_single)
+    assert int(r["evals"][0]) == n * cfg.k
+    assert np.all(np.diff(r["dists"], axis=1) >= 0)
