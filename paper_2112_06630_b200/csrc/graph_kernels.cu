@@ -10,6 +10,9 @@
 // All of these are HBM/L2-latency-bound integer work: one warp per node where
 // a node's k-entry row is the unit (k <= 32: lane i owns entry i), one
 // thread per edge where the edge is the unit.
+#include <algorithm>
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace knng_cuda {
@@ -153,6 +156,129 @@ __global__ void __launch_bounds__(256) init_random_kernel(GraphView g, uint32_t 
         const uint32_t src = ((lane - e) & 3u) << 3;
         const float got = __shfl_sync(0xffffffffu, dist, src);
         if (lane >= e && lane < e + 4) mine = got;
+    }
+    uint64_t key = real ? pack_key(mine, id) : kEmptyKey;
+    key = warp_sort_u64(key);
+    if (real) g.keys[size_t(u) * k + lane] = key;
+    const uint64_t last = __shfl_sync(0xffffffffu, key, k - 1);
+    if (lane == 0) {
+        g.flags[u] = full_mask_k(k);
+        g.maxd[u] = key_dist(last);
+    }
+}
+
+// init_random for long rows with the candidate rows bulk-copied into shared
+// memory: each warp stages its node's row once and the 20 candidate rows four
+// at a time (cp.async.bulk, one instruction per 4 KB row, two batches in
+// flight per warp), then its four 8-lane groups evaluate the reference's
+// scalar l2_sq from shared memory (same arithmetic as group8_l2_scalar, bit
+// for bit).  The row-major kernel keeps ~1 KB of 32-byte loads in flight per
+// warp; this one keeps up to 8 rows (30 KB for C5).
+constexpr uint32_t kBulkWarpsMax = 8;
+
+__device__ __forceinline__ uint32_t gk_su32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ float group8_l2_shared(const float* a, const float* b, uint32_t stride,
+                                                  bool active) {
+    const uint32_t l8 = lane_id() & 7u;
+    float acc = 0.0f;
+    if (active) {
+#pragma unroll 8
+        for (uint32_t c = 0; c < stride; c += 8) {
+            const float diff = __fsub_rn(a[c + l8], b[c + l8]);
+            acc = __fadd_rn(acc, __fmul_rn(diff, diff));
+        }
+    }
+    acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 1));
+    acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 2));
+    acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 4));
+    return acc;
+}
+
+__global__ void init_random_bulk_kernel(GraphView g, uint32_t seed_lo, uint32_t seed_hi) {
+    extern __shared__ __align__(128) float bulk_smem[];
+    __shared__ __align__(8) unsigned long long bars[kBulkWarpsMax][2];
+    const uint32_t w = threadIdx.x >> 5, lane = lane_id(), k = g.k, n = g.n;
+    const uint32_t stride = g.stride, row_bytes = stride * 4;
+    float* const own = bulk_smem + size_t(w) * 9 * stride;  // own row, then 2 x 4 rows
+    const uint32_t warp = blockIdx.x * (blockDim.x >> 5) + w;
+    const bool node = g.lo + warp < g.hi;
+    const uint32_t u = node ? g.lo + warp : g.lo;
+    if (lane == 0) {
+        for (uint32_t b = 0; b < 2; ++b)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(gk_su32(&bars[w][b])));
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncwarp();
+    if (!node) return;
+    // the reference's draws: k distinct ids != u (as init_random_kernel)
+    const bool real = lane < k;
+    uint32_t id = n + lane;
+    bool accepted = !real;
+    uint32_t attempt = 0;
+    const uint32_t lt = (1u << lane) - 1u;
+    while (true) {
+        if (!accepted) {
+            const Philox4 r = philox4x32_10(u, lane, attempt, kSaltInit, seed_lo, seed_hi);
+            id = bounded(r.x, n);
+        }
+        ++attempt;
+        const uint32_t same = __match_any_sync(0xffffffffu, id);
+        const uint32_t acc_mask = __ballot_sync(0xffffffffu, accepted);
+        if (!accepted) {
+            const uint32_t pending = ~acc_mask;
+            const bool conflict = id == u || (same & acc_mask) != 0u || (same & pending & lt) != 0u;
+            accepted = !conflict;
+        }
+        if (__all_sync(0xffffffffu, accepted)) break;
+    }
+    const uint32_t nb = (k + 3) / 4;
+    // the ids of a batch's rows live in lanes 4 batch + j: issue reads them by shuffle
+    auto issue_ids = [&](uint32_t batch) {
+        uint32_t r[4];
+        for (uint32_t j = 0; j < 4; ++j) r[j] = __shfl_sync(0xffffffffu, id, (4 * batch + j) & 31u);
+        if (lane == 0) {
+            const uint32_t b = batch & 1u, e = 4 * batch;
+            const uint32_t cnt = min(4u, k - e) + (batch == 0 ? 1u : 0u);
+            unsigned long long* bar = &bars[w][b];
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(
+                             gk_su32(bar)),
+                         "r"(cnt * row_bytes)
+                         : "memory");
+            auto copy_row = [&](float* dst, uint32_t rr) {
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], "
+                    "%2, [%3];\n" ::"r"(gk_su32(dst)),
+                    "l"(g.data + size_t(rr) * stride), "r"(row_bytes), "r"(gk_su32(bar))
+                    : "memory");
+            };
+            if (batch == 0) copy_row(own, u);
+            float* const buf = own + size_t(1 + 4 * b) * stride;
+            for (uint32_t j = 0; j < 4 && e + j < k; ++j) copy_row(buf + size_t(j) * stride, r[j]);
+        }
+    };
+    issue_ids(0);
+    if (nb > 1) issue_ids(1);
+    float mine = 0.0f;
+    for (uint32_t batch = 0; batch < nb; ++batch) {
+        const uint32_t b = batch & 1u, e = 4 * batch;
+        const uint32_t parity = (batch >> 1) & 1u;
+        asm volatile(
+            "{\n .reg .pred p;\n BW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+            " @!p bra BW_%=;\n}\n" ::"r"(gk_su32(&bars[w][b])),
+            "r"(parity)
+            : "memory");
+        const uint32_t pair = e + (lane >> 3);
+        const bool act = pair < k;
+        const float* rv = own + size_t(1 + 4 * b + (lane >> 3)) * stride;
+        const float dist = group8_l2_shared(own, rv, stride, act);
+        const uint32_t src = ((lane - e) & 3u) << 3;
+        const float got = __shfl_sync(0xffffffffu, dist, src);
+        if (lane >= e && lane < e + 4) mine = got;
+        __syncwarp();  // every group done with buffer b before it is refilled
+        if (batch + 2 < nb) issue_ids(batch + 2);
     }
     uint64_t key = real ? pack_key(mine, id) : kEmptyKey;
     key = warp_sort_u64(key);
@@ -926,6 +1052,27 @@ void launch_init_random(const GraphView& g, uint64_t seed, cudaStream_t s, const
                         const int32_t* lnorm) {
     if (g.hi <= g.lo) return;
     const uint32_t blocks = blocks_for(size_t(g.hi - g.lo) * 32, 256);
+    // long rows: the bulk-staged kernel (KNNG_INIT_BULK=0 keeps the row-major
+    // one); 9 rows of shared memory per warp
+    const char* bv = getenv("KNNG_INIT_BULK");
+    const size_t warp_bytes = size_t(9) * g.stride * 4;
+    const uint32_t bw = uint32_t(std::min<size_t>(kBulkWarpsMax, (220u * 1024u) / warp_bytes));
+    const char* bm = getenv("KNNG_INIT_BULK_MIN");
+    const uint32_t bulk_min = bm ? uint32_t(atoi(bm)) : 512u;
+    if (!packed && g.stride >= bulk_min && bw >= 1 && g.k <= 32 && !(bv && bv[0] == '0')) {
+        static bool attr[kMaxDevices] = {};
+        bool& done = attr[current_device()];
+        if (!done) {
+            check_launch(cudaFuncSetAttribute(init_random_bulk_kernel,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              220 * 1024));
+            done = true;
+        }
+        const uint32_t nodes = g.hi - g.lo;
+        init_random_bulk_kernel<<<(nodes + bw - 1) / bw, bw * 32, bw * warp_bytes, s>>>(
+            g, uint32_t(seed), uint32_t(seed >> 32));
+        return;
+    }
     if (packed)
         init_random_kernel<true><<<blocks, 256, 0, s>>>(g, uint32_t(seed), uint32_t(seed >> 32),
                                                         packed, lnorm, u8_lane_bytes(g.stride));

@@ -207,8 +207,11 @@ def test_join_variants_match_oracle(gpu, restated, monkeypatch, env, kind, n, k,
     assert checked > 0
 
 
-def test_init_random_properties(gpu, restated):
-    data = make_data("C1", 3000)
+@pytest.mark.parametrize("kind,bulk", [("C1", "1"), ("C5", "1"), ("C5", "0"), ("C2", "1")])
+def test_init_random_properties(gpu, restated, monkeypatch, kind, bulk):
+    # bulk=1: rows of >= 512 floats take the bulk-staged kernel (C5)
+    monkeypatch.setenv("KNNG_INIT_BULK", bulk)
+    data = make_data(kind, 3000)
     g, rev, ev = kg.init_random(data, 20, 77)
     n, k = g.ids.shape
     assert ev == n * k
