@@ -256,6 +256,7 @@ int knng_cuda_locality_permutation(uint32_t n, uint32_t k, const uint32_t* ids,
  * of the shard's own; sample, step and merge return host counts and so
  * synchronise it.
  * knng_cuda_run_multi drives the same phases for N GPUs in one process.
+ * Deterministic mode is not supported on shards.
  */
 typedef struct knng_cuda_shard knng_cuda_shard;
 
@@ -301,6 +302,17 @@ int knng_cuda_shard_merge(knng_cuda_shard* shard, const uint32_t* d_records, uin
                           uint64_t* changes);
 /* owned rows, sorted by (distance, id): (hi - lo) x k ids and distances. */
 int knng_cuda_shard_export(knng_cuda_shard* shard, uint32_t* d_ids, float* d_dists);
+/* The locality reorder on shards (descent.hpp:230-235), after iteration
+ * params.reorder_after_iteration: the caller first all-gathers every shard's
+ * owned rows (info.keys rows [lo, hi) x k, info.flags, info.maxd) into every
+ * shard; each shard then computes sigma from the whole graph (a deterministic
+ * function of it, so every shard gets the same one) and permutes its data
+ * and graph.  Shards go on owning rows [lo, hi) of the permuted order, i.e.
+ * contiguous ranges of sigma.  *info is refreshed (the graph buffers move);
+ * *d_sigma / *d_sigma_inv (n u32, device) map the exported rows back
+ * (descent.hpp:245). */
+int knng_cuda_shard_reorder(knng_cuda_shard* shard, knng_cuda_shard_info* info,
+                            const uint32_t** d_sigma, const uint32_t** d_sigma_inv);
 /* This shard's share so far: per-kernel device times (params.profile at
  * creation) and one row per iteration (its evaluations, candidates, inserts
  * into owned rows and join-kernel time). */

@@ -51,6 +51,7 @@ EXPORTS = (
     "knng_cuda_shard_merge",
     "knng_cuda_shard_export",
     "knng_cuda_shard_metrics",
+    "knng_cuda_shard_reorder",
     "knng_cuda_run_multi",
 )
 
@@ -181,6 +182,8 @@ def lib() -> C.CDLL:
     fn("knng_cuda_shard_merge", C.c_int, [vp, vp, C.c_uint64, u64p])
     fn("knng_cuda_shard_export", C.c_int, [vp, vp, vp])
     fn("knng_cuda_shard_metrics", C.c_int, [vp, C.POINTER(Metrics)])
+    fn("knng_cuda_shard_reorder", C.c_int, [vp, C.POINTER(ShardInfo), C.POINTER(vp),
+                                            C.POINTER(vp)])
     fn("knng_cuda_run_multi", C.c_int, [f32p, u32, u32, C.POINTER(Params), C.c_int, vp, u32p,
                                         f32p, C.POINTER(Metrics)])
     _lib = L

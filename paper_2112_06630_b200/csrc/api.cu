@@ -581,9 +581,10 @@ struct Engine {
         DevBuf<uint64_t> keys2;
         DevBuf<uint32_t> flags2;
         DevBuf<float> maxd2;
-        keys2.alloc(size_t(n) * k, pool, s);
-        flags2.alloc(n, pool, s);
-        maxd2.alloc(n, pool, s);
+        // rows_alloc rows (>= n): multi-GPU shards all-gather equal slices
+        keys2.alloc(size_t(rows_alloc) * k, pool, s);
+        flags2.alloc(rows_alloc, pool, s);
+        maxd2.alloc(rows_alloc, pool, s);
         GraphView out = gv();
         out.keys = keys2.p;
         out.flags = flags2.p;
@@ -1489,9 +1490,7 @@ knng_cuda_shard* shard_new(const float* data, bool data_on_device, uint32_t n, u
     if (nranks > kMaxShards)
         raise(KNNG_CUDA_INVALID_ARGUMENT, "this build supports at most 1023 shards");
     validate_params(n, d, p);
-    if (p.reorder && !allow_reorder)
-        raise(KNNG_CUDA_NOT_IMPLEMENTED,
-              "reorder on shards is supported by knng_cuda_run_multi, not by the phase API");
+    (void)allow_reorder;  // the phase API reorders through knng_cuda_shard_reorder
     if (p.deterministic)
         raise(KNNG_CUDA_NOT_IMPLEMENTED, "deterministic mode is not supported on the sharded path");
     auto* sh = new knng_cuda_shard();
@@ -1661,6 +1660,29 @@ int knng_cuda_shard_merge(knng_cuda_shard* sh, const uint32_t* d_records, uint64
         sh->enq_merge(d_records, count);
         sh->fin_merge();
         *changes = sh->last.changes;  // local + received merges of this iteration
+    });
+}
+
+int knng_cuda_shard_reorder(knng_cuda_shard* sh, knng_cuda_shard_info* info,
+                            const uint32_t** d_sigma, const uint32_t** d_sigma_inv) {
+    return guarded([&] {
+        if (!sh || !info || !d_sigma || !d_sigma_inv)
+            raise(KNNG_CUDA_INVALID_ARGUMENT, "null argument");
+        DeviceGuard dg(sh->device);
+        Engine& e = *sh->e;
+        // sigma is a deterministic function of the (gathered) graph, so every
+        // shard computes the same one
+        e.compute_sigma();
+        const uint32_t lo0 = e.lo, hi0 = e.hi;
+        e.lo = 0;
+        e.hi = e.n;
+        e.apply_sigma();
+        e.lo = lo0;
+        e.hi = hi0;
+        CK(cudaStreamSynchronize(sh->s));
+        shard_fill_info(sh, info);  // the graph buffers were reallocated
+        *d_sigma = e.sigma.p;
+        *d_sigma_inv = e.sigma_inv.p;
     });
 }
 

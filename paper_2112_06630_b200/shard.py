@@ -83,11 +83,30 @@ class GpuShardEngine:
         check(N.lib().knng_cuda_shard_create(self._data.data_ptr(), self.n, self.d, C.byref(p),
                                              rank, nranks, stream or None, C.byref(self._h),
                                              C.byref(info)))
+        self._views(info)
+        self.sigma = self.sigma_inv = None
+
+    def _views(self, info) -> None:
         self.chunk, self.lo, self.hi = int(info.chunk), int(info.lo), int(info.hi)
         self.seg_cap = int(info.seg_cap)
         rows = int(info.rows_alloc)
+        self.keys = _device_view(info.keys, rows * self.k, "<i8", self.device)
+        self.flags = _device_view(info.flags, rows, "<i4", self.device)
         self.maxd = _device_view(info.maxd, rows, "<f4", self.device)
         self.indeg = _device_view(info.indeg, self.n, "<i4", self.device)
+
+    def reorder(self):
+        """The locality reorder (descent.hpp:230-235) once every shard's rows
+        have been all-gathered into keys / flags / maxd: sigma (the same on
+        every shard), data and graph permuted; (sigma, sigma_inv) as int32
+        device views for the final remap."""
+        info = N.ShardInfo()
+        ps, pi = C.c_void_p(), C.c_void_p()
+        check(N.lib().knng_cuda_shard_reorder(self._h, C.byref(info), C.byref(ps), C.byref(pi)))
+        self._views(info)
+        self.sigma = _device_view(ps.value, self.n, "<i4", self.device)
+        self.sigma_inv = _device_view(pi.value, self.n, "<i4", self.device)
+        return self.sigma, self.sigma_inv
 
     def seeds(self, seed: int, count: int) -> np.ndarray:
         return seed_sequence(seed, count)
@@ -172,6 +191,7 @@ class ShardedResult:
     hi: int
     metrics: RunMetrics = field(default_factory=RunMetrics)
     bytes_exchanged: int = 0  # records sent by this rank (all iterations)
+    sigma: object = None      # after a reorder: rows / ids above are in sigma's order
 
 
 def _staged(t, group=None) -> bool:
@@ -232,6 +252,14 @@ def _exchange(segs: List, counts: List[int], width: int, dtype, dev, group=None)
     return recv
 
 
+def _allgather_rows(engine, group=None) -> None:
+    """Every shard's owned rows (keys, flags, row maxima) into every shard."""
+    r, P, chunk, k = engine.rank, engine.nranks, engine.chunk, engine.k
+    for buf, width in ((engine.keys, k), (engine.flags, 1), (engine.maxd, 1)):
+        parts = [buf[i * chunk * width:(i + 1) * chunk * width] for i in range(P)]
+        _all_gather(parts, parts[r].clone(), group=group)
+
+
 def _allgather_maxd(engine, group=None) -> None:
     import torch.distributed as dist
     r, P, chunk = engine.rank, engine.nranks, engine.chunk
@@ -274,6 +302,13 @@ def run_sharded(engine, params: RunParams, group=None) -> ShardedResult:
         tot = torch.tensor([changes, st["evals"], st["cands"]], dtype=torch.float64, device=dev)
         _all_reduce(tot, group=group)
         changes_all, evals_all, cands_all = (int(x) for x in tot.tolist())
+        # the locality reorder (descent.hpp:230-235): every shard gathers the
+        # whole graph and computes the same sigma; the shards then own
+        # contiguous ranges of sigma
+        if (params.reorder and getattr(engine, "sigma", None) is None
+                and it == params.reorder_after_iteration and hasattr(engine, "reorder")):
+            _allgather_rows(engine, group)
+            engine.reorder()
         metrics.iterations.append(IterationMetrics(it, time.perf_counter() - t0, evals_all,
                                                    changes_all, cands_all))
         if changes_all < threshold:
@@ -284,7 +319,8 @@ def run_sharded(engine, params: RunParams, group=None) -> ShardedResult:
         metrics.total_dist_evals += itm.dist_evals
         metrics.total_changes += itm.changes
     ids, dists = engine.export()
-    return ShardedResult(ids, dists, engine.lo, engine.hi, metrics, sent)
+    return ShardedResult(ids, dists, engine.lo, engine.hi, metrics, sent,
+                         getattr(engine, "sigma", None))
 
 
 def gather_graph(res: ShardedResult, n: int, k: int, group=None):
@@ -300,4 +336,17 @@ def gather_graph(res: ShardedResult, n: int, k: int, group=None):
     outs_d = [torch.empty_like(dd) for _ in range(P)]
     _all_gather(outs_i, ids.contiguous(), group=group)
     _all_gather(outs_d, dd.contiguous(), group=group)
-    return torch.cat(outs_i)[:n], torch.cat(outs_d)[:n]
+    ids_all, d_all = torch.cat(outs_i)[:n], torch.cat(outs_d)[:n]
+    if res.sigma is not None:
+        # back to the caller's ids (descent.hpp:245): row u is permuted row
+        # sigma[u], ids renamed by sigma_inv, rows re-sorted by (distance, id)
+        sigma = res.sigma.long()
+        inv = torch.empty_like(sigma)
+        inv[sigma] = torch.arange(n, device=sigma.device)
+        ids_all = inv[ids_all[sigma].long()]
+        d_all = d_all[sigma]
+        key = (d_all.contiguous().view(torch.int32).long() << 32) | ids_all
+        order = torch.argsort(key, dim=1)
+        ids_all = torch.gather(ids_all, 1, order).int()
+        d_all = torch.gather(d_all, 1, order)
+    return ids_all, d_all

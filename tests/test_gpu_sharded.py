@@ -236,7 +236,7 @@ def test_run_multi_reorder(gpu, kind, n, shards):
     assert np.allclose(dists[i], d64, rtol=1e-4, atol=1e-4)
 
 
-def _mp_worker(rank, world, port, out_path, kind, n):
+def _mp_worker(rank, world, port, out_path, kind, n, reorder=False):
     import sys
     sys.path.insert(0, ROOT)
     import torch
@@ -250,7 +250,8 @@ def _mp_worker(rank, world, port, out_path, kind, n):
                             world_size=world)
     cfg = ds.CONFIGS[kind]
     data = ds.generate(cfg, n=n) if kind in ("C3", "C4") else ds.generate(cfg)[:n]
-    params = kg2.RunParams(k=cfg.k, max_candidates=cfg.cap, seed=0)
+    params = kg2.RunParams(k=cfg.k, max_candidates=cfg.cap, seed=0, reorder=reorder,
+                           reorder_after_iteration=1)
     eng = GpuShardEngine(torch.from_numpy(data).cuda(), params, rank, world)
     res = run_sharded(eng, params)
     ids, dists = gather_graph(res, data.shape[0], cfg.k)
@@ -266,8 +267,12 @@ def _mp_worker(rank, world, port, out_path, kind, n):
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("kind,n,world", [("C1", 10000, 2), ("C4", 20000, 3), ("C2", 12000, 2)])
-def test_run_sharded_multiprocess(gpu, kind, n, world):
+@pytest.mark.parametrize("kind,n,world,reorder", [("C1", 10000, 2, False),
+                                                  ("C4", 20000, 3, False),
+                                                  ("C2", 12000, 2, False),
+                                                  ("C4", 20000, 2, True),
+                                                  ("C1", 10000, 3, True)])
+def test_run_sharded_multiprocess(gpu, kind, n, world, reorder):
     """shard.py's run_sharded in separate processes (the torchrun path of
     bench.py --gpus N), each rank a real CUDA shard engine; the GPU is shared,
     so the collectives go over gloo through host memory (NCCL does not
@@ -277,7 +282,7 @@ def test_run_sharded_multiprocess(gpu, kind, n, world):
 
     import torch.multiprocessing as mp
     out = tempfile.mktemp(suffix=".npz")
-    mp.spawn(_mp_worker, args=(world, _port(), out, kind, n), nprocs=world, join=True)
+    mp.spawn(_mp_worker, args=(world, _port(), out, kind, n, reorder), nprocs=world, join=True)
     r = np.load(out)
     os.unlink(out)
     cfg = datasets.CONFIGS[kind]
@@ -286,6 +291,12 @@ def test_run_sharded_multiprocess(gpu, kind, n, world):
     single = kg.run(data, params)
     ex, _ = kg.brute_force_knng(data, cfg.k)
     r_mp, r_single = kg.recall(r["ids"], ex), kg.recall(single.graph.ids, ex)
-    assert abs(r_mp - r_single) <= 0.005, (r_mp, r_single)
+    # with the reorder (shards own sigma ranges): within 0.01 of the plain
+    # build (test_descent.cpp:211-224)
+    assert abs(r_mp - r_single) <= (0.01 if reorder else 0.005), (r_mp, r_single)
     assert int(r["evals"][0]) == n * cfg.k
+    assert not np.any(r["ids"] == np.arange(n)[:, None])
+    i = np.arange(0, n, 97)
+    d64 = ((data[i, None, :].astype(np.float64) - data[r["ids"][i]].astype(np.float64)) ** 2).sum(-1)
+    assert np.allclose(r["dists"][i], d64, rtol=1e-4, atol=1e-4)
     assert np.all(np.diff(r["dists"], axis=1) >= 0)
