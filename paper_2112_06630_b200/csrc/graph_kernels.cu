@@ -393,6 +393,58 @@ __device__ __forceinline__ void offer(const CandView& c, uint32_t k, const uint3
     }
 }
 
+// The list insertion of an accepted offer that already holds its slot (the
+// reservoir rule of offer()).
+__device__ __forceinline__ void place(const CandView& c, uint32_t target, uint32_t cand,
+                                      uint32_t is_new, uint32_t slot, uint32_t r_slot) {
+    uint32_t* list = c.ids + size_t(target) * 2 * c.cap + (is_new ? 0u : c.cap);
+    if (slot < c.cap) {
+        list[slot] = cand;
+    } else {
+        const uint32_t j = bounded(r_slot, slot + 1u);
+        if (j < c.cap) list[j] = cand;
+    }
+}
+
+// Non-deterministic sampling, kEdges edges per thread: every edge's in-degree
+// loads, then every accepted offer's counter atomic, then the list stores, so
+// a thread keeps 2 kEdges independent random accesses in flight at each step
+// instead of a load -> atomic -> store chain per offer (the kernel is bound
+// by their latency: ncu long-scoreboard ~90 cycles per issue).
+template <uint32_t kEdges>
+__global__ void __launch_bounds__(256) sample_fast_kernel(GraphView g, CandView c,
+                                                          const uint32_t* __restrict__ indeg,
+                                                          uint32_t seed_lo, uint32_t seed_hi,
+                                                          const IterCounters* gate) {
+    if (gate->halt) return;
+    const size_t total = size_t(g.n) * g.k;
+    const size_t e0 = (size_t(blockIdx.x) * blockDim.x) * kEdges + threadIdx.x;
+    uint32_t tgt[2 * kEdges], cnd[2 * kEdges], nw[2 * kEdges], rs[2 * kEdges], slot[2 * kEdges];
+    bool acc[2 * kEdges];
+#pragma unroll
+    for (uint32_t q = 0; q < kEdges; ++q) {
+        const size_t e = e0 + size_t(q) * blockDim.x;
+        acc[2 * q] = acc[2 * q + 1] = false;
+        if (e >= total) continue;
+        const uint32_t u = uint32_t(e / g.k), i = uint32_t(e % g.k);
+        const uint32_t v = key_id(g.keys[e]);
+        const uint32_t is_new = (__ldg(g.flags + u) >> i) & 1u;
+        const Philox4 r = philox4x32_10(uint32_t(e), uint32_t(e >> 32), kSaltSample, 0u, seed_lo,
+                                        seed_hi);
+        tgt[2 * q] = u, cnd[2 * q] = v, rs[2 * q] = r.y;          // v into u
+        tgt[2 * q + 1] = v, cnd[2 * q + 1] = u, rs[2 * q + 1] = r.w;  // u into v
+        nw[2 * q] = nw[2 * q + 1] = is_new;
+        acc[2 * q] = u >= g.lo && u < g.hi && accept_offer(c, g.k, indeg, u, r.x);
+        acc[2 * q + 1] = v >= g.lo && v < g.hi && accept_offer(c, g.k, indeg, v, r.z);
+    }
+#pragma unroll
+    for (uint32_t o = 0; o < 2 * kEdges; ++o)
+        if (acc[o]) slot[o] = atomicAdd((nw[o] ? c.raw_new : c.raw_old) + tgt[o], 1u);
+#pragma unroll
+    for (uint32_t o = 0; o < 2 * kEdges; ++o)
+        if (acc[o]) place(c, tgt[o], cnd[o], nw[o], slot[o], rs[o]);
+}
+
 __global__ void __launch_bounds__(256) sample_kernel(GraphView g, CandView c,
                                                      const uint32_t* indeg, uint32_t seed_lo,
                                                      uint32_t seed_hi, IterCounters* gate,
@@ -1126,6 +1178,13 @@ void launch_apply_offers(const CandView& c, const uint4* recs, uint64_t count,
 void launch_sample(const GraphView& g, const CandView& c, const uint32_t* indeg, uint64_t seed,
                    cudaStream_t s, IterCounters* gate, uint64_t det_seed) {
     const uint32_t blocks = blocks_for(size_t(g.n) * g.k, 256);
+    const char* fv = getenv("KNNG_SAMPLE_FAST");
+    if (!c.det && !(fv && fv[0] == '0')) {
+        constexpr uint32_t kE = 2;
+        sample_fast_kernel<kE><<<blocks_for(size_t(g.n) * g.k, 256 * kE), 256, 0, s>>>(
+            g, c, indeg, uint32_t(seed), uint32_t(seed >> 32), gate);
+        return;
+    }
     sample_kernel<<<blocks, 256, 0, s>>>(g, c, indeg, uint32_t(seed), uint32_t(seed >> 32), gate,
                                          uint32_t(det_seed), uint32_t(det_seed >> 32));
     if (c.det && g.hi > g.lo) {

@@ -1122,10 +1122,22 @@ __global__ void scatter_rev_kernel(CandView c, const uint32_t* __restrict__ acti
     if (lane == 0)  // the distance kernel's per-node record
         c.arec[a] = make_uint4(u, nn | (no << 16), uint32_t(off), uint32_t(off >> 32));
     const uint32_t* list = c.ids + size_t(u) * 2 * c.cap;
-    for (uint32_t p = lane; p < m; p += 32) {
-        const uint32_t x = p < nn ? list[p] : list[c.cap + p - nn];
-        const uint32_t slot = c.roff[x] + atomicAdd(c.rcur + x, 1u);
-        c.rev[slot] = off + prow(p, nn, m);  // t's row of u's proposal block
+    // all of this lane's candidates' cursor atomics in flight at once (m <=
+    // 128: up to four per lane), then the reverse-index stores
+    constexpr uint32_t kPer = (2 * kMaxCap + 31) / 32;
+    uint32_t x[kPer], slot[kPer];
+#pragma unroll
+    for (uint32_t q = 0; q < kPer; ++q) {
+        const uint32_t p = lane + 32 * q;
+        if (p < m) {
+            x[q] = p < nn ? list[p] : list[c.cap + p - nn];
+            slot[q] = atomicAdd(c.rcur + x[q], 1u);
+        }
+    }
+#pragma unroll
+    for (uint32_t q = 0; q < kPer; ++q) {
+        const uint32_t p = lane + 32 * q;
+        if (p < m) c.rev[c.roff[x[q]] + slot[q]] = off + prow(p, nn, m);  // t's row of u's block
     }
 }
 
