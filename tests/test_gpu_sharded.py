@@ -300,3 +300,19 @@ def test_run_sharded_multiprocess(gpu, kind, n, world, reorder):
     d64 = ((data[i, None, :].astype(np.float64) - data[r["ids"][i]].astype(np.float64)) ** 2).sum(-1)
     assert np.allclose(r["dists"][i], d64, rtol=1e-4, atol=1e-4)
     assert np.all(np.diff(r["dists"], axis=1) >= 0)
+
+
+@pytest.mark.parametrize("n,k,shards", [(12, 3, 8), (50, 5, 8), (200, 10, 7)])
+def test_run_multi_tiny_and_empty_shards(gpu, n, k, shards):
+    """More shards than rows per shard, some owning no rows at all: the
+    exchanges with empty segments and the termination still work, and on a
+    tiny set the build reaches the exact K-NNG like the single-GPU one."""
+    data = np.random.default_rng(n).standard_normal((n, 6)).astype(np.float32)
+    params = kg.RunParams(k=k, max_candidates=2 * k, seed=1)
+    ids, dists, m = kg.run_multi(data, params, num_gpus=shards)
+    ex, _ = kg.brute_force_knng(data, k)
+    single = kg.run(data, params)
+    assert kg.recall(ids, ex) >= kg.recall(single.graph.ids, ex) - 0.02
+    assert all(len(set(r)) == k for r in ids.tolist())
+    assert not np.any(ids == np.arange(n)[:, None])
+    assert np.all(np.diff(dists, axis=1) >= 0)
