@@ -424,13 +424,17 @@ def run_sharded_bench(args, rank, world, local):
     t0 = time.perf_counter()
     e2e_evals = 0
     d2h = 0
+    ids_h = dists_h = None  # page-locked result rows, reused
     for _ in range(args.steps):
         dd = pinned.to(f"cuda:{local}", non_blocking=True)
         torch.cuda.synchronize()
         e = GpuShardEngine(dd, params, rank, world)
         r = run_sharded(e, params)
-        ids_h = r.ids.cpu()
-        dists_h = r.dists.cpu()
+        if ids_h is None or ids_h.shape != r.ids.shape:
+            ids_h = torch.empty(r.ids.shape, dtype=r.ids.dtype, pin_memory=True)
+            dists_h = torch.empty(r.dists.shape, dtype=r.dists.dtype, pin_memory=True)
+        ids_h.copy_(r.ids)
+        dists_h.copy_(r.dists)
         d2h += ids_h.numel() * 4 + dists_h.numel() * 4
         e2e_evals += r.metrics.total_dist_evals
         e.close()
@@ -542,13 +546,17 @@ def run_ours(args, rank, world, local):
     launches = sum(2 + 8 * (len(m.iterations) - 1) for m in mets)
     kernel_ms = {kname: sum(m.kernel_ms[kname] for m in mets) for kname in mets[0].kernel_ms}
 
-    # ---- e2e through the host-pointer C-ABI (pinned host data, graph back to host)
+    # ---- e2e through the host-pointer C-ABI (pinned host data, graph back to
+    # host into page-locked result arrays reused across builds, kg.run(out=))
     pinned = torch.empty((n, d), dtype=torch.float32, pin_memory=True)
     pinned.numpy()[:] = data
     host = pinned.numpy()
+    out = kg.KnnGraph(torch.empty((n, k), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32),
+                      torch.empty((n, k), dtype=torch.float32, pin_memory=True).numpy(),
+                      torch.empty((n, k), dtype=torch.uint8, pin_memory=True).numpy())
     hp = kg.RunParams(k=k, max_candidates=cap, termination_delta=cfg.delta, seed=cfg_r.seed,
                       device=local)
-    res = kg.run(host, hp)  # warm
+    res = kg.run(host, hp, out=out)  # warm
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -556,7 +564,7 @@ def run_ours(args, rank, world, local):
     e2e_evals = 0
     h2d = d2h = 0
     for _ in range(args.steps):
-        res = kg.run(host, hp)
+        res = kg.run(host, hp, out=out)
         e2e_evals += res.metrics.total_dist_evals
         h2d += res.metrics.h2d_bytes
         d2h += res.metrics.d2h_bytes

@@ -410,12 +410,27 @@ struct Engine {
     }
 
     // Rows padded to ceil8(d) with zeros (dataset.hpp:72-77).
+    // Host rows cross PCIe as one contiguous copy (a pitched host-to-device
+    // copy of 3136-byte rows ran at 34 GB/s against 57 for a flat one, C2) and
+    // are padded on the device.
     void upload(const float* src, bool src_on_device) {
+        const size_t bytes = sizeof(float) * size_t(n) * d;
         if (stride != d) CK(cudaMemsetAsync(data.p, 0, sizeof(float) * size_t(n) * stride, s));
-        CK(cudaMemcpy2DAsync(data.p, sizeof(float) * stride, src, sizeof(float) * d,
-                             sizeof(float) * d, n,
-                             src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
-        if (!src_on_device) h2d += sizeof(float) * size_t(n) * d;
+        if (src_on_device) {
+            CK(cudaMemcpy2DAsync(data.p, sizeof(float) * stride, src, sizeof(float) * d,
+                                 sizeof(float) * d, n, cudaMemcpyDeviceToDevice, s));
+            return;
+        }
+        h2d += bytes;
+        if (stride == d) {
+            copy_from_host({{const_cast<float*>(src), data.p, bytes}}, s);
+            return;
+        }
+        DevBuf<float> flat;
+        flat.alloc(size_t(n) * d, pool, s);
+        copy_from_host({{const_cast<float*>(src), flat.p, bytes}}, s);
+        CK(cudaMemcpy2DAsync(data.p, sizeof(float) * stride, flat.p, sizeof(float) * d,
+                             sizeof(float) * d, n, cudaMemcpyDeviceToDevice, s));
     }
 
     // the current slot's counters -> h_ctr[0]
@@ -887,11 +902,23 @@ void to_device(DevBuf<T>& buf, const T* host, size_t count, Engine& e) {
     e.h2d += sizeof(T) * count;
 }
 
+// Returns with the data on the host (host_io.cu stages pageable buffers).
 template <typename T>
 void to_host(T* host, const T* dev, size_t count, Engine& e) {
     if (!host) return;
-    CK(cudaMemcpyAsync(host, dev, sizeof(T) * count, cudaMemcpyDeviceToHost, e.s));
+    copy_to_host({{host, const_cast<T*>(dev), sizeof(T) * count}}, e.s);
     e.d2h += sizeof(T) * count;
+}
+
+// Several results in one staged transfer (null host buffers skipped).
+void results_to_host(std::vector<HostSeg> segs, Engine& e) {
+    std::vector<HostSeg> out;
+    for (const HostSeg& g : segs)
+        if (g.host && g.bytes) {
+            out.push_back(g);
+            e.d2h += g.bytes;
+        }
+    copy_to_host(out, e.s);
 }
 
 // from_rows validation (graph.hpp:70-93)
@@ -995,11 +1022,11 @@ int knng_cuda_run(const float* data, uint32_t n, uint32_t d, const knng_cuda_par
         if (want_sigma) sig.alloc(n, e.pool, e.s);
         run_engine(e, data, false, p, ids.p, dists.p, out_flags ? fl.p : nullptr, out_metrics,
                    want_sigma ? sig.p : nullptr);
-        to_host(out_ids, ids.p, nk, e);
-        to_host(out_dists, dists.p, nk, e);
-        if (out_flags) to_host(out_flags, fl.p, nk, e);
-        if (want_sigma) to_host(out_sigma, sig.p, n, e);
-        CK(cudaStreamSynchronize(e.s));
+        results_to_host({{out_ids, ids.p, sizeof(uint32_t) * nk},
+                         {out_dists, dists.p, sizeof(float) * nk},
+                         {out_flags, fl.p, nk},
+                         {want_sigma ? out_sigma : nullptr, sig.p, sizeof(uint32_t) * n}},
+                        e);
         if (out_metrics) {
             out_metrics->h2d_bytes = e.h2d;
             out_metrics->d2h_bytes = e.d2h;
@@ -2048,9 +2075,8 @@ void run_multi(const float* data, uint32_t n, uint32_t d, const knng_cuda_params
         ids.alloc(cnt, e0.pool, e0.s);
         dd.alloc(cnt, e0.pool, e0.s);
         e0.export_rows(ids.p, dd.p, nullptr);
-        CK(cudaMemcpyAsync(out_ids, ids.p, sizeof(uint32_t) * cnt, cudaMemcpyDeviceToHost, e0.s));
-        CK(cudaMemcpyAsync(out_dists, dd.p, sizeof(float) * cnt, cudaMemcpyDeviceToHost, e0.s));
-        CK(cudaStreamSynchronize(e0.s));
+        copy_to_host({{out_ids, ids.p, sizeof(uint32_t) * cnt}, {out_dists, dd.p, sizeof(float) * cnt}},
+                     e0.s);
     }
     // owned rows -> host
     for (uint32_t r = 0; r < P && !reordered; ++r) {
@@ -2064,11 +2090,9 @@ void run_multi(const float* data, uint32_t n, uint32_t d, const knng_cuda_params
         ids.alloc(cnt, s->e->pool, s->s);
         dd.alloc(cnt, s->e->pool, s->s);
         s->e->export_owned(ids.p, dd.p, nullptr);
-        CK(cudaMemcpyAsync(out_ids + size_t(lo) * p.k, ids.p, sizeof(uint32_t) * cnt,
-                           cudaMemcpyDeviceToHost, s->s));
-        CK(cudaMemcpyAsync(out_dists + size_t(lo) * p.k, dd.p, sizeof(float) * cnt,
-                           cudaMemcpyDeviceToHost, s->s));
-        CK(cudaStreamSynchronize(s->s));
+        copy_to_host({{out_ids + size_t(lo) * p.k, ids.p, sizeof(uint32_t) * cnt},
+                      {out_dists + size_t(lo) * p.k, dd.p, sizeof(float) * cnt}},
+                     s->s);
     }
     if (m) {
         uint64_t h2d = 0, d2h = 0;

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <vector>
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -222,5 +223,20 @@ void launch_permute_rows(const float* in, float* out, const uint32_t* sigma, uin
                          uint32_t stride, cudaStream_t s);
 void launch_remap_graph(const GraphView& in, const GraphView& out, const uint32_t* sigma,
                         cudaStream_t s);
+
+// --- host_io.cu -----------------------------------------------------------
+// One host buffer <-> one device buffer of `bytes` bytes.
+struct HostSeg {
+    void* host;
+    void* dev;
+    size_t bytes;
+};
+bool host_is_pinned(const void* p);
+// Pageable buffers go through a pinned ring drained / filled by host threads
+// while the copy engine runs; pinned ones are copied directly.
+// copy_from_host returns once the host buffers may be reused (copies
+// enqueued on s); copy_to_host returns once the data is in the host buffers.
+void copy_from_host(const std::vector<HostSeg>& segs, cudaStream_t s);
+void copy_to_host(const std::vector<HostSeg>& segs, cudaStream_t s);
 
 }  // namespace knng_cuda

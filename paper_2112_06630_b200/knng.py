@@ -203,21 +203,39 @@ def _as_data(data) -> np.ndarray:
     return data
 
 
-def run(data, params: RunParams = RunParams(), observer=None) -> RunResult:
+def _out_array(a, name, shape, dtype):
+    if (not isinstance(a, np.ndarray) or a.shape != shape or a.dtype != dtype
+            or not a.flags.c_contiguous or not a.flags.writeable):
+        raise InvalidArgument(f"out.{name} must be a writeable C-contiguous {np.dtype(dtype).name} "
+                              f"array of shape {shape}")
+    return a
+
+
+def run(data, params: RunParams = RunParams(), observer=None,
+        out: Optional[KnnGraph] = None) -> RunResult:
     """knng::run (descent.hpp:193-255) on the GPU; host arrays in and out.
 
     observer(iteration, KnnGraph): the reference's IterationObserver
     (descent.hpp:184, called at :241), after each iteration in the run's
-    current labeling (permuted ids after a reorder)."""
+    current labeling (permuted ids after a reorder).
+
+    out: caller-owned result arrays (n x k uint32 ids, float32 dists, uint8
+    flags or None), e.g. page-locked ones reused across builds; the returned
+    graph is `out`.  Without it the result goes to fresh arrays."""
     data = _as_data(data)
     params.validate()
     n, d = data.shape
     if n <= params.k:
         raise InvalidArgument("run: need n > k")
     k = params.k
-    ids = np.zeros((n, k), np.uint32)
-    dists = np.zeros((n, k), np.float32)
-    flags = np.zeros((n, k), np.uint8)
+    if out is None:
+        ids = np.zeros((n, k), np.uint32)
+        dists = np.zeros((n, k), np.float32)
+        flags = np.zeros((n, k), np.uint8)
+    else:
+        ids = _out_array(out.ids, "ids", (n, k), np.uint32)
+        dists = _out_array(out.dists, "dists", (n, k), np.float32)
+        flags = None if out.flags is None else _out_array(out.flags, "flags", (n, k), np.uint8)
     sigma = np.zeros(n, np.uint32) if params.reorder else None
     m, rows = _metrics(params.max_iterations + 1)
     p = params._c()
@@ -232,10 +250,11 @@ def run(data, params: RunParams = RunParams(), observer=None) -> RunResult:
         cb = N.OBSERVER(_obs)
         p.observer = C.cast(cb, C.c_void_p)
     check(N.lib().knng_cuda_run(data.ctypes.data, n, d, C.byref(p), ids.ctypes.data,
-                                dists.ctypes.data, flags.ctypes.data,
+                                dists.ctypes.data, flags.ctypes.data if flags is not None else None,
                                 sigma.ctypes.data if sigma is not None else None, C.byref(m)))
     del cb
-    return RunResult(KnnGraph(ids, dists, flags), RunMetrics._from_c(m, rows), sigma)
+    return RunResult(out if out is not None else KnnGraph(ids, dists, flags),
+                     RunMetrics._from_c(m, rows), sigma)
 
 
 def run_multi(data, params: RunParams = RunParams(), num_gpus: int = 2, devices=None):

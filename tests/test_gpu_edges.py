@@ -105,3 +105,42 @@ def test_iteration_observer(gpu):
     assert len(seen) == len(res2.metrics.iterations) - 1
     sig = res2.permutation
     assert np.array_equal(np.sort(seen[-1][1][sig], axis=1), np.sort(sig[res2.graph.ids], axis=1))
+
+
+# zero-padded stride 104; stride == d with 77 MB of rows (more chunks than
+# the 64 MiB ring has slots, so slots are reused)
+@pytest.mark.parametrize("n,d", [(30000, 100), (200000, 96)])
+def test_pinned_and_pageable_host_buffers_agree(gpu, n, d):
+    """host_io.cu: pageable rows and results go through the pinned ring (above
+    2 MiB), pinned ones are copied directly; both give the same graph as the
+    device-resident entry point."""
+    import torch
+    k = 20
+    data = np.random.default_rng(d).standard_normal((n, d), dtype=np.float32)
+    p = kg.RunParams(k=k, max_candidates=30, seed=5, deterministic=True)
+    a = kg.run(data, p)                                   # pageable in and out
+    pinned = torch.empty((n, d), dtype=torch.float32, pin_memory=True)
+    pinned.numpy()[:] = data
+    b = kg.run(pinned.numpy(), p)                         # pinned in, pageable out
+    assert a.metrics.h2d_bytes == b.metrics.h2d_bytes == data.nbytes
+    np.testing.assert_array_equal(a.graph.ids, b.graph.ids)
+    np.testing.assert_array_equal(a.graph.dists, b.graph.dists)
+    np.testing.assert_array_equal(a.graph.flags, b.graph.flags)
+    out = kg.KnnGraph(torch.empty((n, k), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32),
+                      torch.empty((n, k), dtype=torch.float32, pin_memory=True).numpy(),
+                      torch.empty((n, k), dtype=torch.uint8, pin_memory=True).numpy())
+    c = kg.run(pinned.numpy(), p, out=out)                # pinned in and out (caller-owned)
+    assert c.graph is out
+    np.testing.assert_array_equal(a.graph.ids, out.ids)
+    np.testing.assert_array_equal(a.graph.dists, out.dists)
+    np.testing.assert_array_equal(a.graph.flags, out.flags)
+    nof = kg.run(data, p, out=kg.KnnGraph(np.zeros((n, k), np.uint32), np.zeros((n, k), np.float32)))
+    assert nof.graph.flags is None
+    np.testing.assert_array_equal(a.graph.ids, nof.graph.ids)
+    dev = torch.from_numpy(data).cuda()
+    ids = torch.empty((n, k), dtype=torch.int32, device="cuda")
+    dd = torch.empty((n, k), dtype=torch.float32, device="cuda")
+    kg.run_device(dev.data_ptr(), n, d, p, ids.data_ptr(), dd.data_ptr())
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(a.graph.ids, ids.cpu().numpy().view(np.uint32))
+    np.testing.assert_array_equal(a.graph.dists, dd.cpu().numpy())

@@ -56,6 +56,15 @@ def test_invalid_arguments_before_any_device_work(native):
             kg.run(data, params)
     with pytest.raises(kg.InvalidArgument):
         kg.nndescent_l2(data, k=10, sample_rate=0.5)  # cap 5 < k
+    # caller-owned result arrays must match the graph's shape and types
+    p = kg.RunParams(k=5, max_candidates=10)
+    good = (np.zeros((30, 5), np.uint32), np.zeros((30, 5), np.float32), np.zeros((30, 5), np.uint8))
+    for bad in ((np.zeros((30, 4), np.uint32),) + good[1:],
+                (good[0].astype(np.int64),) + good[1:],
+                (good[0], np.zeros((5, 30), np.float32).T, good[2]),   # not C-contiguous
+                good[:2] + (np.zeros((30, 5), np.float32),)):
+        with pytest.raises(kg.InvalidArgument):
+            kg.run(data, p, out=kg.KnnGraph(*bad))
 
 
 @pytest.mark.skipif(os.environ.get("CUDA_VISIBLE_DEVICES") is None and
