@@ -21,12 +21,12 @@ OBJ = os.path.join(PKG, "build")
 LIB = os.path.join(PKG, "lib", "libknng_cuda.so")
 DIAG = os.path.join(PKG, "lib", "libknng_diag.so")  # FFMA peak probe (bench only)
 CLI = os.path.join(ROOT, "proj", "tools", "build", "knng_cuda_cli")  # build / recall front end
-SOURCES = ["graph_kernels.cu", "join.cu", "join_gl.cu", "join_tc.cu", "join_u8.cu", "join_u8_tc.cu", "bruteforce.cu", "reorder.cu", "host_io.cu", "api.cu"]
+SOURCES = ["graph_kernels.cu", "join.cu", "join5.cu", "join_gl.cu", "join_tc.cu", "join_u8.cu", "join_u8_tc.cu", "bruteforce.cu", "reorder.cu", "host_io.cu", "api.cu"]
 HEADERS = ["common.cuh", "kernels.cuh", "tile_math.cuh"]
 # join.cu: no FMA contraction anywhere, so the unfused (multiply, then add)
 # distance path stays unfused at the SASS level; explicit fma intrinsics are
 # unaffected (SURVEY.md §8a-6 bit-exactness)
-PER_FILE = {"join.cu": ["--fmad=false"], "join_gl.cu": ["--fmad=false"], "join_tc.cu": ["--fmad=false"]}
+PER_FILE = {"join.cu": ["--fmad=false"], "join5.cu": ["--fmad=false"], "join_gl.cu": ["--fmad=false"], "join_tc.cu": ["--fmad=false"]}
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
          "-I", os.path.join(ROOT, "include")]

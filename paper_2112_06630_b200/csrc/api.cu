@@ -518,6 +518,8 @@ struct Engine {
                 norms_valid = true;
             }
             launch_join_tc(gv(), cv(), cur, n, nrm2.p, nrmu.p, ovf.p, octr.p, s);
+        } else if (use_t5_join()) {
+            launch_join5(gv(), cv(), cur, n, s);
         } else {
             launch_join_distances(gv(), cv(), active.p, cur, n, s);
         }
@@ -564,6 +566,13 @@ struct Engine {
             u8_map_for = packed.p;
         }
         return true;
+    }
+
+    // The 5-aligned tile kernel (join5.cu): KNNG_JOIN_T5=1 / 0 forces it on /
+    // off.
+    bool use_t5_join() const {
+        const char* v = getenv("KNNG_JOIN_T5");
+        return v && v[0] == '1';
     }
 
     // The register-staged join (join_gl.cu) is opt-in: KNNG_JOIN_GL=1.

@@ -152,6 +152,11 @@ void launch_scatter_rev(const CandView& c, const uint32_t* active, IterCounters*
 // Distance stage of the local join: every active node's distance block.
 void launch_join_distances(const GraphView& g, const CandView& c, const uint32_t* active,
                            IterCounters* ctr, uint32_t max_active, cudaStream_t s);
+// --- join5.cu ----------------------------------------------------------------
+// The same distance stage with 5 x 10 tiles aligned to the reference's
+// 5-blocking (same proposal blocks, bit-identical distances).
+void launch_join5(const GraphView& g, const CandView& c, IterCounters* ctr, uint32_t max_active,
+                  cudaStream_t s);
 // --- join_gl.cu --------------------------------------------------------------
 // Long rows: the distance stage with candidate rows loaded straight into
 // registers from a lane-major copy of the data (same proposal blocks,

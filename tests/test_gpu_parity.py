@@ -169,7 +169,8 @@ VARIANT_CASES = [("C1", 10000, 20, 20, 0, 5), ("C3", 4000, 30, 50, 2, 4),
                  ("D100", 1500, 12, 20, 5, 2), ("G24", 600, 8, 15, 11, 3)]
 
 
-@pytest.mark.parametrize("env", ["KNNG_JOIN_UTILES=1", "KNNG_JOIN_UTILES=0", "KNNG_JOIN_GL=1"])
+@pytest.mark.parametrize("env", ["KNNG_JOIN_UTILES=1", "KNNG_JOIN_UTILES=0", "KNNG_JOIN_GL=1",
+                                 "KNNG_JOIN_T5=1"])
 @pytest.mark.parametrize("kind,n,k,cap,seed,t", VARIANT_CASES)
 def test_join_variants_match_oracle(gpu, restated, monkeypatch, env, kind, n, k, cap, seed, t):
     """The distance-stage variants forced on — U tiles for the leftover rows
