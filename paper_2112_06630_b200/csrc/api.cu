@@ -568,11 +568,11 @@ struct Engine {
         return true;
     }
 
-    // The 5-aligned tile kernel (join5.cu): KNNG_JOIN_T5=1 / 0 forces it on /
-    // off.
+    // The 5-aligned tile kernel (join5.cu) is the FP32 distance stage;
+    // KNNG_JOIN_T5=0 falls back to join.cu's 8 x 8 tile kernel (kept for A/B).
     bool use_t5_join() const {
         const char* v = getenv("KNNG_JOIN_T5");
-        return v && v[0] == '1';
+        return !(v && v[0] == '0');
     }
 
     // The register-staged join (join_gl.cu) is opt-in: KNNG_JOIN_GL=1.

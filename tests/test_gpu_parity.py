@@ -169,16 +169,18 @@ VARIANT_CASES = [("C1", 10000, 20, 20, 0, 5), ("C3", 4000, 30, 50, 2, 4),
                  ("D100", 1500, 12, 20, 5, 2), ("G24", 600, 8, 15, 11, 3)]
 
 
-@pytest.mark.parametrize("env", ["KNNG_JOIN_UTILES=1", "KNNG_JOIN_UTILES=0", "KNNG_JOIN_GL=1",
-                                 "KNNG_JOIN_T5=1"])
+@pytest.mark.parametrize("env", ["KNNG_JOIN_T5=1", "KNNG_JOIN_T5=0,KNNG_JOIN_UTILES=1",
+                                 "KNNG_JOIN_T5=0,KNNG_JOIN_UTILES=0", "KNNG_JOIN_GL=1"])
 @pytest.mark.parametrize("kind,n,k,cap,seed,t", VARIANT_CASES)
 def test_join_variants_match_oracle(gpu, restated, monkeypatch, env, kind, n, k, cap, seed, t):
-    """The distance-stage variants forced on — U tiles for the leftover rows
-    (join.cu tile_slab_u; default for long rows), 8x8 tiles only, and the
-    register-staged kernel (join_gl.cu, opt-in) — give the oracle's
-    accepted-update set and the reference's exact distance for every pair."""
-    name, val = env.split("=")
-    monkeypatch.setenv(name, val)
+    """The distance-stage variants forced on — the 5 x 10 tile kernel (join5.cu,
+    the default), join.cu's 8 x 8 tile kernel with and without U tiles for the
+    leftover rows, and the register-staged kernel (join_gl.cu, opt-in) — give
+    the oracle's accepted-update set and the reference's exact distance for
+    every pair."""
+    for item in env.split(","):
+        name, val = item.split("=")
+        monkeypatch.setenv(name, val)
     data = make_data(kind, n, seed)
     gi, c, go, _, ev_ref = restated.capture_step(data, k, cap, seed, t)
     cands = kg.CandidateSet(c.ids, c.new_counts, c.old_counts)
