@@ -9,15 +9,21 @@
 // (nn = 5..20 new, 20..40 old candidates) only a quarter to a third of the
 // computed pair slots are live.  Here a tile is 5 rows x 10 columns (two
 // independent 5-column blocks), so the reference's own block boundaries are
-// tile boundaries:
-//   F  (fused)    new rows [5i, 5i + 5) x two 5-blocks out of
-//                 {new blocks j >= i (j == i: the triangle)} ++ {full old blocks}
-//   U  (unfused)  the nn % 5 leftover new rows x every column, 10 at a time
-//   U2 (unfused)  the no % 5 leftover old candidates (as rows) x the fused
-//                 new candidates, 10 at a time
-// A node's candidates keep their list order as slots (new, then old), with no
-// padding inside a node or between the nodes of a batch.  nn = 7, no = 23:
-// 3 F + 3 U + 1 U2 tiles of 50 pairs against ten 8 x 8 tiles.
+// tile boundaries.  A node's candidates take slots in the order
+//   [ fn fused new | r = nn % 5 leftover new | ro = no % 5 leftover old | fo fused old ]
+// (no padding inside a node or between the nodes of a batch), and its pairs
+// run as
+//   F (fused)    new rows [5i, 5i + 5) x two 5-blocks out of
+//                {new blocks j >= i (j == i: the triangle)} ++ {full old blocks}
+//   U (unfused)  the leftover rows -- the r leftover new candidates against
+//                every column, and (when the node has fused new candidates) the
+//                ro leftover old candidates against the fused new ones -- share
+//                the row block [fn, fn + 5): 5 x 10 tiles over the columns; a
+//                second row block only when r + ro > 5
+//   T (unfused)  the same leftover rows when r + ro <= 2: thin 2 x 24 tiles
+//                (a late node with one new and 23 old candidates is one tile of
+//                48 pair slots instead of three of 50)
+// nn = 7, no = 23: 3 F + 3 U tiles of 50 pairs against ten 8 x 8 tiles.
 //
 // Everything else is join.cu's design: persistent CTAs of 16 groups of 8
 // lanes (thread l8 = reference lane l8, packed FFMA2 arithmetic, the
@@ -54,7 +60,14 @@ constexpr uint32_t kMaxBatch = 8;
 constexpr uint32_t kSlotTab = 320;  // batch slots
 constexpr uint32_t kBlkTab = kSlotTab / 8;
 constexpr uint32_t kMaxTiles = 384;
-constexpr uint32_t kDeadTile = 0xffffffffu;
+constexpr uint32_t kDeadTile = 3u << 22;   // kind 3: padding, no work
+constexpr uint32_t kGroupEnd = 1u << 27;   // last tile of a pass group
+
+#ifndef KNNG_T5_ENDMIN
+#define KNNG_T5_ENDMIN 17  // off: measured no gain (C5 391 vs 388 ms with 12 vs off)
+#endif
+constexpr uint32_t kEndMin = KNNG_T5_ENDMIN;  // fewest tiles of a pass cut short at a group boundary
+constexpr uint32_t kGroupSlots = (kPassBlk - 1) * 8;  // a pass group's slots fit one pass
 static_assert(kBlkTab <= 64, "pass block masks are 64-bit");
 static_assert(kPassBlk >= 6, "one tile reads up to six blocks");
 static_assert(kRingRows % (kThreads / (kSlab / 4)) == 0, "staging sweeps cover the ring");
@@ -62,8 +75,14 @@ static_assert(kRingRows % (kThreads / (kSlab / 4)) == 0, "staging sweeps cover t
 // tile descriptor: node-relative slots
 //   [0,7) ra   first row slot        [7,14) ca   first slot of column block A
 //   [14,21) cb first slot of column block B      [21] column block B present
-//   [22,24) kind (0 F, 1 U, 2 U2)    [24,27) node index in the batch
-constexpr uint32_t kKindF = 0, kKindU = 1, kKindU2 = 2;
+//   [22,24) kind (0 F, 1 U, 2 T, 3 dead)  [24,27) node index in the batch
+//   [27] last tile of its pass group
+constexpr uint32_t kKindF = 0, kKindU = 1, kKindT = 2;
+__device__ __forceinline__ bool tile_dead(uint32_t tile) { return ((tile >> 22) & 3u) == 3u; }
+constexpr uint32_t kThinCols = 24;  // T tile: 2 rows x 24 columns
+#ifndef KNNG_T5_THIN
+#define KNNG_T5_THIN 1
+#endif
 __device__ __forceinline__ uint32_t make_tile(uint32_t v, uint32_t kind, uint32_t ra, uint32_t ca,
                                               uint32_t cb, bool has_b) {
     return ra | (ca << 7) | ((cb & 127u) << 14) | (uint32_t(has_b) << 21) | (kind << 22) |
@@ -72,22 +91,41 @@ __device__ __forceinline__ uint32_t make_tile(uint32_t v, uint32_t kind, uint32_
 
 struct Geom5 {
     uint32_t nn, no, fn, fo, m;
-    __device__ __forceinline__ void set(uint32_t nn_, uint32_t no_) {
+    uint32_t ro;    // leftover old candidates (slots [nn, nn + ro))
+    uint32_t lrow;  // live leftover rows: slots [fn, fn + lrow)
+    uint32_t ext;   // columns the first leftover row block runs against: [0, ext)
+    bool thin_ok;   // thin tiles allowed (compile-time per kernel instantiation)
+    __device__ __forceinline__ void set(uint32_t nn_, uint32_t no_, bool thin_ok_) {
+        thin_ok = thin_ok_;
         nn = nn_;
         no = no_;
         fn = nn - nn % 5;
-        fo = no - no % 5;
+        ro = no % 5;
+        fo = no - ro;
         m = nn + no;
+        // leftover old candidates are rows only against fused new columns
+        lrow = (nn - fn) + (fn ? ro : 0u);
+        ext = nn > fn ? m : fn;
     }
+    // slot -> position in the node's candidate order (new list, then old list)
+    __device__ __forceinline__ uint32_t cand(uint32_t slot) const {
+        if (slot < nn) return slot;
+        const uint32_t x = slot - nn;
+        return x < ro ? nn + fo + x : nn + x - ro;
+    }
+    __device__ __forceinline__ bool thin() const { return thin_ok && lrow <= 2; }
     __device__ __forceinline__ uint32_t f_tiles() const {
         const uint32_t nfb = fn / 5, nob = fo / 5;
         uint32_t t = 0;
         for (uint32_t i = 0; i < nfb; ++i) t += (nfb - i + nob + 1) / 2;
         return t;
     }
-    __device__ __forceinline__ uint32_t u_tiles() const { return nn > fn ? (m + 9) / 10 : 0u; }
-    __device__ __forceinline__ uint32_t u2_tiles() const {
-        return (no > fo && fn) ? (fn + 9) / 10 : 0u;
+    __device__ __forceinline__ uint32_t u_tiles() const {
+        if (!lrow || thin()) return 0u;
+        return (ext + 9) / 10 + (lrow > 5 ? (fn + 9) / 10 : 0u);
+    }
+    __device__ __forceinline__ uint32_t t_tiles() const {
+        return lrow && thin() ? (ext + kThinCols - 1) / kThinCols : 0u;
     }
     // t-th fused tile
     __device__ __forceinline__ uint32_t f_tile(uint32_t v, uint32_t t) const {
@@ -98,15 +136,30 @@ struct Geom5 {
             ++i;
         }
         const uint32_t len = nfb - i + nob, q0 = 2 * t, q1 = 2 * t + 1;
-        auto col = [&](uint32_t q) { return q < nfb - i ? 5 * (i + q) : nn + 5 * (q - (nfb - i)); };
+        auto col = [&](uint32_t q) {
+            return q < nfb - i ? 5 * (i + q) : nn + ro + 5 * (q - (nfb - i));
+        };
         return make_tile(v, kKindF, 5 * i, col(q0), q1 < len ? col(q1) : 0u, q1 < len);
     }
-    // t-th unfused tile (U tiles first, then U2)
+    // t-th 5 x 10 leftover-row tile: the first row block over [0, ext), then
+    // the second (leftover old rows only) over the fused new columns
     __device__ __forceinline__ uint32_t u_tile(uint32_t v, uint32_t t) const {
-        const uint32_t nu = u_tiles();
-        if (t < nu) return make_tile(v, kKindU, fn, 10 * t, 10 * t + 5, 10 * t + 5 < m);
-        t -= nu;
-        return make_tile(v, kKindU2, nn + fo, 10 * t, 10 * t + 5, 10 * t + 5 < fn);
+        const uint32_t na = (ext + 9) / 10;
+        if (t < na) return make_tile(v, kKindU, fn, 10 * t, 10 * t + 5, 10 * t + 5 < ext);
+        t -= na;
+        return make_tile(v, kKindU, fn + 5, 10 * t, 10 * t + 5, 10 * t + 5 < fn);
+    }
+    // t-th thin tile
+    __device__ __forceinline__ uint32_t t_tile(uint32_t v, uint32_t t) const {
+        return make_tile(v, kKindT, fn, kThinCols * t, 0u, false);
+    }
+    // columns a leftover-row tile with first row ra runs against
+    __device__ __forceinline__ uint32_t col_end(uint32_t ra) const { return ra == fn ? ext : fn; }
+    // is (row slot r, column slot cc) a pair of the leftover-row tiles?  Every
+    // unfused pair exactly once.
+    __device__ __forceinline__ bool leftover_pair(uint32_t r, uint32_t cc) const {
+        if (r < nn) return cc < m && (cc < fn || cc >= nn || cc > r);  // r >= fn: a leftover new row
+        return r < fn + lrow && cc < fn;  // a leftover old row: fused new columns only
     }
 };
 
@@ -114,7 +167,7 @@ struct Shared5 {
     // the slab ring follows this struct in dynamic shared memory
     uint32_t colrow[kSlotTab];   // batch slot -> data row id (~0: none)
     float colmax[kSlotTab];      // batch slot -> candidate's row maximum
-    uint32_t rowcnt[kSlotTab];   // proposals kept per candidate row
+    uint32_t rowcnt[kSlotTab];   // per candidate row: write cursor in the node's proposal block
     uint32_t tiles[kMaxTiles];
     uint8_t blkpos[kBlkTab];     // pass mode: batch 8-slot block -> ring position
     uint8_t blklist[kPassBlk + 2];
@@ -138,13 +191,21 @@ __device__ __forceinline__ void cp_async_wait_pending() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(kPending));
 }
 
-constexpr size_t kRingOffset = (sizeof(Shared5) + 127) / 128 * 128;
-// eight spare rows: a tile's last rows may overhang its node (masked pairs)
-constexpr size_t kSmem5 = kRingOffset + size_t(kStages * kRingRows + 8) * kPitch * sizeof(float);
-static_assert(kSmem5 + 1024 <= 228 * 1024 / 4, "four CTAs per SM");
+// Dynamic shared memory: the slab ring first, then the tables.  A tile's last
+// rows may overhang its node and a thin tile reads 24 consecutive ring rows
+// whatever its live width, so reads can run up to 23 rows past the ring's end:
+// they land in the tables (masked pairs, any bit pattern will do).
+constexpr size_t kRingBytes = size_t(kStages) * kRingRows * kPitch * sizeof(float);
+constexpr size_t kSmem5 = kRingBytes + sizeof(Shared5);
+static_assert(kRingBytes % 16 == 0, "tables stay 16-byte aligned");
+static_assert(sizeof(Shared5) >= (kThinCols - 1) * kPitch * sizeof(float), "overhang stays inside");
+#ifndef KNNG_T5_CTAS
+#define KNNG_T5_CTAS 4
+#endif
+static_assert(kSmem5 + 1024 <= 228 * 1024 / KNNG_T5_CTAS, "CTAs per SM");
 
 __device__ __forceinline__ float* ring5(Shared5& sh) {
-    return reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(&sh) + kRingOffset);
+    return reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(&sh) - kRingBytes);
 }
 
 // One 32-float slab of a 5 x 10 tile.  pa / pb / pc: element l8 of the tile's
@@ -188,6 +249,29 @@ __device__ __forceinline__ void slab5(const float* __restrict__ pa, const float*
     }
 }
 
+// One 32-float slab of a thin 2 x 24 unfused tile.  pa: element l8 of the first
+// of the two rows, pb: of the first of 24 consecutive column rows.
+// acc[12 x + j] holds pairs (x, 2j) and (x, 2j + 1); acc[24] stays zero.
+__device__ __forceinline__ void slab_thin(const float* __restrict__ pa,
+                                          const float* __restrict__ pb, uint32_t nseg,
+                                          float2 minus_zero, float2 (&acc)[25]) {
+    const float2 minus_one = make_float2(-1.0f, -1.0f);
+#pragma unroll
+    for (uint32_t s = 0; s < kSlab / 8; ++s) {
+        if (s >= nseg) break;
+        const float a0 = pa[8 * s], a1 = pa[kPitch + 8 * s];
+        const float2 ax0 = make_float2(a0, a0), ax1 = make_float2(a1, a1);
+#pragma unroll
+        for (uint32_t j = 0; j < kThinCols / 2; ++j) {
+            const float2 b = make_float2(pb[(2 * j) * kPitch + 8 * s], pb[(2 * j + 1) * kPitch + 8 * s]);
+            const float2 d0 = __ffma2_rn(b, minus_one, ax0);
+            const float2 d1 = __ffma2_rn(b, minus_one, ax1);
+            acc[j] = __fadd2_rn(acc[j], __ffma2_rn(d0, d0, minus_zero));
+            acc[kThinCols / 2 + j] = __fadd2_rn(acc[kThinCols / 2 + j], __ffma2_rn(d1, d1, minus_zero));
+        }
+    }
+}
+
 __device__ __forceinline__ float acc5_at(const float2 (&acc)[25], uint32_t p) {
     if (p >= 50) return 0.0f;
     return (p & 1u) ? acc[p >> 1].y : acc[p >> 1].x;
@@ -220,19 +304,37 @@ __device__ __forceinline__ void group_reduce56(const float2 (&acc)[25], uint32_t
     }
 }
 
-__global__ void __launch_bounds__(kThreads, 4) join5_kernel(GraphView g, CandView c,
-                                                            IterCounters* ctr,
-                                                            uint32_t res_slots,
-                                                            float minus_zero) {
+// Three instantiations (a third of the code each: the short-row configs were
+// stalling on instruction fetch with everything in one kernel):
+//   kModeResident  short rows, a batch's rows staged once (C1, C4)
+//   kModePass      rows streamed through the slab ring, a few slabs per pass
+//                  (C3): per-pass set-up dominates, so the batch is one pass
+//                  group (phase-major tile list, fewest passes) and there are
+//                  no thin tiles
+//   kModePassLong  rows of kLongRow floats or more (C5): node-major pass groups
+//                  and thin tiles, which cut the rows staged per evaluation
+constexpr int kModeResident = 0, kModePass = 1, kModePassLong = 2;
+#ifndef KNNG_T5_LONGROW
+#define KNNG_T5_LONGROW 512
+#endif
+constexpr uint32_t kLongRow = KNNG_T5_LONGROW;
+template <int kMode>
+__global__ void __launch_bounds__(kThreads, KNNG_T5_CTAS) join5_kernel(GraphView g, CandView c,
+                                                                      IterCounters* ctr,
+                                                                      uint32_t res_slots,
+                                                                      float minus_zero) {
+    constexpr bool kResident = kMode == kModeResident;
+    constexpr bool kGrouped = kMode == kModePassLong;
+    constexpr bool kThinOK = KNNG_T5_THIN && kMode == kModePassLong;
     const float2 mz2 = make_float2(minus_zero, minus_zero);  // -0.0f, opaque to ptxas
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    Shared5& sh = *reinterpret_cast<Shared5*>(smem_raw);
+    Shared5& sh = *reinterpret_cast<Shared5*>(smem_raw + kRingBytes);
     const uint32_t tid = threadIdx.x, group = tid >> 3, l8 = tid & 7u;
     const uint32_t stride = g.stride, cap = c.cap;
     if (ctr->overflow || ctr->halt) return;
     const uint32_t n_active = ctr->active;
     const uint32_t n_slabs = (stride + kSlab - 1) / kSlab;
-    const bool resident = res_slots != 0;
+    constexpr bool resident = kResident;
     if (tid == 0) {
         sh.qn = 0;
         sh.slot_budget = resident ? res_slots : kSlotTab;
@@ -262,9 +364,10 @@ __global__ void __launch_bounds__(kThreads, 4) join5_kernel(GraphView g, CandVie
             nn = rec.y & 0xffffu;
             no = rec.y >> 16;
             Geom5 ng;
-            ng.set(nn, no);
+            ng.set(nn, no, kThinOK);
             s_l = ng.m;
-            t_l = ng.f_tiles() + ng.u_tiles() + ng.u2_tiles();
+            t_l = ((ng.f_tiles() + 3u) & ~3u) + ((ng.u_tiles() + 3u) & ~3u) + ((ng.t_tiles() + 3u) & ~3u);
+            if (t_l < kGroups) t_l = kGroups;  // an upper bound of its share of the tile list
         }
         uint32_t si = s_l, ti = t_l;
 #pragma unroll
@@ -277,7 +380,7 @@ __global__ void __launch_bounds__(kThreads, 4) join5_kernel(GraphView g, CandVie
             }
         }
         const bool fit = lane < qn && lane < kMaxBatch &&
-                         (lane == 0 || (si <= sh.slot_budget && ti <= kMaxTiles - 8));
+                         (lane == 0 || (si <= sh.slot_budget && ti <= kMaxTiles));
         const uint32_t nv = __popc(__ballot_sync(0xffffffffu, fit));  // a prefix
         __syncwarp();
         if (lane < nv) {
@@ -311,7 +414,9 @@ __global__ void __launch_bounds__(kThreads, 4) join5_kernel(GraphView g, CandVie
                 uint32_t v = 0;
                 while (v + 1 < D.nv && D.colbase[v + 1] <= sidx) ++v;
                 const uint32_t x = sidx - D.colbase[v], nn = D.vnn[v];
-                const uint32_t pos = x < nn ? x : cap + x - nn;
+                Geom5 ng;
+                ng.set(nn, D.vno[v], kThinOK);
+                const uint32_t pos = x < nn ? x : cap + ng.cand(x) - nn;
                 const size_t base = size_t(D.node[v]) * 2 * cap;
                 pf_id[j] = c.ids[base + pos];
                 pf_max[j] = c.filter ? c.cmax[base + pos] : __int_as_float(0x7f800000);
@@ -335,7 +440,17 @@ __global__ void __launch_bounds__(kThreads, 4) join5_kernel(GraphView g, CandVie
             if (sidx < ((nslots + 7u) & ~7u)) {  // the last block's tail reads as "no row"
                 sh.colrow[sidx] = pf_id[j];
                 sh.colmax[sidx] = pf_max[j];
-                sh.rowcnt[sidx] = 0;
+                // the row's write cursor: word index, in the node's proposal
+                // block, of the next key (the row's first word is its count)
+                uint32_t cursor = 0;
+                if (sidx < nslots) {
+                    uint32_t v = 0;
+                    while (v + 1 < nv && B.colbase[v + 1] <= sidx) ++v;
+                    Geom5 ng;
+                    ng.set(B.vnn[v], B.vno[v], kThinOK);
+                    cursor = uint32_t(prow(ng.cand(sidx - B.colbase[v]), ng.nn, ng.m)) + 1u;
+                }
+                sh.rowcnt[sidx] = cursor;
             }
         }
         if (tid < 32) form_batch(sh.bd[cur ^ 1u]);
@@ -358,21 +473,69 @@ __global__ void __launch_bounds__(kThreads, 4) join5_kernel(GraphView g, CandVie
             }
             cp_async_commit();
         }
-        // the batch's tiles: every node's fused tiles, padding to a whole
-        // warp, then the unfused ones, so each warp runs one path
+        // The batch's tiles.  Nodes are taken in pass groups: consecutive nodes
+        // whose tiles fill at most one pass (16 tiles, kGroupSlots slots), so
+        // that a node's rows are staged once for all of its tiles; a node with
+        // more tiles is a group of its own.  Inside a group: the 5 x 10
+        // leftover-row tiles of its nodes, the thin ones, then the fused ones
+        // (a big node's later fused row blocks read only its later columns),
+        // each run padded to a whole warp so that each warp runs one path.
+        // Resident mode stages the batch once, and short rows want the fewest
+        // passes: there the whole batch is one group.
         if (tid < 32) {
             const uint32_t lane = tid;
-            uint32_t cf_l = 0, cu_l = 0;
+            uint32_t cnt_l[3] = {0, 0, 0}, s_l = 0;  // F, U, T tiles; slots
             if (lane < nv) {
                 Geom5 ng;
-                ng.set(B.vnn[lane], B.vno[lane]);
-                cf_l = ng.f_tiles();
-                cu_l = ng.u_tiles() + ng.u2_tiles();
+                ng.set(B.vnn[lane], B.vno[lane], kThinOK);
+                cnt_l[0] = ng.f_tiles();
+                cnt_l[1] = ng.u_tiles();
+                cnt_l[2] = ng.t_tiles();
+                s_l = ng.m;
             }
-            uint32_t nt = 0;
-            for (uint32_t phase = 0; phase < 2; ++phase) {
-                const uint32_t mine = phase ? cu_l : cf_l;
-                uint32_t incl = mine;
+            auto pad4 = [](uint32_t x) { return (x + 3u) & ~3u; };
+            // every lane walks the nodes; lane v keeps node v's run offsets
+            uint32_t gbase = 0, gfirst = 0, gf = 0, gu = 0, gt = 0, gs = 0;
+            uint32_t pre[3] = {0, 0, 0}, off[3] = {0, 0, 0};
+            uint32_t gend_l = 0;  // lane v: index of its group's last tile slot
+            auto close = [&](uint32_t wend) {  // the group is nodes [gfirst, wend)
+                const uint32_t pu = pad4(gu), pt = pad4(gt), pf = pad4(gf);
+                uint32_t len = pu + pt + pf;
+                if (lane >= gfirst && lane < wend) {
+                    off[1] = gbase + pre[1];
+                    off[2] = gbase + pu + pre[2];
+                    off[0] = gbase + pu + pt + pre[0];
+                    gend_l = gbase + len - 1;
+                }
+                gbase += len;
+                gfirst = wend;
+                gf = gu = gt = gs = 0;
+            };
+            for (uint32_t w = 0; w < nv; ++w) {
+                const uint32_t fw = __shfl_sync(0xffffffffu, cnt_l[0], w);
+                const uint32_t uw = __shfl_sync(0xffffffffu, cnt_l[1], w);
+                const uint32_t tw = __shfl_sync(0xffffffffu, cnt_l[2], w);
+                const uint32_t sw = __shfl_sync(0xffffffffu, s_l, w);
+                if (kGrouped && w > gfirst &&
+                    (pad4(gf + fw) + pad4(gu + uw) + pad4(gt + tw) > kGroups || gs + sw > kGroupSlots))
+                    close(w);
+                if (lane == w) {
+                    pre[0] = gf;
+                    pre[1] = gu;
+                    pre[2] = gt;
+                }
+                gf += fw;
+                gu += uw;
+                gt += tw;
+                gs += sw;
+            }
+            close(nv);
+            const uint32_t nt = gbase;
+            for (uint32_t t = lane; t < nt; t += 32) sh.tiles[t] = kDeadTile;
+            __syncwarp();
+#pragma unroll
+            for (uint32_t phase = 0; phase < 3; ++phase) {
+                uint32_t incl = cnt_l[phase];
 #pragma unroll
                 for (uint32_t o = 1; o < kMaxBatch; o <<= 1) {
                     const uint32_t p = __shfl_up_sync(0xffffffffu, incl, o);
@@ -390,19 +553,18 @@ __global__ void __launch_bounds__(kThreads, 4) join5_kernel(GraphView g, CandVie
                             before = iw;
                         }
                     }
+                    const uint32_t ov = __shfl_sync(0xffffffffu, off[phase], v & 31u);
                     if (t < total) {
                         Geom5 ng;
-                        ng.set(B.vnn[v], B.vno[v]);
-                        sh.tiles[nt + t] = phase ? ng.u_tile(v, t - before) : ng.f_tile(v, t - before);
+                        ng.set(B.vnn[v], B.vno[v], kThinOK);
+                        sh.tiles[ov + t - before] = phase == 0   ? ng.f_tile(v, t - before)
+                                                    : phase == 1 ? ng.u_tile(v, t - before)
+                                                                 : ng.t_tile(v, t - before);
                     }
                 }
-                nt += total;
-                if (phase == 0) {  // pad the fused run to whole warps
-                    const uint32_t padded = (nt + 3u) & ~3u;
-                    if (lane < padded - nt) sh.tiles[nt + lane] = kDeadTile;
-                    nt = padded;
-                }
             }
+            __syncwarp();
+            if (lane < nv) atomicOr(&sh.tiles[gend_l], kGroupEnd);
             if (lane == 0) sh.n_tiles = nt;
         }
         if (resident) cp_async_wait_pending<0>();
@@ -419,21 +581,32 @@ __global__ void __launch_bounds__(kThreads, 4) join5_kernel(GraphView g, CandVie
                     uint64_t m = 0;
                     if (lane < left) {
                         const uint32_t tile = sh.tiles[t0 + lane];
-                        if (tile != kDeadTile) {
-                            const uint32_t v = tile >> 24, kind = (tile >> 22) & 3u;
+                        if (!tile_dead(tile)) {
+                            const uint32_t v = (tile >> 24) & 7u, kind = (tile >> 22) & 3u;
                             const uint32_t ra = tile & 127u, ca = (tile >> 7) & 127u,
                                            cb = (tile >> 14) & 127u;
                             Geom5 ng;
-                            ng.set(B.vnn[v], B.vno[v]);
+                            ng.set(B.vnn[v], B.vno[v], kThinOK);
                             const uint32_t base = B.colbase[v];
-                            const uint32_t rend = kind == kKindF ? ra + 5 : (kind == kKindU ? ng.nn : ng.m);
-                            const uint32_t cend = kind == kKindF ? 128u : (kind == kKindU ? ng.m : ng.fn);
-                            auto range = [&](uint32_t s0, uint32_t end) {
-                                const uint32_t s1 = min(s0 + 5, end) - 1;  // last needed slot
-                                return (1ull << ((base + s0) >> 3)) | (1ull << ((base + s1) >> 3));
+                            // 8-slot blocks of the node's slots [s0, s1]
+                            auto range = [&](uint32_t s0, uint32_t s1) {
+                                const uint32_t lo = (base + s0) >> 3, hi = (base + s1) >> 3;
+                                return ((2ull << hi) - 1ull) & ~((1ull << lo) - 1ull);
                             };
-                            m = range(ra, rend) | range(ca, cend);
-                            if ((tile >> 21) & 1u) m |= range(cb, cend);
+                            if (kind == kKindF) {
+                                m = range(ra, ra + 4) | range(ca, ca + 4);
+                                if ((tile >> 21) & 1u) m |= range(cb, cb + 4);
+                            } else {
+                                const uint32_t rend = ng.fn + ng.lrow, cend = ng.col_end(ra);
+                                const uint32_t rows = kind == kKindU ? 5u : 2u;
+                                m = range(ra, min(ra + rows, rend) - 1);
+                                if (kind == kKindU) {
+                                    m |= range(ca, min(ca + 5, cend) - 1);
+                                    if ((tile >> 21) & 1u) m |= range(cb, min(cb + 5, cend) - 1);
+                                } else {
+                                    m |= range(ca, min(ca + kThinCols, cend) - 1);
+                                }
+                            }
                         }
                     }
 #pragma unroll
@@ -447,7 +620,14 @@ __global__ void __launch_bounds__(kThreads, 4) join5_kernel(GraphView g, CandVie
                     const uint32_t fitm = __ballot_sync(0xffffffffu, fits);
                     const uint32_t okm = __ballot_sync(
                         0xffffffffu, fits && ((lane & 3u) == 3u || lane + 1 == left));
-                    const uint32_t last = 31u - __clz(okm ? okm : fitm);
+                    // ... and end at a pass-group boundary when that still
+                    // fills kEndMin groups: the next group then starts a pass
+                    // and its rows are staged once
+                    const uint32_t endm = __ballot_sync(
+                        0xffffffffu, fits && (sh.tiles[t0 + min(lane, left - 1)] & kGroupEnd));
+                    uint32_t pick = okm ? okm : fitm;
+                    if ((endm & pick) >> (kEndMin - 1)) pick &= endm;
+                    const uint32_t last = 31u - __clz(pick);
                     const uint64_t pm = __shfl_sync(0xffffffffu, m, last);
                     for (uint32_t bit = lane; bit < kBlkTab; bit += 32)
                         if ((pm >> bit) & 1ull) {
@@ -467,9 +647,9 @@ __global__ void __launch_bounds__(kThreads, 4) join5_kernel(GraphView g, CandVie
             }
             const uint32_t t = t0 + group;
             const uint32_t tile0 = group < pass_len && t < n_tiles ? sh.tiles[t] : kDeadTile;
-            const bool live = tile0 != kDeadTile;
+            const bool live = !tile_dead(tile0);
             const uint32_t tile = live ? tile0 : 0u;
-            const uint32_t v = tile >> 24, kind = (tile >> 22) & 3u;
+            const uint32_t v = (tile >> 24) & 7u, kind = (tile >> 22) & 3u;
             const uint32_t ra = tile & 127u, ca = (tile >> 7) & 127u;
             const bool has_b = (tile >> 21) & 1u;
             const uint32_t cb = has_b ? (tile >> 14) & 127u : ca;
@@ -487,8 +667,10 @@ __global__ void __launch_bounds__(kThreads, 4) join5_kernel(GraphView g, CandVie
                         const uint32_t nseg = min(kSlab, stride - s * kSlab) / 8u;
                         if (kind == kKindF)
                             slab5<true>(pa, pb, pc, nseg, mz2, acc);
-                        else
+                        else if (kind == kKindU)
                             slab5<false>(pa, pb, pc, nseg, mz2, acc);
+                        else
+                            slab_thin(pa, pb, nseg, mz2, acc);
                         pa += slab_floats;
                         pb += slab_floats;
                         pc += slab_floats;
@@ -541,8 +723,10 @@ __global__ void __launch_bounds__(kThreads, 4) join5_kernel(GraphView g, CandVie
                     if (live) {
                         if (kind == kKindF)
                             slab5<true>(stage + oa, stage + ob, stage + oc, nseg, mz2, acc);
-                        else
+                        else if (kind == kKindU)
                             slab5<false>(stage + oa, stage + ob, stage + oc, nseg, mz2, acc);
+                        else
+                            slab_thin(stage + oa, stage + ob, nseg, mz2, acc);
                     }
                 }
                 gslab += n_slabs;
@@ -551,25 +735,29 @@ __global__ void __launch_bounds__(kThreads, 4) join5_kernel(GraphView g, CandVie
             group_reduce56(acc, l8, sums);
             if (live) {
                 Geom5 ng;
-                ng.set(B.vnn[v], B.vno[v]);
-                const uint32_t nn = ng.nn, m = ng.m, fn = ng.fn;
+                ng.set(B.vnn[v], B.vno[v], kThinOK);
+                const uint32_t nn = ng.nn;
                 uint64_t* const D = c.D + B.doff[v];
                 const uint32_t p0 = 28u * (l8 & 1u) + 14u * ((l8 >> 1) & 1u) + 7u * ((l8 >> 2) & 1u);
 #pragma unroll
                 for (uint32_t q = 0; q < 7; ++q) {
                     const uint32_t p = p0 + q;
                     if (p >= 50) break;
-                    const uint32_t x = p / 10u, y = p % 10u;
-                    if (y >= 5 && !has_b) continue;
-                    const uint32_t r = ra + x, cc = y < 5 ? ca + y : cb + (y - 5);
-                    // every evaluated pair exactly once, in the reference's class
-                    bool ok;
-                    if (kind == kKindF)
-                        ok = cc >= nn || cc > r;  // r < fn; new block j >= i, or a full old block
-                    else if (kind == kKindU)
-                        ok = r < nn && cc < m && (cc >= nn || cc < fn || cc > r);
-                    else
-                        ok = r < m && cc < fn;
+                    uint32_t r, cc;
+                    if (kind == kKindT) {
+                        const uint32_t x = p / kThinCols, y = p % kThinCols;
+                        if (x >= 2) continue;
+                        r = ra + x;
+                        cc = ca + y;
+                    } else {
+                        const uint32_t x = p / 10u, y = p % 10u;
+                        if (y >= 5 && !has_b) continue;
+                        r = ra + x;
+                        cc = y < 5 ? ca + y : cb + (y - 5);
+                    }
+                    // every evaluated pair exactly once, in the reference's class:
+                    // fused rows (r < fn) against new blocks j >= i or full old blocks
+                    const bool ok = kind == kKindF ? (cc >= nn || cc > r) : ng.leftover_pair(r, cc);
                     if (!ok) continue;
                     const uint32_t sr = base + r, sc = base + cc;
                     const uint32_t id_r = sh.colrow[sr], id_c = sh.colrow[sc];
@@ -577,23 +765,21 @@ __global__ void __launch_bounds__(kThreads, 4) join5_kernel(GraphView g, CandVie
                     // self (graph.hpp:116-129)
                     if (c.filter && id_r == id_c) continue;
                     const float dist = sums[q];
-                    if (dist < sh.colmax[sr]) {
-                        const uint32_t pos = atomicAdd(&sh.rowcnt[sr], 1u);
-                        D[prow(r, nn, m) + 1 + pos] = pack_key(dist, id_c);
-                    }
-                    if (dist < sh.colmax[sc]) {
-                        const uint32_t pos = atomicAdd(&sh.rowcnt[sc], 1u);
-                        D[prow(cc, nn, m) + 1 + pos] = pack_key(dist, id_r);
-                    }
+                    if (dist < sh.colmax[sr]) D[atomicAdd(&sh.rowcnt[sr], 1u)] = pack_key(dist, id_c);
+                    if (dist < sh.colmax[sc]) D[atomicAdd(&sh.rowcnt[sc], 1u)] = pack_key(dist, id_r);
                 }
             }
         }
         // row counts of the batch's proposal blocks
         __syncthreads();
         for (uint32_t v = 0; v < nv; ++v) {
-            const uint32_t nn = B.vnn[v], m = nn + B.vno[v];
-            for (uint32_t r = tid; r < m; r += kThreads)
-                c.D[B.doff[v] + prow(r, nn, m)] = sh.rowcnt[B.colbase[v] + r];
+            Geom5 ng;
+            ng.set(B.vnn[v], B.vno[v], kThinOK);
+            for (uint32_t r = tid; r < ng.m; r += kThreads)
+            {
+                const uint32_t first = uint32_t(prow(ng.cand(r), ng.nn, ng.m));
+                c.D[B.doff[v] + first] = sh.rowcnt[B.colbase[v] + r] - first - 1u;
+            }
         }
         __syncthreads();  // the next batch rewrites the slot tables
         cur ^= 1u;
@@ -614,20 +800,25 @@ void launch_join5(const GraphView& g, const CandView& c, IterCounters* ctr, uint
         return !(v && v[0] == '0');
     }();
     if (res_slots < 2 * c.cap || !allow_resident) res_slots = 0;
-    static int occ[kMaxDevices] = {};  // per device: the attribute is per device
-    int& per_sm = occ[current_device()];
+    // per device and instantiation: the attribute is per device
+    static int occ[3][kMaxDevices] = {};
+    const int mode = res_slots ? kModeResident : (g.stride >= kLongRow ? kModePassLong : kModePass);
+    auto kernel = mode == kModeResident ? join5_kernel<kModeResident>
+                  : mode == kModePass   ? join5_kernel<kModePass>
+                                        : join5_kernel<kModePassLong>;
+    int& per_sm = occ[mode][current_device()];
     if (!per_sm) {
-        check_launch(cudaFuncSetAttribute(join5_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        check_launch(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           int(kSmem5)));
         int v = 0;
-        check_launch(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, join5_kernel, int(kThreads),
+        check_launch(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kernel, int(kThreads),
                                                                    kSmem5));
         per_sm = v < 1 ? 1 : v;
     }
     uint32_t grid = device_sm_count() * uint32_t(per_sm);
     if (grid > max_active) grid = max_active;
     check_launch(cudaMemsetAsync(&ctr->work, 0, sizeof(uint32_t), s));
-    join5_kernel<<<grid, kThreads, kSmem5, s>>>(g, c, ctr, res_slots, -0.0f);
+    kernel<<<grid, kThreads, kSmem5, s>>>(g, c, ctr, res_slots, -0.0f);
 }
 
 }  // namespace knng_cuda
