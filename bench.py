@@ -223,7 +223,7 @@ def _traffic(config):
 
 
 def join_roofline(mets, n, d, k, peak_tflops, config):
-    """Roofline of the local-join distance kernel (join_distances_kernel).
+    """Roofline of the local-join distance kernel (join5_kernel, csrc/join5.cu).
 
     Per launch (one per iteration) the algorithmic work is, after SURVEY.md
     §8d: F = evals * (3d - 1) credited flops (distance.hpp:19-21) and
@@ -268,7 +268,7 @@ def join_roofline(mets, n, d, k, peak_tflops, config):
                 "peak_source": beta_src}
     roof.update({
         "frac": round(frac, 4), "traffic": traffic, "traffic_note": traffic_note,
-        "kernel": "join_distances_kernel (local-join distance stage)",
+        "kernel": "join5_kernel (local-join distance stage, 5 x 10 tiles)",
         "frac_definition": "sum over launches of max(F/pi, Q/beta) / sum of launch times",
         "fp32_tflops_achieved": round(F / t / 1e12, 3) if t else None,
         "gather_gbs_achieved": round(Q / t / 1e9, 1) if t else None,

@@ -45,12 +45,18 @@ namespace {
 
 constexpr uint32_t kThreads = 128;  // 16 groups of 8 lanes
 constexpr uint32_t kGroups = kThreads / 8;
-constexpr uint32_t kSlab = 32;      // floats per row per ring stage
-constexpr uint32_t kStages = 3;
+#ifndef KNNG_T5_SLAB
+#define KNNG_T5_SLAB 32
+#endif
+#ifndef KNNG_T5_STAGES
+#define KNNG_T5_STAGES 3
+#endif
+constexpr uint32_t kSlab = KNNG_T5_SLAB;      // floats per row per ring stage
+constexpr uint32_t kStages = KNNG_T5_STAGES;
 // Ring rows are kPitch floats apart: 36 puts rows r and r + 10 (the column
 // blocks of the four tiles a warp usually runs) 8 banks apart, and rows r and
 // r + 5 20 banks apart, so the groups' 8-bank reads do not collide.
-constexpr uint32_t kPitch = 36;
+constexpr uint32_t kPitch = kSlab + 4;
 #ifndef KNNG_T5_PASSBLK
 #define KNNG_T5_PASSBLK 14
 #endif
@@ -215,14 +221,14 @@ __device__ __forceinline__ float* ring5(Shared5& sh) {
 // fma(b, -1, a) == a - b, then fma(diff, diff, acc) on fused tiles or
 // acc + fma(diff, diff, -0) (the rounded square; -0 opaque to ptxas) on
 // unfused ones.
+// (seg5: one 8-float segment.  A slab without the per-segment exit test lets
+// ptxas hoist loads across segments but costs spills: C5 -0.4%, C4 +5%.)
 template <bool kFusedTile>
-__device__ __forceinline__ void slab5(const float* __restrict__ pa, const float* __restrict__ pb,
-                                      const float* __restrict__ pc, uint32_t nseg,
-                                      float2 minus_zero, float2 (&acc)[25]) {
+__device__ __forceinline__ void seg5(const float* __restrict__ pa, const float* __restrict__ pb,
+                                     const float* __restrict__ pc, uint32_t s, float2 minus_zero,
+                                     float2 (&acc)[25]) {
     const float2 minus_one = make_float2(-1.0f, -1.0f);
-#pragma unroll
-    for (uint32_t s = 0; s < kSlab / 8; ++s) {
-        if (s >= nseg) break;  // the row's last slab may be partial (stride % 32)
+    {
         float a[5];
         float2 b[5];
 #pragma unroll
@@ -248,17 +254,25 @@ __device__ __forceinline__ void slab5(const float* __restrict__ pa, const float*
         }
     }
 }
+template <bool kFusedTile>
+__device__ __forceinline__ void slab5(const float* __restrict__ pa, const float* __restrict__ pb,
+                                      const float* __restrict__ pc, uint32_t nseg,
+                                      float2 minus_zero, float2 (&acc)[25]) {
+#pragma unroll
+    for (uint32_t s = 0; s < kSlab / 8; ++s) {
+        if (s >= nseg) break;  // the row's last slab may be partial (stride % 32)
+        seg5<kFusedTile>(pa, pb, pc, s, minus_zero, acc);
+    }
+}
 
 // One 32-float slab of a thin 2 x 24 unfused tile.  pa: element l8 of the first
 // of the two rows, pb: of the first of 24 consecutive column rows.
 // acc[12 x + j] holds pairs (x, 2j) and (x, 2j + 1); acc[24] stays zero.
-__device__ __forceinline__ void slab_thin(const float* __restrict__ pa,
-                                          const float* __restrict__ pb, uint32_t nseg,
-                                          float2 minus_zero, float2 (&acc)[25]) {
+__device__ __forceinline__ void seg_thin(const float* __restrict__ pa,
+                                         const float* __restrict__ pb, uint32_t s,
+                                         float2 minus_zero, float2 (&acc)[25]) {
     const float2 minus_one = make_float2(-1.0f, -1.0f);
-#pragma unroll
-    for (uint32_t s = 0; s < kSlab / 8; ++s) {
-        if (s >= nseg) break;
+    {
         const float a0 = pa[8 * s], a1 = pa[kPitch + 8 * s];
         const float2 ax0 = make_float2(a0, a0), ax1 = make_float2(a1, a1);
 #pragma unroll
@@ -269,6 +283,15 @@ __device__ __forceinline__ void slab_thin(const float* __restrict__ pa,
             acc[j] = __fadd2_rn(acc[j], __ffma2_rn(d0, d0, minus_zero));
             acc[kThinCols / 2 + j] = __fadd2_rn(acc[kThinCols / 2 + j], __ffma2_rn(d1, d1, minus_zero));
         }
+    }
+}
+__device__ __forceinline__ void slab_thin(const float* __restrict__ pa,
+                                          const float* __restrict__ pb, uint32_t nseg,
+                                          float2 minus_zero, float2 (&acc)[25]) {
+#pragma unroll
+    for (uint32_t s = 0; s < kSlab / 8; ++s) {
+        if (s >= nseg) break;
+        seg_thin(pa, pb, s, minus_zero, acc);
     }
 }
 
