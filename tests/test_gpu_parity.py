@@ -30,6 +30,10 @@ def make_data(kind, n, seed=0):
         return datasets.generate(datasets.CONFIGS[kind], n)
     if kind == "G24":
         return np.random.default_rng(seed).standard_normal((n, 24), dtype=np.float32)
+    if kind == "L600":  # stride 600: long-row pass mode with a partial last slab (24 floats)
+        rng = np.random.default_rng(seed)
+        c = rng.normal(0, 4, (12, 600)).astype(np.float32)
+        return (c[rng.integers(0, 12, n)] + rng.standard_normal((n, 600), dtype=np.float32))
     if kind == "D100":  # stride 104: a partial last slab (8 floats) in resident staging
         return np.random.default_rng(seed).uniform(0, 1, (n, 100)).astype(np.float32)
     raise KeyError(kind)
@@ -43,6 +47,7 @@ CASES = [  # kind, n, k, cap, seed, step
     ("C4", 4000, 10, 50, 3, 1), ("C4", 4000, 10, 50, 3, 3),
     ("C5", 2000, 20, 50, 4, 1), ("C5", 2000, 20, 50, 4, 2),
     ("D100", 1500, 12, 20, 5, 1), ("D100", 1500, 12, 20, 5, 2),
+    ("L600", 1500, 12, 24, 6, 1), ("L600", 1500, 12, 24, 6, 5),
 ]
 
 
@@ -166,7 +171,10 @@ def test_candidate_distances_bit_exact(gpu, restated, kind, n, k, cap, seed, t):
 
 VARIANT_CASES = [("C1", 10000, 20, 20, 0, 5), ("C3", 4000, 30, 50, 2, 4),
                  ("C5", 2000, 20, 50, 4, 2), ("C5", 2000, 20, 50, 4, 8),
-                 ("D100", 1500, 12, 20, 5, 2), ("G24", 600, 8, 15, 11, 3)]
+                 ("D100", 1500, 12, 20, 5, 2), ("G24", 600, 8, 15, 11, 3),
+                 ("L600", 1500, 12, 24, 6, 4),
+                 # the largest lists the build supports (cap 64: up to 128 slots per node)
+                 ("C3", 3000, 32, 64, 7, 2), ("L600", 1200, 32, 64, 8, 2)]
 
 
 @pytest.mark.parametrize("env", ["KNNG_JOIN_T5=1", "KNNG_JOIN_T5=0,KNNG_JOIN_UTILES=1",
