@@ -22,7 +22,7 @@ LIB = os.path.join(PKG, "lib", "libknng_cuda.so")
 DIAG = os.path.join(PKG, "lib", "libknng_diag.so")  # FFMA peak probe (bench only)
 CLI = os.path.join(ROOT, "proj", "tools", "build", "knng_cuda_cli")  # build / recall front end
 SOURCES = ["graph_kernels.cu", "join.cu", "join5.cu", "join_gl.cu", "join_tc.cu", "join_u8.cu", "join_u8_tc.cu", "bruteforce.cu", "reorder.cu", "host_io.cu", "api.cu"]
-HEADERS = ["common.cuh", "kernels.cuh", "tile_math.cuh"]
+HEADERS = ["common.cuh", "kernels.cuh", "tile_math.cuh", "join5_geom.cuh"]
 # join.cu: no FMA contraction anywhere, so the unfused (multiply, then add)
 # distance path stays unfused at the SASS level; explicit fma intrinsics are
 # unaffected (SURVEY.md §8a-6 bit-exactness)

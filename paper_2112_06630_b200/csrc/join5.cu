@@ -36,6 +36,7 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include "join5_geom.cuh"
 #include "kernels.cuh"
 #include "tile_math.cuh"
 
@@ -78,96 +79,11 @@ static_assert(kBlkTab <= 64, "pass block masks are 64-bit");
 static_assert(kPassBlk >= 6, "one tile reads up to six blocks");
 static_assert(kRingRows % (kThreads / (kSlab / 4)) == 0, "staging sweeps cover the ring");
 
-// tile descriptor: node-relative slots
-//   [0,7) ra   first row slot        [7,14) ca   first slot of column block A
-//   [14,21) cb first slot of column block B      [21] column block B present
-//   [22,24) kind (0 F, 1 U, 2 T, 3 dead)  [24,27) node index in the batch
-//   [27] last tile of its pass group
-constexpr uint32_t kKindF = 0, kKindU = 1, kKindT = 2;
-__device__ __forceinline__ bool tile_dead(uint32_t tile) { return ((tile >> 22) & 3u) == 3u; }
-constexpr uint32_t kThinCols = 24;  // T tile: 2 rows x 24 columns
+// (tile descriptors and Geom5: join5_geom.cuh)
+using namespace t5;
 #ifndef KNNG_T5_THIN
 #define KNNG_T5_THIN 1
 #endif
-__device__ __forceinline__ uint32_t make_tile(uint32_t v, uint32_t kind, uint32_t ra, uint32_t ca,
-                                              uint32_t cb, bool has_b) {
-    return ra | (ca << 7) | ((cb & 127u) << 14) | (uint32_t(has_b) << 21) | (kind << 22) |
-           (v << 24);
-}
-
-struct Geom5 {
-    uint32_t nn, no, fn, fo, m;
-    uint32_t ro;    // leftover old candidates (slots [nn, nn + ro))
-    uint32_t lrow;  // live leftover rows: slots [fn, fn + lrow)
-    uint32_t ext;   // columns the first leftover row block runs against: [0, ext)
-    bool thin_ok;   // thin tiles allowed (compile-time per kernel instantiation)
-    __device__ __forceinline__ void set(uint32_t nn_, uint32_t no_, bool thin_ok_) {
-        thin_ok = thin_ok_;
-        nn = nn_;
-        no = no_;
-        fn = nn - nn % 5;
-        ro = no % 5;
-        fo = no - ro;
-        m = nn + no;
-        // leftover old candidates are rows only against fused new columns
-        lrow = (nn - fn) + (fn ? ro : 0u);
-        ext = nn > fn ? m : fn;
-    }
-    // slot -> position in the node's candidate order (new list, then old list)
-    __device__ __forceinline__ uint32_t cand(uint32_t slot) const {
-        if (slot < nn) return slot;
-        const uint32_t x = slot - nn;
-        return x < ro ? nn + fo + x : nn + x - ro;
-    }
-    __device__ __forceinline__ bool thin() const { return thin_ok && lrow <= 2; }
-    __device__ __forceinline__ uint32_t f_tiles() const {
-        const uint32_t nfb = fn / 5, nob = fo / 5;
-        uint32_t t = 0;
-        for (uint32_t i = 0; i < nfb; ++i) t += (nfb - i + nob + 1) / 2;
-        return t;
-    }
-    __device__ __forceinline__ uint32_t u_tiles() const {
-        if (!lrow || thin()) return 0u;
-        return (ext + 9) / 10 + (lrow > 5 ? (fn + 9) / 10 : 0u);
-    }
-    __device__ __forceinline__ uint32_t t_tiles() const {
-        return lrow && thin() ? (ext + kThinCols - 1) / kThinCols : 0u;
-    }
-    // t-th fused tile
-    __device__ __forceinline__ uint32_t f_tile(uint32_t v, uint32_t t) const {
-        const uint32_t nfb = fn / 5, nob = fo / 5;
-        uint32_t i = 0;
-        while (t >= (nfb - i + nob + 1) / 2) {
-            t -= (nfb - i + nob + 1) / 2;
-            ++i;
-        }
-        const uint32_t len = nfb - i + nob, q0 = 2 * t, q1 = 2 * t + 1;
-        auto col = [&](uint32_t q) {
-            return q < nfb - i ? 5 * (i + q) : nn + ro + 5 * (q - (nfb - i));
-        };
-        return make_tile(v, kKindF, 5 * i, col(q0), q1 < len ? col(q1) : 0u, q1 < len);
-    }
-    // t-th 5 x 10 leftover-row tile: the first row block over [0, ext), then
-    // the second (leftover old rows only) over the fused new columns
-    __device__ __forceinline__ uint32_t u_tile(uint32_t v, uint32_t t) const {
-        const uint32_t na = (ext + 9) / 10;
-        if (t < na) return make_tile(v, kKindU, fn, 10 * t, 10 * t + 5, 10 * t + 5 < ext);
-        t -= na;
-        return make_tile(v, kKindU, fn + 5, 10 * t, 10 * t + 5, 10 * t + 5 < fn);
-    }
-    // t-th thin tile
-    __device__ __forceinline__ uint32_t t_tile(uint32_t v, uint32_t t) const {
-        return make_tile(v, kKindT, fn, kThinCols * t, 0u, false);
-    }
-    // columns a leftover-row tile with first row ra runs against
-    __device__ __forceinline__ uint32_t col_end(uint32_t ra) const { return ra == fn ? ext : fn; }
-    // is (row slot r, column slot cc) a pair of the leftover-row tiles?  Every
-    // unfused pair exactly once.
-    __device__ __forceinline__ bool leftover_pair(uint32_t r, uint32_t cc) const {
-        if (r < nn) return cc < m && (cc < fn || cc >= nn || cc > r);  // r >= fn: a leftover new row
-        return r < fn + lrow && cc < fn;  // a leftover old row: fused new columns only
-    }
-};
 
 struct Shared5 {
     // the slab ring follows this struct in dynamic shared memory
@@ -759,7 +675,6 @@ __global__ void __launch_bounds__(kThreads, KNNG_T5_CTAS) join5_kernel(GraphView
             if (live) {
                 Geom5 ng;
                 ng.set(B.vnn[v], B.vno[v], kThinOK);
-                const uint32_t nn = ng.nn;
                 uint64_t* const D = c.D + B.doff[v];
                 const uint32_t p0 = 28u * (l8 & 1u) + 14u * ((l8 >> 1) & 1u) + 7u * ((l8 >> 2) & 1u);
 #pragma unroll
@@ -767,21 +682,7 @@ __global__ void __launch_bounds__(kThreads, KNNG_T5_CTAS) join5_kernel(GraphView
                     const uint32_t p = p0 + q;
                     if (p >= 50) break;
                     uint32_t r, cc;
-                    if (kind == kKindT) {
-                        const uint32_t x = p / kThinCols, y = p % kThinCols;
-                        if (x >= 2) continue;
-                        r = ra + x;
-                        cc = ca + y;
-                    } else {
-                        const uint32_t x = p / 10u, y = p % 10u;
-                        if (y >= 5 && !has_b) continue;
-                        r = ra + x;
-                        cc = y < 5 ? ca + y : cb + (y - 5);
-                    }
-                    // every evaluated pair exactly once, in the reference's class:
-                    // fused rows (r < fn) against new blocks j >= i or full old blocks
-                    const bool ok = kind == kKindF ? (cc >= nn || cc > r) : ng.leftover_pair(r, cc);
-                    if (!ok) continue;
+                    if (!ng.tile_pair(tile, p, r, cc)) continue;
                     const uint32_t sr = base + r, sc = base + cc;
                     const uint32_t id_r = sh.colrow[sr], id_c = sh.colrow[sc];
                     // an id listed twice pairs with itself: try_insert ignores
@@ -845,3 +746,33 @@ void launch_join5(const GraphView& g, const CandView& c, IterCounters* ctr, uint
 }
 
 }  // namespace knng_cuda
+
+// Test hook (host only, no GPU): every pair the tiles of a node with nn new and
+// no old candidates evaluate, as {row position, column position, fused} triples
+// in candidate order (new list, then old list).  Returns the number of tiles;
+// *count = the number of pairs (the first `capacity` are written).
+extern "C" int knng_cuda_debug_join5_pairs(uint32_t nn, uint32_t no, int thin, uint32_t* out,
+                                           uint32_t capacity, uint32_t* count) {
+    using namespace knng_cuda::t5;
+    Geom5 ng;
+    ng.set(nn, no, thin != 0);
+    uint32_t n_pairs = 0, n_tiles = 0;
+    auto emit = [&](uint32_t tile) {
+        ++n_tiles;
+        for (uint32_t p = 0; p < 50; ++p) {
+            uint32_t r, cc;
+            if (!ng.tile_pair(tile, p, r, cc)) continue;
+            if (n_pairs < capacity) {
+                out[3 * n_pairs] = ng.cand(r);
+                out[3 * n_pairs + 1] = ng.cand(cc);
+                out[3 * n_pairs + 2] = ((tile >> 22) & 3u) == kKindF;
+            }
+            ++n_pairs;
+        }
+    };
+    for (uint32_t t = 0; t < ng.f_tiles(); ++t) emit(ng.f_tile(0, t));
+    for (uint32_t t = 0; t < ng.u_tiles(); ++t) emit(ng.u_tile(0, t));
+    for (uint32_t t = 0; t < ng.t_tiles(); ++t) emit(ng.t_tile(0, t));
+    *count = n_pairs;
+    return int(n_tiles);
+}
