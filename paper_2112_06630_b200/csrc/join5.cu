@@ -44,7 +44,10 @@ namespace knng_cuda {
 
 namespace {
 
-constexpr uint32_t kThreads = 128;  // 16 groups of 8 lanes
+#ifndef KNNG_T5_THREADS
+#define KNNG_T5_THREADS 128
+#endif
+constexpr uint32_t kThreads = KNNG_T5_THREADS;  // 16 groups of 8 lanes
 constexpr uint32_t kGroups = kThreads / 8;
 #ifndef KNNG_T5_SLAB
 #define KNNG_T5_SLAB 32
