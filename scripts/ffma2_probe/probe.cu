@@ -183,6 +183,75 @@ void run2(const char* name, float* out, const float* in, int sms, double clock_g
            cudaGetErrorString(cudaGetLastError()));
 }
 
+// (f) two 5 x 10 tiles per thread (two accumulator sets, ~200 registers), 2 CTAs
+// per SM: what a pass of 32 tiles on 16 groups could reach -- a whole
+// iteration-1 node per pass at half the passes.
+__global__ void __launch_bounds__(128, 2) pattern_two(float* out, const float* in, int steps, float seed) {
+    extern __shared__ float smem[];
+    const int tid = threadIdx.x, l8 = tid & 7, group = tid >> 3;
+    for (int i = tid; i < 112 * kPitch; i += 128) smem[i] = in[i % 1024] + seed;
+    __syncthreads();
+    float2 acc0[25], acc1[25];
+#pragma unroll
+    for (int p = 0; p < 25; ++p) acc0[p] = acc1[p] = make_float2(0.f, 0.f);
+    const float2 m1 = make_float2(-1.f, -1.f);
+    const float* pa0 = smem + (group * 5 % 100) * kPitch + l8;
+    const float* pb0 = smem + ((group * 10 + 5) % 100) * kPitch + l8;
+    const float* pa1 = smem + ((group * 5 + 40) % 100) * kPitch + l8;
+    const float* pb1 = smem + ((group * 10 + 55) % 100) * kPitch + l8;
+    for (int s = 0; s < steps; ++s) {
+        const int o = (s & 3) * 8;
+        float a0[5], a1[5];
+        float2 b0[5], b1[5];
+#pragma unroll
+        for (int x = 0; x < 5; ++x) {
+            a0[x] = pa0[x * kPitch + o];
+            a1[x] = pa1[x * kPitch + o];
+        }
+#pragma unroll
+        for (int j = 0; j < 5; ++j) {
+            b0[j] = make_float2(pb0[(2 * j) * kPitch + o], pb0[(2 * j + 1) * kPitch + o]);
+            b1[j] = make_float2(pb1[(2 * j) * kPitch + o], pb1[(2 * j + 1) * kPitch + o]);
+        }
+#pragma unroll
+        for (int x = 0; x < 5; ++x) {
+            const float2 ax0 = make_float2(a0[x], a0[x]), ax1 = make_float2(a1[x], a1[x]);
+#pragma unroll
+            for (int j = 0; j < 5; ++j) {
+                const float2 d0 = __ffma2_rn(b0[j], m1, ax0);
+                acc0[5 * x + j] = __ffma2_rn(d0, d0, acc0[5 * x + j]);
+                const float2 d1 = __ffma2_rn(b1[j], m1, ax1);
+                acc1[5 * x + j] = __ffma2_rn(d1, d1, acc1[5 * x + j]);
+            }
+        }
+    }
+    float sum = 0.f;
+#pragma unroll
+    for (int p = 0; p < 25; ++p) sum += acc0[p].x + acc0[p].y + acc1[p].x + acc1[p].y;
+    if (sum == 12345.678f) out[0] = sum;
+}
+
+void run_two(float* out, const float* in, int sms, double clock_ghz) {
+    const int steps = 1 << 13, ctas = 2, blocks = sms * ctas, smem = 100 * 1024;
+    cudaFuncSetAttribute(pattern_two, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    for (int w = 0; w < 3; ++w) pattern_two<<<blocks, 128, smem>>>(out, in, steps, 0.5f);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    const int reps = 5;
+    for (int r = 0; r < reps; ++r) pattern_two<<<blocks, 128, smem>>>(out, in, steps, 0.5f);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double ffma2_per_smsp = 100.0 * steps * ctas * reps;
+    const double clocks = double(ms) * 1e-3 * clock_ghz * 1e9;
+    printf("{\"variant\": \"two 5 x 10 tiles per thread, load both then compute both\", \"ctas_per_sm\": %d, \"ms\": %.3f, \"ffma2_per_clk_per_smsp\": %.4f, \"frac_of_peak\": %.4f, \"err\": \"%s\"}\n",
+           ctas, ms / reps, ffma2_per_smsp / clocks, ffma2_per_smsp / clocks / 0.5,
+           cudaGetErrorString(cudaGetLastError()));
+}
+
 int main() {
     int sms = 0, khz = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -200,5 +269,6 @@ int main() {
     run2<3>("join layout, next segment loaded before this segment's arithmetic", out, in, sms, ghz, 3);
     run2<3>("join layout, next segment loaded before this segment's arithmetic", out, in, sms, ghz, 2);
     run2<4>("5 x 5 tile per 4-thread group, 10 LDS.64 per 50 FFMA2", out, in, sms, ghz);
+    run_two(out, in, sms, ghz);
     return 0;
 }
