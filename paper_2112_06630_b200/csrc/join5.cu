@@ -67,9 +67,15 @@ constexpr uint32_t kPitch = kSlab + 4;
 constexpr uint32_t kPassBlk = KNNG_T5_PASSBLK;  // 8-slot blocks one pass may stage
 constexpr uint32_t kRingRows = kPassBlk * 8;
 constexpr uint32_t kMaxBatch = 8;
-constexpr uint32_t kSlotTab = 320;  // batch slots
+#ifndef KNNG_T5_SLOTTAB
+#define KNNG_T5_SLOTTAB 320
+#endif
+constexpr uint32_t kSlotTab = KNNG_T5_SLOTTAB;  // batch slots
 constexpr uint32_t kBlkTab = kSlotTab / 8;
-constexpr uint32_t kMaxTiles = 384;
+#ifndef KNNG_T5_MAXTILES
+#define KNNG_T5_MAXTILES 384
+#endif
+constexpr uint32_t kMaxTiles = KNNG_T5_MAXTILES;
 constexpr uint32_t kDeadTile = 3u << 22;   // kind 3: padding, no work
 constexpr uint32_t kGroupEnd = 1u << 27;   // last tile of a pass group
 
