@@ -66,7 +66,11 @@ constexpr uint32_t kPitch = kSlab + 4;
 #endif
 constexpr uint32_t kPassBlk = KNNG_T5_PASSBLK;  // 8-slot blocks one pass may stage
 constexpr uint32_t kRingRows = kPassBlk * 8;
-constexpr uint32_t kMaxBatch = 8;
+#ifndef KNNG_T5_MAXBATCH
+#define KNNG_T5_MAXBATCH 8
+#endif
+constexpr uint32_t kMaxBatch = KNNG_T5_MAXBATCH;  // nodes per batch (tile descriptors hold 4 bits)
+static_assert(kMaxBatch <= 16, "node index field of a tile descriptor");
 #ifndef KNNG_T5_SLOTTAB
 #define KNNG_T5_SLOTTAB 320
 #endif
@@ -77,7 +81,7 @@ constexpr uint32_t kBlkTab = kSlotTab / 8;
 #endif
 constexpr uint32_t kMaxTiles = KNNG_T5_MAXTILES;
 constexpr uint32_t kDeadTile = 3u << 22;   // kind 3: padding, no work
-constexpr uint32_t kGroupEnd = 1u << 27;   // last tile of a pass group
+constexpr uint32_t kGroupEnd = 1u << 28;   // last tile of a pass group
 
 #ifndef KNNG_T5_ENDMIN
 #define KNNG_T5_ENDMIN 17  // off: measured no gain (C5 391 vs 388 ms with 12 vs off)
@@ -530,7 +534,7 @@ __global__ void __launch_bounds__(kThreads, KNNG_T5_CTAS) join5_kernel(GraphView
                     if (lane < left) {
                         const uint32_t tile = sh.tiles[t0 + lane];
                         if (!tile_dead(tile)) {
-                            const uint32_t v = (tile >> 24) & 7u, kind = (tile >> 22) & 3u;
+                            const uint32_t v = (tile >> 24) & 15u, kind = (tile >> 22) & 3u;
                             const uint32_t ra = tile & 127u, ca = (tile >> 7) & 127u,
                                            cb = (tile >> 14) & 127u;
                             Geom5 ng;
@@ -597,7 +601,7 @@ __global__ void __launch_bounds__(kThreads, KNNG_T5_CTAS) join5_kernel(GraphView
             const uint32_t tile0 = group < pass_len && t < n_tiles ? sh.tiles[t] : kDeadTile;
             const bool live = !tile_dead(tile0);
             const uint32_t tile = live ? tile0 : 0u;
-            const uint32_t v = (tile >> 24) & 7u, kind = (tile >> 22) & 3u;
+            const uint32_t v = (tile >> 24) & 15u, kind = (tile >> 22) & 3u;
             const uint32_t ra = tile & 127u, ca = (tile >> 7) & 127u;
             const bool has_b = (tile >> 21) & 1u;
             const uint32_t cb = has_b ? (tile >> 14) & 127u : ca;

@@ -21,8 +21,8 @@ namespace t5 {
 // tile descriptor: node-relative slots
 //   [0,7) ra   first row slot        [7,14) ca   first slot of column block A
 //   [14,21) cb first slot of column block B      [21] column block B present
-//   [22,24) kind (0 F, 1 U, 2 T, 3 dead)  [24,27) node index in the batch
-//   [27] last tile of its pass group
+//   [22,24) kind (0 F, 1 U, 2 T, 3 dead)  [24,28) node index in the batch
+//   [28] last tile of its pass group
 constexpr uint32_t kKindF = 0, kKindU = 1, kKindT = 2;
 KNNG_HD bool tile_dead(uint32_t tile) { return ((tile >> 22) & 3u) == 3u; }
 constexpr uint32_t kThinCols = 24;  // T tile: 2 rows x 24 columns
