@@ -65,3 +65,14 @@ for key in sorted(z.files, key=lambda s: int(s[1:])):
         w = h[nn, no]
         base += w * sum(cur(nn, no)[:3]); a += w * merged(nn, no, False); b += w * merged(nn, no, True)
     print(f"{name} it {key[1:]:>2}: merged {a / base:.3f}  merged+thin {b / base:.3f}")
+
+# --- the kept tiling (merged leftover rows; thin tiles for long rows): live share ---
+print("kept tiling: live share of the FMA-pipe cost (thin tiles as for long rows / off)")
+for key in sorted(z.files, key=lambda s: int(s[1:])):
+    h = z[key]; a = b = live = 0.0
+    for nn, no in zip(*np.nonzero(h)):
+        if nn == 0: continue
+        w = h[nn, no]
+        c5 = cur(nn, no)
+        live += w * (c5[3] + c5[4]); a += w * merged(nn, no, True); b += w * merged(nn, no, False)
+    print(f"{name} it {key[1:]:>2}: live {live / a:.3f} / {live / b:.3f}")
