@@ -44,6 +44,22 @@ namespace knng_cuda {
 
 namespace {
 
+#ifndef KNNG_T5_CHECKS
+#define KNNG_T5_CHECKS 0  // 1: device-side bounds checks with a message (diagnostics build)
+#endif
+#if KNNG_T5_CHECKS
+#define T5CHECK(cond, what, a, b)                                                        \
+    do {                                                                                \
+        if (!(cond)) {                                                                  \
+            printf("join5 check failed: %s (%u, %u) block %d thread %d\n", what,       \
+                   unsigned(a), unsigned(b), int(blockIdx.x), int(threadIdx.x));      \
+            __trap();                                                                   \
+        }                                                                               \
+    } while (0)
+#else
+#define T5CHECK(cond, what, a, b) ((void)0)
+#endif
+
 #ifndef KNNG_T5_THREADS
 #define KNNG_T5_THREADS 128
 #endif
@@ -518,6 +534,8 @@ __global__ void __launch_bounds__(kThreads, KNNG_T5_CTAS) join5_kernel(GraphView
             __syncwarp();
             if (lane < nv) atomicOr(&sh.tiles[gend_l], kGroupEnd);
             if (lane == 0) sh.n_tiles = nt;
+            T5CHECK(nt <= kMaxTiles, "tile list", nt, kMaxTiles);
+            T5CHECK(B.nslots <= sh.slot_budget || nv == 1, "batch slots", B.nslots, sh.slot_budget);
         }
         if (resident) cp_async_wait_pending<0>();
         __syncthreads();
@@ -635,6 +653,9 @@ __global__ void __launch_bounds__(kThreads, KNNG_T5_CTAS) join5_kernel(GraphView
                 const uint32_t oa = live ? ringpos(base + ra) * kPitch + l8 : 0u;
                 const uint32_t ob = live ? ringpos(base + ca) * kPitch + l8 : 0u;
                 const uint32_t oc = live ? ringpos(base + cb) * kPitch + l8 : 0u;
+                T5CHECK(oa / kPitch + 5 <= kRingRows + 23 && ob / kPitch + (kind == kKindT ? kThinCols : 5) <= kRingRows + 23 &&
+                            oc / kPitch + 5 <= kRingRows + 23,
+                        "ring row", ob / kPitch, oc / kPitch);
                 // kStages-deep cp.async ring, one barrier per slab; thread tid
                 // stages 16-byte chunk tid % 8 of ring rows tid / 8 + 16 q
                 constexpr uint32_t kC4 = kSlab / 4, kSweep = kThreads / kC4;
@@ -702,6 +723,17 @@ __global__ void __launch_bounds__(kThreads, KNNG_T5_CTAS) join5_kernel(GraphView
                     // self (graph.hpp:116-129)
                     if (c.filter && id_r == id_c) continue;
                     const float dist = sums[q];
+#if KNNG_T5_CHECKS
+                    {
+                        auto row_end = [&](uint32_t slot) {  // one past the row's last word
+                            const uint32_t cd = ng.cand(slot);
+                            return uint32_t(prow(cd, ng.nn, ng.m)) + (cd < ng.nn ? ng.m : ng.nn + 1u);
+                        };
+                        T5CHECK(r < ng.m && cc < ng.m && r != cc, "pair slots", r, cc);
+                        T5CHECK(sh.rowcnt[sr] < row_end(r), "row cursor", sh.rowcnt[sr], row_end(r));
+                        T5CHECK(sh.rowcnt[sc] < row_end(cc), "column cursor", sh.rowcnt[sc], row_end(cc));
+                    }
+#endif
                     if (dist < sh.colmax[sr]) D[atomicAdd(&sh.rowcnt[sr], 1u)] = pack_key(dist, id_c);
                     if (dist < sh.colmax[sc]) D[atomicAdd(&sh.rowcnt[sc], 1u)] = pack_key(dist, id_r);
                 }
